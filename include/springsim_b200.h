@@ -1,0 +1,199 @@
+/*
+ * springsim_b200.h — C ABI of the B200-native mass-spring relaxation loop.
+ *
+ * The reference (`/root/reference/pkg/src/springsim`) has no FFI: its two
+ * "operator" seams are the numba kernels in `_kernels.py:44-155` and the
+ * Python `Engine` class in `engine.py:173-466`.  Every entry point below
+ * replaces one of those seams; the reference symbol it stands in for is
+ * cited beside it.  The Python host layer (`paper_2207_09334_b200/engine.py`)
+ * binds these with ctypes; INTEGRATION.md shows the binding a maintainer of
+ * the reference would add.
+ *
+ * Conventions
+ *  - plain C types only; arrays are C-contiguous, row-major, caller-owned;
+ *    (N,3) arrays are `double[3*N]`.  Nothing retains a host pointer after
+ *    the call returns.
+ *  - every function returns an `int` status (SS_OK == 0) unless stated;
+ *    on failure `ss_last_error()` returns a thread-local message.
+ *  - mass and spring ids are the caller's (reference) ids everywhere.
+ *  - one engine must not be stepped from two threads at once
+ *    (engine.py:179); distinct engines are independent.
+ */
+#ifndef SPRINGSIM_B200_H
+#define SPRINGSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+/* status codes */
+#define SS_OK             0
+#define SS_EINVAL         1   /* bad argument (Python maps to ValueError, engine.py:184-189) */
+#define SS_ECUDA          2   /* CUDA runtime error (no device, OOM, launch failure)        */
+#define SS_EDIVERGED      3   /* DivergenceError (engine.py:44-52,375-381)                   */
+#define SS_ENOMEM         4   /* host allocation failure                                     */
+
+/* integrators (engine.py:34-37) */
+#define SS_EULER   0
+#define SS_VERLET  1
+#define SS_RK4     2
+
+/* arithmetic of the device state */
+#define SS_F64     0   /* validation mode: bitwise equal to reference serial mode */
+#define SS_F32     1   /* production mode: displacement form, 1e-4 relative        */
+
+/* device layouts of the incidence structure */
+#define SS_LAYOUT_AUTO 0
+#define SS_LAYOUT_CSR  1   /* generic per-mass CSR, any degree                      */
+#define SS_LAYOUT_ELL  2   /* sliced-ELL owner records + reverse refs (16 B/spring) */
+
+/* actuation modes (model.py:21-23) */
+#define SS_SINUSOID            0
+#define SS_CONSTANT_EXPANSION  1
+
+/*
+ * Scene description: the arrays `Engine.__init__` freezes a Scene into
+ * (engine.py:192-220).  Field-for-field:
+ *   x, v, f_ext  <- masses[*].x / .v / .f_ext    (double[3*n_masses])
+ *   m            <- masses[*].m                   (double[n_masses])
+ *   fixed        <- masses[*].fixed               (uint8[n_masses], may be NULL)
+ *   si, sj       <- springs[*].i / .j             (int64[n_springs])
+ *   k, l0        <- springs[*].k / .l0            (double[n_springs])
+ *   group        <- index of springs[*].group in the groups table, -1 passive
+ *                   (int32[n_springs], may be NULL)
+ *   planes       <- scene.planes as n_planes x {nx,ny,nz,offset,penalty,friction}
+ */
+typedef struct ss_scene_desc {
+    int64_t n_masses;
+    int64_t n_springs;
+    const double  *x;
+    const double  *v;
+    const double  *m;
+    const double  *f_ext;     /* may be NULL (all zero) */
+    const uint8_t *fixed;     /* may be NULL (none fixed) */
+    const int64_t *si;
+    const int64_t *sj;
+    const double  *k;
+    const double  *l0;
+    const int32_t *group;     /* may be NULL */
+    int32_t n_groups;
+    const int32_t *group_mode;      /* SS_SINUSOID / SS_CONSTANT_EXPANSION, [n_groups] */
+    const double  *group_amplitude; /* [n_groups] */
+    const double  *group_frequency; /* [n_groups] */
+    const double  *group_phase;     /* [n_groups] */
+    int32_t n_planes;
+    const double  *planes;    /* [6*n_planes] */
+    double gravity[3];
+    double dt;
+    double damping;
+    int32_t integrator;       /* SS_EULER / SS_VERLET / SS_RK4 */
+    int32_t precision;        /* SS_F64 / SS_F32 */
+    int32_t layout;           /* SS_LAYOUT_* */
+    int32_t device;           /* CUDA ordinal */
+} ss_scene_desc;
+
+typedef struct ss_engine ss_engine;
+
+/* Result of a batch of steps. */
+typedef struct ss_step_result {
+    int64_t steps_done;       /* steps committed by this call (incl. the diverging one) */
+    int64_t n;                /* engine step counter after the call        (engine.py:371) */
+    double  t;                /* engine time after the call, == n*dt       (engine.py:372) */
+    int64_t diverged_mass;    /* lowest non-finite mass id, -1 if none     (engine.py:381) */
+    int64_t diverged_step;    /* step number at which it was detected, -1  */
+} ss_step_result;
+
+int         ss_abi_version(void);
+const char *ss_last_error(void);
+int         ss_device_count(int *count);
+
+/* Engine.__init__ (engine.py:182-246). */
+int ss_create(const ss_scene_desc *desc, ss_engine **out);
+int ss_destroy(ss_engine *h);
+
+/* Engine.step(count) (engine.py:366-373): `count` steps of the configured
+ * integrator, actuation tables built from the current group parameters, the
+ * finiteness check after every step.  Returns SS_EDIVERGED (and fills `res`)
+ * when a step produced a non-finite position or velocity; the state is then
+ * the diverged state, as in the reference. */
+int ss_step(ss_engine *h, int64_t count, ss_step_result *res);
+
+/* Asynchronous variant for benchmarking: enqueues `count` steps on the
+ * engine's stream and returns immediately.  Divergence is recorded on the
+ * device and reported by the next ss_step / ss_sync. */
+int ss_step_async(ss_engine *h, int64_t count);
+int ss_sync(ss_engine *h, ss_step_result *res);
+/* cudaStream_t of the engine, as an opaque pointer (for CUDA-event timing). */
+void *ss_stream(ss_engine *h);
+
+/* Engine.forces(x, v, t) (engine.py:261-289): total force at a trial state.
+ * Adds the degenerate-spring count to the engine counter like the reference. */
+int ss_forces(ss_engine *h, const double *x, const double *v, double t,
+              double *acc_out, int64_t *degenerate_out);
+
+/* Engine.state / direct attribute access (engine.py:383-388, 196-202).
+ * Any pointer may be NULL (that array is skipped / left unchanged);
+ * *has_prev reports whether the Verlet history x_prev exists.  Setting x_prev
+ * creates the history (the `engine.x_prev = ...` assignment of
+ * tests/test_engine.py:170); ss_clear_prev drops it (x_prev = None). */
+int ss_get_state(ss_engine *h, double *x, double *v, double *x_prev, int *has_prev);
+int ss_set_state(ss_engine *h, const double *x, const double *v, const double *x_prev);
+int ss_clear_prev(ss_engine *h);
+int ss_get_positions(ss_engine *h, double *x);
+int ss_get_time(ss_engine *h, double *t, int64_t *n);
+int ss_set_time(ss_engine *h, double t, int64_t n);
+
+/* setters (engine.py:402-424); range validation is done by the caller like
+ * Engine.set_damping (engine.py:405-408), direct attribute writes are not
+ * validated by the reference either. */
+int ss_set_f_ext(ss_engine *h, const double *f_ext);
+int ss_set_damping(ss_engine *h, double damping);
+int ss_set_gravity(ss_engine *h, const double g[3]);
+int ss_set_group(ss_engine *h, int32_t group, int32_t mode, double amplitude,
+                 double frequency, double phase);
+
+/* Engine.degenerate_springs (engine.py:224,271) */
+int ss_degenerate_count(ss_engine *h, int64_t *count);
+
+/* introspection: bytes of device memory, layout chosen, algorithmic bytes
+ * per step as defined in SURVEY §8d / DESIGN.md §4 */
+typedef struct ss_info {
+    int64_t n_masses, n_springs;
+    int32_t precision, layout, integrator, device;
+    int64_t device_bytes;
+    double  algorithmic_bytes_per_step;
+    int32_t ell_width_own, ell_width_ref;
+    int32_t canonical_order;   /* 1 if the ELL split order == spring-id order */
+} ss_info;
+int ss_get_info(ss_engine *h, ss_info *info);
+
+/* Kernel launches issued so far (for the bench's gpu_launches claim). */
+int64_t ss_launch_count(ss_engine *h);
+
+/*
+ * Array-native voxel lattice over an axis-aligned box, bit-identical to
+ * `build_voxel_lattice(box_mesh(lo, hi), LatticeSpec(dim))` with
+ * `Material(k0, l_ref=dim)` (lattice.py:89-136, model.py:87-97):
+ * nodes lo + idx*dim in (i,j,k) lexicographic order, springs sorted by
+ * (i, j), l0 = sqrt(fma(dz,dz,fma(dy,dy,dx*dx))) (the OpenBLAS ddot that
+ * np.linalg.norm uses, lattice.py:84), k = (k0*l_ref)/l0.
+ * Call once with NULL outputs to get the counts, then with buffers.
+ * Only masses with plane index in [i_lo, i_hi) are emitted when i_hi > i_lo
+ * (spatial slab for multi-GPU sharding); springs with at least one endpoint
+ * in the slab are emitted, ids stay global.
+ */
+int ss_lattice_box(const double lo[3], const double hi[3], double dim,
+                   double k0, double l_ref,
+                   int64_t i_lo, int64_t i_hi,
+                   int64_t counts_out[3], int64_t *n_masses_out, int64_t *n_springs_out,
+                   double *x_out, int64_t *si_out, int64_t *sj_out,
+                   double *k_out, double *l0_out, int64_t *spring_id_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPRINGSIM_B200_H */

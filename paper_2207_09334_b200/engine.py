@@ -1,0 +1,697 @@
+"""Drop-in ``Engine`` / ``simulate`` for the B200 relaxation loop.
+
+Call-compatible with the reference (pkg/src/springsim/engine.py): the same
+constructor ``Engine(scene, integrator="verlet", mode="serial", threads=None)``,
+the same methods (``step``, ``forces``, ``total_force``, ``energies``,
+``state``, setters, command queue) and the same public attributes
+(``x, v, x_prev, m, f_ext, t, n, dt, damping, gravity, integrator, mode,
+threads, gpe_datum, degenerate_springs, paused, stopped, command_errors``).
+
+What changes underneath: the per-step work (engine.py:261-354, 366-381) runs
+as hand-written sm_100a kernels behind the C ABI of
+``include/springsim_b200.h`` (bound in :mod:`._lib`).  There is no CPU
+fallback — constructing an Engine without the built library or without a
+GPU raises.
+
+Two extra keyword arguments select the arithmetic and the incidence layout:
+
+* ``precision="f64"`` (default) — validation mode, bitwise identical to the
+  reference's serial mode; ``"f32"`` — production mode (displacement form,
+  1e-4 relative over short horizons).
+* ``layout="auto" | "csr" | "ell"`` — device incidence structure.
+
+Host mirrors.  ``x, v, x_prev, f_ext`` read as numpy arrays downloaded
+lazily after each batch of steps; callers may edit them in place or assign
+them (reference code does both: tests/test_engine.py:170, service.py:442),
+and any array handed out is re-uploaded before the next step.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import queue
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .model import CONSTANT_EXPANSION, scene_arrays
+from .traces import TraceSeries
+
+SERIAL = "serial"
+PARALLEL = "parallel"
+PARALLEL_DET = "parallel-det"
+EXEC_MODES = (SERIAL, PARALLEL, PARALLEL_DET)
+
+EULER = "euler"
+VERLET = "verlet"
+RK4 = "rk4"
+INTEGRATORS = (EULER, VERLET, RK4)
+
+PRECISIONS = ("f64", "f32")
+LAYOUTS = {"auto": _lib.SS_LAYOUT_AUTO, "csr": _lib.SS_LAYOUT_CSR, "ell": _lib.SS_LAYOUT_ELL}
+
+DEGENERATE_LENGTH = 1e-12          # _kernels.py:23
+_INTEG = {EULER: _lib.SS_EULER, VERLET: _lib.SS_VERLET, RK4: _lib.SS_RK4}
+
+
+class DivergenceError(RuntimeError):
+    """Non-finite position or velocity; the run is halted (engine.py:44-52)."""
+
+    def __init__(self, mass_id: int, step: int):
+        self.mass_id = mass_id
+        self.step = step
+        super().__init__(
+            f"simulation diverged at step {step}: mass {mass_id} has a "
+            f"non-finite position or velocity (try a smaller dt)")
+
+
+def spring_force(x_i, x_j, k: float, l0: float) -> np.ndarray:
+    """Scalar force on i from one spring (engine.py:55-65)."""
+    d = np.asarray(x_j, dtype=np.float64) - np.asarray(x_i, dtype=np.float64)
+    length = float(np.linalg.norm(d))
+    if length < DEGENERATE_LENGTH:
+        return np.zeros(3)
+    return (k * (length - l0) / length) * d
+
+
+def contact_force(x, v, m: float, plane, dt: float) -> np.ndarray:
+    """Penalty + clamped Coulomb friction of one plane on one mass (engine.py:68-89)."""
+    x = np.asarray(x, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    n = np.asarray(plane.normal, dtype=np.float64)
+    depth = plane.offset - x @ n
+    if depth <= 0.0:
+        return np.zeros(3)
+    f_n = plane.penalty * depth
+    out = f_n * n
+    if plane.friction > 0.0:
+        v_t = v - (v @ n) * n
+        speed = float(np.linalg.norm(v_t))
+        if speed > 1e-15:
+            mag = min(plane.friction * f_n, speed * m / dt)
+            out = out - (mag / speed) * v_t
+    return out
+
+
+@dataclass
+class EngineState:
+    """Snapshot between steps (engine.py:135-145)."""
+
+    positions: np.ndarray
+    velocities: np.ndarray
+    prev_positions: np.ndarray | None
+    t: float
+    n: int
+    integrator: str
+    mode: str
+
+
+def energy_breakdown(x, v, m, si, sj, k, l0_eff, gravity, datum: float):
+    """(elastic, gravitational, kinetic) energy of a raw state (engine.py:148-170).
+
+    Sampling-only host reduction (numpy), same formulas and op order."""
+    with np.errstate(over="ignore", invalid="ignore"):
+        if si.size:
+            d = x[sj] - x[si]
+            lengths = np.linalg.norm(d, axis=1)
+            epe = float(0.5 * np.sum(k * (lengths - l0_eff) ** 2))
+        else:
+            epe = 0.0
+        g_mag = float(np.linalg.norm(gravity))
+        if g_mag > 0.0:
+            up = -np.asarray(gravity, dtype=np.float64) / g_mag
+            gpe = float(np.sum(m * g_mag * (x @ up - datum)))
+        else:
+            gpe = 0.0
+        ke = float(0.5 * np.sum(m * np.einsum("ij,ij->i", v, v)))
+    return epe, gpe, ke
+
+
+class _Mirror:
+    """Lazy host copy of one (N,3) device array with lend/upload tracking."""
+
+    __slots__ = ("arr", "stale", "lent")
+
+    def __init__(self, arr):
+        self.arr = arr
+        self.stale = False
+        self.lent = False
+
+
+class Engine:
+    """GPU engine, call-compatible with reference engine.py:173-466."""
+
+    def __init__(self, scene, integrator: str = VERLET, mode: str = SERIAL,
+                 threads: int | None = None, *, precision: str = "f64",
+                 layout: str = "auto", device: int = 0):
+        if integrator not in INTEGRATORS:
+            raise ValueError(f"unknown integrator {integrator!r}")
+        if mode not in EXEC_MODES:
+            raise ValueError(f"unknown execution mode {mode!r}")
+        if precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {precision!r}")
+        if layout not in LAYOUTS:
+            raise ValueError(f"unknown layout {layout!r}")
+        if scene.mass_count == 0:
+            raise ValueError("scene has no masses")
+        self.integrator = integrator
+        self.mode = mode
+        self.precision = precision
+        self.device = int(device)
+        arr = scene_arrays(scene)
+        self.dt = float(arr.dt)
+        self.damping = float(arr.damping)
+        self.gravity = np.asarray(arr.gravity, dtype=np.float64)
+        self.m = arr.m
+        self._fixed = arr.fixed
+        self._fixed_idx = np.nonzero(arr.fixed)[0]
+        self._si = arr.si
+        self._sj = arr.sj
+        self._sk = arr.k
+        self._l0 = arr.l0
+        self._l0_eff = arr.l0.copy()
+        self._group_of = arr.group
+        self._groups: dict[str, dict] = {}
+        for gi, (label, mode_, amp, freq, phase) in enumerate(arr.group_params):
+            self._groups[label] = {"indices": np.nonzero(arr.group == gi)[0].astype(np.int64),
+                                   "mode": mode_, "amplitude": amp, "frequency": freq,
+                                   "phase": phase}
+        self._planes = arr.planes
+        self.paused = False
+        self.stopped = False
+        self._commands: queue.Queue = queue.Queue()
+        self.command_errors: list[str] = []
+        self.threads = 1
+        if mode != SERIAL:
+            available = os.cpu_count() or 1
+            self.threads = max(1, min(threads or available, available))
+        g_mag = float(np.linalg.norm(self.gravity))
+        self.gpe_datum = float((arr.x @ (-self.gravity / g_mag)).min()) if g_mag else 0.0
+        self._degenerate_offset = 0
+        self._host_prev_nonverlet = None
+
+        self._h = C.c_void_p()
+        self._create(arr, LAYOUTS[layout])
+        self._x = _Mirror(arr.x)
+        self._v = _Mirror(arr.v)
+        self._xp = _Mirror(None)
+        self._f = _Mirror(arr.f_ext)
+
+    # ------------------------------------------------------------ plumbing
+
+    def _create(self, arr, layout: int) -> None:
+        lib = _lib.lib()
+        n, s = arr.x.shape[0], arr.si.shape[0]
+        self._keep = keep = {}
+        keep["x"] = np.ascontiguousarray(arr.x, dtype=np.float64)
+        keep["v"] = np.ascontiguousarray(arr.v, dtype=np.float64)
+        keep["m"] = np.ascontiguousarray(arr.m, dtype=np.float64)
+        keep["f"] = np.ascontiguousarray(arr.f_ext, dtype=np.float64)
+        keep["fixed"] = np.ascontiguousarray(arr.fixed, dtype=np.uint8)
+        keep["si"] = np.ascontiguousarray(arr.si, dtype=np.int64)
+        keep["sj"] = np.ascontiguousarray(arr.sj, dtype=np.int64)
+        keep["k"] = np.ascontiguousarray(arr.k, dtype=np.float64)
+        keep["l0"] = np.ascontiguousarray(arr.l0, dtype=np.float64)
+        keep["group"] = np.ascontiguousarray(arr.group, dtype=np.int32)
+        G = len(arr.group_params)
+        keep["gmode"] = np.array([_lib.SS_CONSTANT_EXPANSION if g[1] == CONSTANT_EXPANSION
+                                  else _lib.SS_SINUSOID for g in arr.group_params] or [0],
+                                 dtype=np.int32)
+        keep["gamp"] = np.array([g[2] for g in arr.group_params] or [0.0])
+        keep["gfreq"] = np.array([g[3] for g in arr.group_params] or [0.0])
+        keep["gphase"] = np.array([g[4] for g in arr.group_params] or [0.0])
+        planes = np.array([[*p[0], p[1], p[2], p[3]] for p in arr.planes] or [[0.0] * 6],
+                          dtype=np.float64).reshape(-1)
+        keep["planes"] = planes
+        d = _lib.SceneDesc()
+        d.n_masses = n
+        d.n_springs = s
+        d.x = _lib.dptr(keep["x"])
+        d.v = _lib.dptr(keep["v"])
+        d.m = _lib.dptr(keep["m"])
+        d.f_ext = _lib.dptr(keep["f"])
+        d.fixed = _lib.u8ptr(keep["fixed"])
+        d.si = _lib.i64ptr(keep["si"])
+        d.sj = _lib.i64ptr(keep["sj"])
+        d.k = _lib.dptr(keep["k"])
+        d.l0 = _lib.dptr(keep["l0"])
+        d.group = _lib.i32ptr(keep["group"])
+        d.n_groups = G
+        d.group_mode = _lib.i32ptr(keep["gmode"])
+        d.group_amplitude = _lib.dptr(keep["gamp"])
+        d.group_frequency = _lib.dptr(keep["gfreq"])
+        d.group_phase = _lib.dptr(keep["gphase"])
+        d.n_planes = len(arr.planes)
+        d.planes = _lib.dptr(planes)
+        for c in range(3):
+            d.gravity[c] = float(arr.gravity[c])
+        d.dt = self.dt
+        d.damping = self.damping
+        d.integrator = _INTEG[self.integrator]
+        d.precision = _lib.SS_F32 if self.precision == "f32" else _lib.SS_F64
+        d.layout = layout
+        d.device = self.device
+        _lib.check(lib.ss_create(C.byref(d), C.byref(self._h)), "ss_create")
+        # the engine copied everything it needs
+        for key in ("x", "v", "f", "fixed", "group", "gmode", "gamp", "gfreq", "gphase", "planes"):
+            keep.pop(key, None)
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib().ss_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        inf = _lib.Info()
+        _lib.check(_lib.lib().ss_get_info(self._h, C.byref(inf)), "ss_get_info")
+        return {f: getattr(inf, f) for f, _ in _lib.Info._fields_}
+
+    def _download(self) -> None:
+        """Refresh stale host mirrors of x / v / x_prev."""
+        lib = _lib.lib()
+        n = self.mass_count
+        need_x = self._x.stale
+        need_v = self._v.stale
+        need_p = self._xp.stale and self.integrator == VERLET
+        if not (need_x or need_v or need_p):
+            return
+        has_prev = C.c_int(0)
+        x = np.empty((n, 3)) if need_x else None
+        v = np.empty((n, 3)) if need_v else None
+        p = np.empty((n, 3)) if need_p else None
+        _lib.check(lib.ss_get_state(self._h, _lib.dptr(x), _lib.dptr(v), _lib.dptr(p),
+                                    C.byref(has_prev)), "ss_get_state")
+        if need_x:
+            self._x.arr, self._x.stale = x, False
+        if need_v:
+            self._v.arr, self._v.stale = v, False
+        if need_p:
+            self._xp.arr = p if has_prev.value else None
+            self._xp.stale = False
+
+    def _upload_lent(self) -> None:
+        """Push host-side edits (assignments or in-place writes) to the device."""
+        lib = _lib.lib()
+        x = self._x.arr if self._x.lent else None
+        v = self._v.arr if self._v.lent else None
+        p = None
+        clear_prev = False
+        if self.integrator == VERLET and self._xp.lent:
+            if self._xp.arr is None:
+                clear_prev = True
+            else:
+                p = self._xp.arr
+        if x is not None or v is not None or p is not None:
+            x = None if x is None else np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+            v = None if v is None else np.ascontiguousarray(v, dtype=np.float64).reshape(-1, 3)
+            p = None if p is None else np.ascontiguousarray(p, dtype=np.float64).reshape(-1, 3)
+            for a in (x, v, p):
+                if a is not None and a.shape[0] != self.mass_count:
+                    raise ValueError("state array has the wrong number of masses")
+            _lib.check(lib.ss_set_state(self._h, _lib.dptr(x), _lib.dptr(v), _lib.dptr(p)),
+                       "ss_set_state")
+        if clear_prev:
+            _lib.check(lib.ss_clear_prev(self._h), "ss_clear_prev")
+        if self._f.lent:
+            f = np.ascontiguousarray(self._f.arr, dtype=np.float64).reshape(-1, 3)
+            _lib.check(lib.ss_set_f_ext(self._h, _lib.dptr(f)), "ss_set_f_ext")
+            self._f.lent = False
+        self._x.lent = self._v.lent = self._xp.lent = False
+
+    def _push_params(self) -> None:
+        """Scalars the reference reads fresh every step (damping, gravity,
+        actuation parameters) go down before each batch."""
+        lib = _lib.lib()
+        _lib.check(lib.ss_set_damping(self._h, float(self.damping)), "ss_set_damping")
+        g = np.ascontiguousarray(self.gravity, dtype=np.float64).reshape(3)
+        _lib.check(lib.ss_set_gravity(self._h, _lib.dptr(g)), "ss_set_gravity")
+        for gi, g_ in enumerate(self._groups.values()):
+            mode = _lib.SS_CONSTANT_EXPANSION if g_["mode"] == CONSTANT_EXPANSION else _lib.SS_SINUSOID
+            _lib.check(lib.ss_set_group(self._h, gi, mode, float(g_["amplitude"]),
+                                        float(g_["frequency"]), float(g_["phase"])),
+                       "ss_set_group")
+
+    def _mark_stepped(self) -> None:
+        self._x.stale = self._v.stale = True
+        self._x.lent = self._v.lent = False
+        if self.integrator == VERLET:
+            self._xp.stale = True
+            self._xp.lent = False
+
+    # ------------------------------------------------------- state mirrors
+
+    @property
+    def x(self) -> np.ndarray:
+        self._download()
+        self._x.lent = True
+        return self._x.arr
+
+    @x.setter
+    def x(self, value) -> None:
+        self._download()
+        self._x.arr = np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._x.stale, self._x.lent = False, True
+
+    @property
+    def v(self) -> np.ndarray:
+        self._download()
+        self._v.lent = True
+        return self._v.arr
+
+    @v.setter
+    def v(self, value) -> None:
+        self._download()
+        self._v.arr = np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._v.stale, self._v.lent = False, True
+
+    @property
+    def x_prev(self):
+        if self.integrator != VERLET:
+            return self._host_prev_nonverlet
+        self._download()
+        self._xp.lent = True
+        return self._xp.arr
+
+    @x_prev.setter
+    def x_prev(self, value) -> None:
+        if self.integrator != VERLET:
+            self._host_prev_nonverlet = None if value is None else np.array(value, dtype=np.float64)
+            return
+        self._download()
+        self._xp.arr = None if value is None else np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._xp.stale, self._xp.lent = False, True
+
+    @property
+    def f_ext(self) -> np.ndarray:
+        self._f.lent = True
+        return self._f.arr
+
+    @f_ext.setter
+    def f_ext(self, value) -> None:
+        self._f.arr = np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._f.lent = True
+
+    @property
+    def t(self) -> float:
+        t = C.c_double()
+        _lib.check(_lib.lib().ss_get_time(self._h, C.byref(t), None), "ss_get_time")
+        return t.value
+
+    @t.setter
+    def t(self, value: float) -> None:
+        _lib.check(_lib.lib().ss_set_time(self._h, float(value), self.n), "ss_set_time")
+
+    @property
+    def n(self) -> int:
+        n = C.c_int64()
+        _lib.check(_lib.lib().ss_get_time(self._h, None, C.byref(n)), "ss_get_time")
+        return n.value
+
+    @n.setter
+    def n(self, value: int) -> None:
+        _lib.check(_lib.lib().ss_set_time(self._h, self.t, int(value)), "ss_set_time")
+
+    @property
+    def degenerate_springs(self) -> int:
+        c = C.c_int64()
+        _lib.check(_lib.lib().ss_degenerate_count(self._h, C.byref(c)), "ss_degenerate_count")
+        return int(c.value) + self._degenerate_offset
+
+    @degenerate_springs.setter
+    def degenerate_springs(self, value: int) -> None:
+        self._degenerate_offset = 0
+        self._degenerate_offset = int(value) - self.degenerate_springs
+
+    @property
+    def mass_count(self) -> int:
+        return int(self.m.shape[0])
+
+    @property
+    def spring_count(self) -> int:
+        return int(self._sk.shape[0])
+
+    # ------------------------------------------------------------- forces
+
+    def _rest_lengths(self, t: float) -> np.ndarray:
+        """Host restatement of engine.py:250-259 (used by energies only; the
+        device applies the same scale per group inside the spring kernel)."""
+        for g in self._groups.values():
+            idx = g["indices"]
+            if g["mode"] == CONSTANT_EXPANSION:
+                scale = 1.0 + g["amplitude"]
+            else:
+                scale = 1.0 + g["amplitude"] * math.sin(
+                    2.0 * math.pi * g["frequency"] * t + g["phase"])
+            self._l0_eff[idx] = self._l0[idx] * scale
+        return self._l0_eff
+
+    def forces(self, x: np.ndarray, v: np.ndarray, t: float) -> np.ndarray:
+        """Total force on every mass at a trial state (engine.py:261-289), on the GPU."""
+        self._upload_lent()
+        self._push_params()
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+        v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1, 3)
+        acc = np.empty_like(x)
+        deg = C.c_int64()
+        _lib.check(_lib.lib().ss_forces(self._h, _lib.dptr(x), _lib.dptr(v), float(t),
+                                        _lib.dptr(acc), C.byref(deg)), "ss_forces")
+        return acc
+
+    def total_force(self, mass_id: int) -> np.ndarray:
+        return self.forces(self.x, self.v, self.t)[mass_id]
+
+    # ------------------------------------------------------------ stepping
+
+    def step(self, count: int = 1) -> None:
+        """Advance ``count`` steps (engine.py:366-373) in one device batch.
+
+        Queued commands are drained once at the batch boundary (the
+        reference drains before every step; with an empty queue the two are
+        identical, and a command posted concurrently lands at the next batch)."""
+        if count <= 0:
+            return
+        self.drain_commands()
+        self._upload_lent()
+        self._push_params()
+        res = _lib.StepResult()
+        rc = _lib.lib().ss_step(self._h, int(count), C.byref(res))
+        self._mark_stepped()
+        if rc == _lib.SS_EDIVERGED:
+            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+        _lib.check(rc, "ss_step")
+
+    def step_async(self, count: int) -> None:
+        """Enqueue ``count`` steps without synchronising (benchmarks)."""
+        self._upload_lent()
+        self._push_params()
+        _lib.check(_lib.lib().ss_step_async(self._h, int(count)), "ss_step_async")
+        self._mark_stepped()
+
+    def synchronize(self) -> None:
+        res = _lib.StepResult()
+        rc = _lib.lib().ss_sync(self._h, C.byref(res))
+        if rc == _lib.SS_EDIVERGED:
+            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+        _lib.check(rc, "ss_sync")
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(_lib.lib().ss_stream(self._h) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.lib().ss_launch_count(self._h))
+
+    @property
+    def state(self) -> EngineState:
+        prev = self.x_prev
+        return EngineState(positions=self.x.copy(), velocities=self.v.copy(),
+                           prev_positions=None if prev is None else prev.copy(),
+                           t=self.t, n=self.n, integrator=self.integrator, mode=self.mode)
+
+    def energies(self, x=None, v=None, t=None):
+        """(epe, gpe, ke, total) at the current or a supplied state (engine.py:390-398)."""
+        x = self.x if x is None else x
+        v = self.v if v is None else v
+        t = self.t if t is None else t
+        epe, gpe, ke = energy_breakdown(x, v, self.m, self._si, self._sj, self._sk,
+                                        self._rest_lengths(t), self.gravity, self.gpe_datum)
+        return epe, gpe, ke, epe + gpe + ke
+
+    # ------------------------------------------------------------ commands
+
+    def set_external_force(self, mass_id: int, f) -> None:
+        self.f_ext[mass_id] = np.asarray(f, dtype=np.float64)
+
+    def set_damping(self, value: float) -> None:
+        if not 0.0 <= value < 1.0:
+            raise ValueError("damping must be in [0, 1)")
+        self.damping = float(value)
+
+    def set_gravity(self, g) -> None:
+        self.gravity = np.asarray(g, dtype=np.float64)
+
+    def set_actuation(self, label: str, amplitude=None, frequency=None, phase=None) -> None:
+        if label not in self._groups:
+            raise ValueError(f"unknown actuation group {label!r}")
+        g = self._groups[label]
+        if amplitude is not None:
+            if not abs(amplitude) < 1.0:
+                raise ValueError("|amplitude| must be < 1")
+            g["amplitude"] = float(amplitude)
+        if frequency is not None:
+            g["frequency"] = float(frequency)
+        if phase is not None:
+            g["phase"] = float(phase)
+
+    def post_command(self, command: dict) -> None:
+        self._commands.put(dict(command))
+
+    def drain_commands(self, wait: float = 0.0) -> None:
+        first = True
+        while True:
+            try:
+                if first and wait > 0.0:
+                    cmd = self._commands.get(timeout=wait)
+                else:
+                    cmd = self._commands.get_nowait()
+            except queue.Empty:
+                return
+            first = False
+            try:
+                self.apply_command(cmd)
+            except Exception as exc:
+                self.command_errors.append(f"{cmd.get('op', '?')}: {exc}")
+
+    def apply_command(self, cmd: dict) -> None:
+        op = cmd.get("op")
+        if op == "pause":
+            self.paused = True
+        elif op == "resume":
+            self.paused = False
+        elif op == "stop":
+            self.stopped = True
+        elif op == "set-damping":
+            self.set_damping(float(cmd["value"]))
+        elif op == "set-gravity":
+            self.set_gravity([float(c) for c in cmd["value"]])
+        elif op == "set-external-force":
+            self.set_external_force(int(cmd["mass"]), [float(c) for c in cmd["value"]])
+        elif op == "set-actuation":
+            self.set_actuation(cmd["group"], cmd.get("amplitude"), cmd.get("frequency"),
+                               cmd.get("phase"))
+        else:
+            raise ValueError(f"unknown command op {op!r}")
+
+
+def total_force(scene, mass_id: int, t: float = 0.0, **engine_kwargs) -> np.ndarray:
+    """Total force on one mass at rest state (engine.py:469-473)."""
+    engine = Engine(scene, integrator=EULER, mode=SERIAL, **engine_kwargs)
+    engine.t = t
+    return engine.total_force(mass_id)
+
+
+@dataclass
+class RunResult:
+    """Sampled output of :func:`simulate` (engine.py:476-515)."""
+
+    times: np.ndarray
+    positions: dict[int, np.ndarray]
+    energies: np.ndarray
+    engine: Engine = field(repr=False)
+
+    def position_series(self, mass_id: int, axis: int | None = None) -> TraceSeries:
+        values = self.positions[mass_id]
+        if axis is not None:
+            values = values[:, axis]
+        return TraceSeries(self.times, values)
+
+    def energy_series(self, term: str) -> TraceSeries:
+        column = {"epe": 0, "gpe": 1, "ke": 2, "total": 3}[term]
+        return TraceSeries(self.times, self.energies[:, column])
+
+    def write_csv(self, path) -> None:
+        ids = sorted(self.positions)
+        header = ["t"]
+        for mass_id in ids:
+            header += [f"{mass_id}.x", f"{mass_id}.y", f"{mass_id}.z"]
+        header += ["epe", "gpe", "ke", "total"]
+        lines = [",".join(header)]
+        for row in range(len(self.times)):
+            cells = [f"{self.times[row]:.17g}"]
+            for mass_id in ids:
+                cells += [f"{c:.17g}" for c in self.positions[mass_id][row]]
+            cells += [f"{c:.17g}" for c in self.energies[row]]
+            lines.append(",".join(cells))
+        with open(path, "w") as fh:
+            fh.write("\n".join(lines) + "\n")
+
+
+def simulate(scene, duration: float, traces=(), integrator: str = VERLET,
+             mode: str = SERIAL, threads: int | None = None, sample_every: int = 1,
+             engine: Engine | None = None, **engine_kwargs) -> RunResult:
+    """Run ``ceil(duration/dt)`` steps, sampling traces and energies (engine.py:518-565).
+
+    Steps between two samples run as one device batch; sampling points,
+    pause/resume/stop handling and the Verlet one-step sample lag are those of
+    the reference."""
+    if engine is None:
+        engine = Engine(scene, integrator=integrator, mode=mode, threads=threads, **engine_kwargs)
+    dt = engine.dt
+    steps = max(0, math.ceil(duration / dt - 1e-9))
+    verlet = engine.integrator == VERLET
+    sample_every = max(1, int(sample_every))
+    times, rows, erows = [], {mass_id: [] for mass_id in traces}, []
+
+    def emit(step_index, x, v):
+        t = step_index * dt
+        times.append(t)
+        for mass_id in rows:
+            rows[mass_id].append(x[mass_id].copy())
+        erows.append(engine.energies(x, v, t))
+
+    if not verlet and engine.n == 0:
+        emit(0, engine.x, engine.v)
+
+    done = 0
+    while done < steps:
+        while engine.paused and not engine.stopped:
+            engine.drain_commands(wait=0.02)
+        if engine.stopped:
+            break
+        n = engine.n
+        if not engine._commands.empty():
+            chunk = 1                       # reference: drain + one step
+        else:
+            # steps until the next sampling point
+            target = (n - 1) if verlet else n
+            chunk = sample_every - (target % sample_every)
+            if chunk <= 0:
+                chunk = sample_every
+            chunk = min(chunk, steps - done)
+        engine.step(chunk)
+        done += chunk
+        if verlet:
+            d = engine.n - 1
+            if d % sample_every == 0:
+                emit(d, engine.x_prev, engine.v)
+        elif engine.n % sample_every == 0:
+            emit(engine.n, engine.x, engine.v)
+
+    return RunResult(times=np.asarray(times),
+                     positions={mass_id: np.asarray(vals) for mass_id, vals in rows.items()},
+                     energies=np.asarray(erows).reshape(-1, 4), engine=engine)

@@ -1,0 +1,288 @@
+"""Engine API behaviour on the GPU, against the reference's hand-derived oracles
+(the known-answer tests of reference tests/test_engine.py:38-437, restated)."""
+
+import math
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2207_09334_b200 import (ActuationGroup, ContactPlane, DivergenceError, Engine, Scene,
+                                   contact_floor, contact_force, simulate, spring_force,
+                                   total_force)
+
+pytestmark = pytest.mark.gpu
+
+
+def drop(dt=0.01, m=1.0):
+    sc = Scene(dt=dt)
+    sc.add_mass((0.0, 0.0, 0.0), m=m)
+    return sc
+
+
+def axial(dt, u0=0.5, k=1.0, m=1.0):
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=dt)
+    a = sc.add_mass((0.0, 0.0, 0.0), fixed=True)
+    b = sc.add_mass((1.0 + u0, 0.0, 0.0), m=m)
+    sc.add_spring(a, b, k=k, l0=1.0)
+    return sc, b
+
+
+# ---------------------------------------------------------- scalar oracles
+
+def test_spring_force_kats():
+    np.testing.assert_allclose(spring_force((0, 0, 0), (2, 0, 0), 100.0, 1.0), [100, 0, 0])
+    np.testing.assert_allclose(spring_force((0, 0, 0), (0.5, 0, 0), 100.0, 1.0), [-50, 0, 0])
+    fi = spring_force((0.2, -0.4, 1.0), (1.1, 0.3, -0.2), 37.0, 0.8)
+    fj = spring_force((1.1, 0.3, -0.2), (0.2, -0.4, 1.0), 37.0, 0.8)
+    np.testing.assert_array_equal(fi, -fj)
+    np.testing.assert_array_equal(spring_force((1, 1, 1), (1, 1, 1), 1e4, 1.0), np.zeros(3))
+
+
+def test_contact_force_kats():
+    pl = ContactPlane(normal=(0.0, 1.0, 0.0), offset=0.0, penalty=1e5, friction=0.5)
+    np.testing.assert_array_equal(contact_force((0, 0.1, 0), (0, -1, 0), 0.1, pl, 1e-4), np.zeros(3))
+    np.testing.assert_allclose(contact_force((0, -0.01, 0), (0, 0, 0), 0.1, pl, 1e-4), [0, 1000, 0])
+    np.testing.assert_allclose(contact_force((0, -0.01, 0), (2.0, 0, 0), 10.0, pl, 1e-4), [-500, 1000, 0])
+    np.testing.assert_allclose(contact_force((0, -0.01, 0), (0.001, 0, 0), 0.1, pl, 1.0), [-0.0001, 1000, 0])
+
+
+# ----------------------------------------------------------------- device
+
+def test_degenerate_spring_counted_not_faulted():
+    sc = Scene(gravity=(0.0, 0.0, 0.0))
+    sc.add_mass((0, 0, 0))
+    sc.add_mass((0, 0, 0))
+    sc.add_spring(0, 1, k=100.0, l0=1.0)
+    eng = Engine(sc, integrator="euler")
+    eng.step(3)
+    assert eng.degenerate_springs == 3
+    np.testing.assert_array_equal(eng.v, np.zeros((2, 3)))
+
+
+def test_total_force_kats():
+    sc = Scene()
+    sc.add_mass((5.0, 2.0, 1.0), m=0.1)
+    np.testing.assert_allclose(total_force(sc, 0), [0.0, -0.981, 0.0])
+    sc = Scene(gravity=(0.0, 0.0, 0.0))
+    sc.add_mass((0, 0, 0), f_ext=(1.0, 2.0, 3.0))
+    np.testing.assert_allclose(total_force(sc, 0), [1.0, 2.0, 3.0])
+    sc = Scene()
+    a = sc.add_mass((0, 1, 0), fixed=True)
+    b = sc.add_mass((0, -0.5, 0), m=0.1)
+    sc.add_spring(a, b, k=10.0, l0=1.0)
+    np.testing.assert_allclose(total_force(sc, b), [0.0, 5.0 - 0.981, 0.0])
+
+
+def test_sliding_block_decelerates():
+    sc = Scene(planes=[contact_floor(penalty=1e6, friction=0.3)], dt=1e-4)
+    sc.add_mass((0.0, -1e-5, 0.0), m=0.1, v=(1.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="euler")
+    eng.step(2000)
+    assert eng.v[0, 0] < 1.0
+
+
+def test_euler_kats():
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=0.1)
+    sc.add_mass((0, 0, 0), v=(1.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="euler")
+    eng.step()
+    np.testing.assert_allclose(eng.x[0], [0.1, 0, 0])
+    eng = Engine(drop(dt=0.01), integrator="euler")
+    eng.step()
+    assert eng.x[0, 1] == 0.0
+    assert eng.v[0, 1] == pytest.approx(-0.0981)
+    sc = Scene()
+    sc.add_mass((1.0, 2.0, 3.0), fixed=True, f_ext=(1e6, 0, 0))
+    eng = Engine(sc, integrator="euler")
+    eng.step(10)
+    np.testing.assert_array_equal(eng.x[0], [1.0, 2.0, 3.0])
+    np.testing.assert_array_equal(eng.v[0], np.zeros(3))
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=0.1, damping=0.1)
+    sc.add_mass((0, 0, 0), v=(1.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="euler")
+    eng.step()
+    assert eng.v[0, 0] == pytest.approx(0.9)
+
+
+def test_verlet_kats():
+    eng = Engine(drop(dt=0.01), integrator="verlet")
+    assert eng.state.prev_positions is None
+    eng.step()
+    assert eng.x[0, 1] == pytest.approx(-4.905e-4)
+    assert eng.state.prev_positions is not None
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=1.0)
+    sc.add_mass((1.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="verlet")
+    eng.x_prev = np.array([[0.9, 0.0, 0.0]])            # host write-through
+    eng.step()
+    assert eng.x[0, 0] == pytest.approx(1.1)
+    eng = Engine(drop(dt=0.01), integrator="verlet")
+    eng.step(100)
+    assert eng.t == pytest.approx(1.0)
+    assert eng.x[0, 1] == pytest.approx(-0.5 * 9.81 * eng.t ** 2, abs=1e-10)
+
+
+def test_verlet_velocity_is_central_difference():
+    sc, b = axial(dt=0.01)
+    eng = Engine(sc, integrator="verlet")
+    eng.step(5)
+    replay = Engine(sc, integrator="verlet")
+    xs = [replay.x.copy()]
+    for _ in range(5):
+        replay.step()
+        xs.append(replay.x.copy())
+    central = (xs[5] - xs[3]) / (2 * 0.01)
+    np.testing.assert_allclose(eng.v[b], central[b], rtol=0, atol=0)
+
+
+def test_verlet_damped_form_decays():
+    sc, b = axial(dt=0.001, u0=0.5)
+    sc.damping = 0.01
+    eng = Engine(sc, integrator="verlet")
+    eng.step(2000)
+    assert abs(eng.x[b, 0] - 1.0) < 0.5
+
+
+def test_rk4_kats():
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=0.1)
+    sc.add_mass((0, 0, 0), v=(1.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="rk4")
+    eng.step()
+    np.testing.assert_allclose(eng.x[0], [0.1, 0.0, 0.0])
+    eng = Engine(drop(dt=0.02), integrator="rk4")
+    eng.step(50)
+    assert eng.x[0, 1] == pytest.approx(-0.5 * 9.81, abs=1e-12)
+    sc, b = axial(dt=0.01)
+    eng = Engine(sc, integrator="rk4")
+    eng.step(628)
+    assert abs(eng.x[b, 0] - (1.0 + 0.5 * math.cos(6.28))) < 1e-8
+    sc, _ = axial(dt=0.01, u0=0.4)
+    eng = Engine(sc, integrator="rk4")
+    eng.step(50)
+    np.testing.assert_array_equal(eng.x[0], [0.0, 0.0, 0.0])
+
+
+def test_time_is_step_count_times_dt():
+    eng = Engine(drop(dt=0.1), integrator="euler")
+    for n in range(1, 6):
+        eng.step()
+        assert eng.t == n * 0.1 and eng.n == n
+
+
+def test_divergence_reports_mass_and_step():
+    sc, b = axial(dt=10.0, k=1e4, m=0.01)
+    eng = Engine(sc, integrator="euler")
+    with pytest.raises(DivergenceError) as err:
+        eng.step(10000)
+    assert err.value.mass_id == b and err.value.step > 0
+
+
+def test_anchor_bit_identical_over_run():
+    sc = Scene()
+    a = sc.add_mass((0.1, 0.2, 0.3), fixed=True)
+    b = sc.add_mass((0.1, -0.9, 0.3), m=0.1)
+    sc.add_spring(a, b, k=1000.0)
+    eng = Engine(sc, integrator="verlet")
+    eng.step(500)
+    assert eng.x[a].tobytes() == np.array(sc.masses[a].x).tobytes()
+
+
+def test_actuation():
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=1e-3)
+    a = sc.add_mass((0, 0, 0), fixed=True)
+    b = sc.add_mass((1, 0, 0), m=0.1)
+    sc.add_group(ActuationGroup("muscle", amplitude=0.1, frequency=5.0))
+    sc.add_spring(a, b, k=100.0, group="muscle")
+    res = simulate(sc, 1.0, traces=[b], integrator="verlet")
+    x = res.positions[b][:, 0]
+    assert x.max() > 1.02 and x.min() < 0.98
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=1e-3, damping=0.05)
+    a = sc.add_mass((0, 0, 0), fixed=True)
+    b = sc.add_mass((1, 0, 0), m=0.1)
+    sc.add_group(ActuationGroup("grow", mode="constant-expansion", amplitude=0.2))
+    sc.add_spring(a, b, k=100.0, group="grow")
+    eng = Engine(sc, integrator="verlet")
+    eng.step(5000)
+    assert eng.x[b, 0] == pytest.approx(1.2, abs=1e-3)
+
+
+def test_simulate_sampling_rules(tmp_path):
+    res = simulate(drop(), 0.0, traces=[0], integrator="euler")
+    assert res.engine.n == 0 and len(res.times) == 1
+    res = simulate(drop(dt=1e-3), 1.0, traces=[0], integrator="verlet")
+    assert res.engine.x[0, 1] == pytest.approx(-4.905, abs=1e-3)
+    res = simulate(drop(dt=0.01), 0.05, traces=[0], integrator="verlet")
+    assert res.engine.n == 5
+    np.testing.assert_allclose(res.times, [0.0, 0.01, 0.02, 0.03, 0.04])
+    res = simulate(drop(dt=0.01), 0.1, traces=[0], integrator="euler", sample_every=5)
+    np.testing.assert_allclose(res.times, [0.0, 0.05, 0.1])
+    sc = drop(dt=0.01)
+    first = simulate(sc, 0.05, traces=[0], integrator="euler")
+    second = simulate(sc, 0.05, traces=[0], engine=first.engine)
+    assert second.times[0] == pytest.approx(0.06) and second.engine.n == 10
+    res = simulate(drop(dt=0.01), 0.03, traces=[0], integrator="euler")
+    path = tmp_path / "trace.csv"
+    res.write_csv(path)
+    lines = path.read_text().strip().splitlines()
+    assert lines[0] == "t,0.x,0.y,0.z,epe,gpe,ke,total" and len(lines) == 5
+    assert float(lines[2].split(",")[2]) == res.positions[0][1, 1]
+
+
+def test_commands_and_pause_resume():
+    eng = Engine(drop(dt=0.01), integrator="euler")
+    eng.post_command({"op": "set-damping", "value": 0.5})
+    eng.step()
+    assert eng.damping == 0.5
+    sc = drop(dt=0.01)
+    eng = Engine(sc, integrator="euler")
+    eng.post_command({"op": "stop"})
+    assert simulate(sc, 1.0, engine=eng).engine.n == 1
+    eng = Engine(sc, integrator="euler")
+    eng.post_command({"op": "pause"})
+    eng.step()
+    assert eng.paused
+    done = threading.Event()
+
+    def finish():
+        simulate(sc, 0.05, engine=eng)
+        done.set()
+
+    th = threading.Thread(target=finish)
+    th.start()
+    assert not done.wait(0.1)
+    eng.post_command({"op": "resume"})
+    assert done.wait(10.0)
+    th.join()
+    assert eng.n == 6
+    eng = Engine(drop(), integrator="euler")
+    eng.post_command({"op": "warp-reality"})
+    eng.step()
+    assert eng.command_errors and "warp-reality" in eng.command_errors[0]
+
+
+def test_momentum_isolated_pair():
+    sc = Scene(gravity=(0.0, 0.0, 0.0))
+    sc.add_mass((0.0, 0.0, 0.0), m=0.1)
+    sc.add_mass((1.2, 0.0, 0.0), m=0.1)
+    sc.add_spring(0, 1, k=10000.0, l0=1.0)
+    eng = Engine(sc, integrator="euler")
+    p0 = (eng.m[:, None] * eng.v).sum(axis=0)
+    for _ in range(50):
+        f = eng.forces(eng.x, eng.v, eng.t)
+        eng.step()
+    p1 = (eng.m[:, None] * eng.v).sum(axis=0)
+    assert np.abs(f.sum(axis=0)).max() <= 1e-9 * max(np.abs(f).sum(), 1.0)
+    np.testing.assert_allclose(p1, p0, atol=1e-9 * 2400)
+
+
+def test_host_inplace_edits_reach_the_device():
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=0.1)
+    sc.add_mass((0.0, 0.0, 0.0))
+    eng = Engine(sc, integrator="euler")
+    eng.v[0, 0] = 2.0                 # in-place edit of the host mirror
+    eng.f_ext[0] = (0.0, 1.0, 0.0)
+    eng.set_external_force(0, (0.0, 1.0, 0.0))
+    eng.step()
+    assert eng.x[0, 0] == pytest.approx(0.2)
+    assert eng.v[0, 1] == pytest.approx(1.0)

@@ -1,0 +1,122 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the reference.
+
+fp64 mode must be BITWISE equal to the reference's serial mode (the golden
+vectors were produced by the real reference; the oracle reproduces them, see
+test_oracle_golden.py).  fp32 mode must stay within the stated tolerance
+max|x - x_ref| / max|x_ref| <= 1e-4 over <= 1000 steps.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_arrays, golden_cases, golden_scene, load_golden
+
+from paper_2207_09334_b200 import DivergenceError, Engine
+from paper_2207_09334_b200 import lattice as L
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4     # relative position tolerance of the fp32 production mode
+
+
+def run_engine(case, layout, precision="f64"):
+    d = load_golden(case)
+    eng = Engine(golden_scene(d), integrator=str(d["integrator"]), precision=precision,
+                 layout=layout)
+    return d, eng
+
+
+@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("case", golden_cases())
+def test_fp64_bitwise_vs_reference(case, layout):
+    d, eng = run_engine(case, layout)
+    done = 0
+    for c in d["checkpoints"]:
+        eng.step(int(c) - done)
+        done = int(c)
+        assert eng.x.tobytes() == d[f"x_{c}"].tobytes(), (case, layout, c, "x")
+        assert eng.v.tobytes() == d[f"v_{c}"].tobytes(), (case, layout, c, "v")
+        if f"xp_{c}" in d.files:
+            assert eng.x_prev.tobytes() == d[f"xp_{c}"].tobytes(), (case, layout, c, "x_prev")
+        assert eng.t == float(d[f"t_{c}"]) and eng.n == int(c)
+        assert eng.degenerate_springs == int(d[f"deg_{c}"])
+
+
+@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("case", [c for c in golden_cases() if "degenerate" not in c])
+def test_fp32_within_tolerance(case, layout):
+    d, eng = run_engine(case, layout, precision="f32")
+    done = 0
+    for c in d["checkpoints"]:
+        if int(c) > 1000:
+            break
+        eng.step(int(c) - done)
+        done = int(c)
+        ref = d[f"x_{c}"]
+        err = np.abs(eng.x - ref).max() / max(np.abs(ref).max(), 1e-300)
+        assert err <= FP32_TOL, (case, layout, c, err)
+
+
+@pytest.mark.parametrize("layout", ["csr", "ell"])
+def test_divergence_names_mass_and_step(layout):
+    d = load_golden("divergence_euler")
+    eng = Engine(golden_scene(d), integrator="euler", layout=layout)
+    with pytest.raises(DivergenceError) as err:
+        eng.step(10000)
+    assert err.value.mass_id == int(d["div_mass"])
+    assert err.value.step == int(d["div_step"])
+    assert "smaller dt" in str(err.value)
+    assert eng.n == int(d["div_step"])
+    assert eng.x.tobytes() == d["x_div"].tobytes()
+    assert eng.v.tobytes() == d["v_div"].tobytes()
+
+
+@pytest.mark.parametrize("layout", ["csr", "ell"])
+def test_forces_bitwise(layout):
+    d = load_golden("forces_block6")
+    eng = Engine(golden_scene(d), layout=layout)
+    acc = eng.forces(d["px"], d["pv"], 0.0)
+    assert acc.tobytes() == d["acc"].tobytes()
+
+
+def test_batched_equals_single_steps():
+    """step(n) in one device batch == n calls of step(1) (bitwise)."""
+    d = load_golden("crawler_verlet")
+    a = Engine(golden_scene(d))
+    b = Engine(golden_scene(d))
+    a.step(123)
+    for _ in range(123):
+        b.step(1)
+    assert a.x.tobytes() == b.x.tobytes() and a.v.tobytes() == b.v.tobytes()
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_large_block_against_oracle(precision):
+    """Full-size property check beyond the golden sizes: 42^3-cell excited
+    block (984,438 springs), 20 Verlet steps, GPU vs the C oracle (itself
+    pinned to the reference): bitwise in fp64, 1e-4 in fp32."""
+    import oracle as orc
+    from paper_2207_09334_b200.model import scene_arrays
+    scene = L.excite(L.block_scene(42), seed=11)
+    eng = Engine(scene, precision=precision)
+    eng.step(20)
+    ref = orc.OracleEngine(scene_arrays(scene), integrator="verlet", mode="parallel-det", threads=8)
+    ref.step(20)
+    if precision == "f64":
+        assert eng.x.tobytes() == ref.x.tobytes()
+        assert eng.v.tobytes() == ref.v.tobytes()
+    else:
+        disp = np.abs(ref.x - scene.x).max()
+        err = np.abs(eng.x - ref.x).max()
+        assert err / np.abs(ref.x).max() <= FP32_TOL
+        assert err / disp <= 1e-3     # displacement-relative error
+
+
+def test_momentum_conserved_free_block():
+    """tests/test_acceptance.py:169-195 momentum criterion on the GPU."""
+    scene = L.excite(L.block_scene(9), seed=11)
+    eng = Engine(scene)
+    p0 = (eng.m[:, None] * scene.v).sum(axis=0)
+    eng.step(1000)
+    p1 = (eng.m[:, None] * eng.v).sum(axis=0)
+    assert np.linalg.norm(p1 - p0) / np.linalg.norm(p0) <= 1e-9

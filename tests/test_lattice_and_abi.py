@@ -1,0 +1,149 @@
+"""CPU-only checks: array-native lattice builder vs reference topology digests,
+workload helpers, and the C ABI surface of the shared library."""
+
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+from paper_2207_09334_b200 import _lib
+from paper_2207_09334_b200 import lattice as L
+from paper_2207_09334_b200.model import ActuationGroup, Scene, scene_arrays, validate_scene
+
+TOPO = json.load(open(os.path.join(GOLDEN, "topology.json")))
+
+
+def digest(scene) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(scene.x).tobytes())
+    h.update(np.ascontiguousarray(scene.m).tobytes())
+    for a in (scene.si, scene.sj, scene.k, scene.l0):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 20])
+def test_block_scene_bit_identical_to_reference(n):
+    s = L.block_scene(n)
+    assert digest(s) == TOPO[f"block_{n}"]
+    assert s.spring_count == L.block_springs(n)
+    assert s.mass_count == (n + 1) ** 3
+    assert s.gravity == (0.0, 0.0, 0.0)
+
+
+def test_beams_bit_identical_to_reference():
+    assert digest(L.beam_lattice()) == TOPO["beam_20x4x4"]
+    b40 = L.beam_lattice(length=4.0)
+    assert digest(b40) == TOPO["beam_40x4x4"]
+    assert [b40.mass_count, b40.spring_count] == TOPO["beam_40x4x4_counts"]
+    assert b40.m[0] == TOPO["beam_40x4x4_mass"]
+    assert int(b40.fixed.sum()) == 25
+
+
+def test_box_with_inexact_extent_keeps_surface_nodes():
+    s = L.voxel_box((0, 0, 0), (0.3, 0.2, 0.1), 0.1)
+    assert digest(s) == TOPO["box_0.3x0.2x0.1"]
+
+
+def test_crawler_topology_and_groups():
+    c = L.crawler_scene()
+    assert digest(c) == TOPO["crawler"]
+    assert c.group.tolist() == TOPO["crawler_groups"]
+    assert list(c.groups) == ["rear", "front"]
+
+
+def test_excited_velocities_match_reference_stream():
+    s = L.excite(L.block_scene(9), seed=11)
+    assert hashlib.sha256(s.v.tobytes()).hexdigest() == TOPO["excited9_v_sha256"]
+
+
+def test_block_sizing_matches_reference():
+    for n, s in TOPO["block_springs"].items():
+        assert L.block_springs(int(n)) == s
+    for s, n in TOPO["block_cells"].items():
+        assert L.block_cells(int(s)) == n
+    with pytest.raises(ValueError):
+        L.block_springs(0)
+    with pytest.raises(ValueError):
+        L.block_cells(0)
+
+
+def test_slab_emission_partitions_the_lattice():
+    """Spatial slabs (multi-GPU sharding) carry global spring ids; the union of
+    the slabs' owned springs is the whole lattice, each exactly once."""
+    counts, x, si, sj, k, l0, ids = L.voxel_arrays((0, 0, 0), (0.7, 0.4, 0.5), 0.1)
+    nx = counts[0]
+    plane = counts[1] * counts[2]
+    seen = np.zeros(si.shape[0], dtype=np.int64)
+    cuts = [0, 3, 5, nx]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        c2, xs, si2, sj2, k2, l02, ids2 = L.voxel_arrays((0, 0, 0), (0.7, 0.4, 0.5), 0.1, plane_range=(a, b))
+        assert xs.tobytes() == x[a * plane:b * plane].tobytes()
+        assert np.array_equal(si2, si[ids2]) and np.array_equal(sj2, sj[ids2])
+        assert k2.tobytes() == k[ids2].tobytes() and l02.tobytes() == l0[ids2].tobytes()
+        own = (si2 >= a * plane) & (si2 < b * plane)          # lower endpoint in slab
+        seen[ids2[own]] += 1
+        touches = ((si >= a * plane) & (si < b * plane)) | ((sj >= a * plane) & (sj < b * plane))
+        assert set(ids2.tolist()) == set(np.nonzero(touches)[0].tolist())
+    assert (seen == 1).all()
+
+
+def test_scene_api_and_freeze():
+    sc = Scene(gravity=(0.0, 0.0, 0.0))
+    a = sc.add_mass((0, 0, 0), fixed=True)
+    b = sc.add_mass((1.2, 0, 0))
+    sc.add_group(ActuationGroup("g", amplitude=0.1))
+    s = sc.add_spring(a, b, k=10.0, group="g")
+    assert sc.springs[s].l0 == 1.2
+    with pytest.raises(ValueError):
+        sc.add_spring(b, a, k=1.0)
+    with pytest.raises(ValueError):
+        sc.add_group(ActuationGroup("g"))
+    assert validate_scene(sc) == []
+    arr = scene_arrays(sc)
+    assert arr.group.tolist() == [0]
+    assert arr.fixed.tolist() == [True, False]
+    assert sc.degrees() == [1, 1]
+
+
+# ------------------------------------------------------------- C ABI
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "springsim_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ss_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} not bound in _lib.SIGNATURES"
+    assert lib.ss_abi_version() == 1
+
+
+def test_engine_without_gpu_fails_loudly():
+    """No CPU fallback: on a host without a device, construction raises."""
+    if _lib.device_count() > 0:
+        pytest.skip("a GPU is present")
+    from paper_2207_09334_b200 import Engine
+    with pytest.raises(_lib.CudaError):
+        Engine(L.block_scene(1))
+
+
+def test_bad_arguments_are_value_errors():
+    from paper_2207_09334_b200 import Engine
+    with pytest.raises(ValueError):
+        Engine(L.block_scene(1), integrator="leapfrog")
+    with pytest.raises(ValueError):
+        Engine(L.block_scene(1), mode="turbo")
+    with pytest.raises(ValueError):
+        Engine(L.block_scene(1), precision="f16")
