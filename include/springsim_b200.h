@@ -50,6 +50,7 @@ extern "C" {
 #define SS_LAYOUT_AUTO 0
 #define SS_LAYOUT_CSR  1   /* generic per-mass CSR, any degree                      */
 #define SS_LAYOUT_ELL  2   /* sliced-ELL owner records + reverse refs (16 B/spring) */
+#define SS_LAYOUT_TILE 3   /* 256-mass brick tiles, TMA-staged records + smem halo   */
 
 /* actuation modes (model.py:21-23) */
 #define SS_SINUSOID            0
@@ -168,6 +169,11 @@ typedef struct ss_info {
     double  algorithmic_bytes_per_step;
     int32_t ell_width_own, ell_width_ref;
     int32_t canonical_order;   /* 1 if the ELL split order == spring-id order */
+    int32_t smem_per_block;    /* TILE: dynamic shared memory per CTA */
+    int64_t tile_count;        /* TILE: number of 256-mass tiles */
+    int64_t tile_blob_bytes;   /* TILE: bytes of records streamed per step */
+    double  tile_halo_ratio;   /* TILE: mean (tile + halo masses) / tile masses */
+    double  tile_foreign_frac; /* TILE: fraction of references whose owner is in another tile */
 } ss_info;
 int ss_get_info(ss_engine *h, ss_info *info);
 

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 SS_OK, SS_EINVAL, SS_ECUDA, SS_EDIVERGED, SS_ENOMEM = 0, 1, 2, 3, 4
 SS_EULER, SS_VERLET, SS_RK4 = 0, 1, 2
 SS_F64, SS_F32 = 0, 1
-SS_LAYOUT_AUTO, SS_LAYOUT_CSR, SS_LAYOUT_ELL = 0, 1, 2
+SS_LAYOUT_AUTO, SS_LAYOUT_CSR, SS_LAYOUT_ELL, SS_LAYOUT_TILE = 0, 1, 2, 3
 SS_SINUSOID, SS_CONSTANT_EXPANSION = 0, 1
 
 _dp = C.POINTER(C.c_double)
@@ -53,7 +53,9 @@ class Info(C.Structure):
                 ("device", C.c_int32), ("device_bytes", C.c_int64),
                 ("algorithmic_bytes_per_step", C.c_double),
                 ("ell_width_own", C.c_int32), ("ell_width_ref", C.c_int32),
-                ("canonical_order", C.c_int32)]
+                ("canonical_order", C.c_int32), ("smem_per_block", C.c_int32),
+                ("tile_count", C.c_int64), ("tile_blob_bytes", C.c_int64),
+                ("tile_halo_ratio", C.c_double), ("tile_foreign_frac", C.c_double)]
 
 
 # Every symbol include/springsim_b200.h declares, with its ctypes signature.

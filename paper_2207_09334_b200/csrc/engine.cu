@@ -3,9 +3,9 @@
 // Host side of the relaxation loop: freezes a scene description into device
 // buffers (engine.py:182-246), builds the incidence layout, and drives the
 // per-step kernels of kernels.cuh on a private CUDA stream.  A batch of
-// `count` steps is enqueued back-to-back (CUDA graph per batch length) with
-// the divergence check fused into each step's epilogue, so a batch costs one
-// host synchronisation, not one per step (engine.py:366-373 syncs per step).
+// `count` steps is enqueued back-to-back with the divergence check fused
+// into each step's epilogue, so a batch costs one host synchronisation, not
+// one per step (engine.py:366-373 checks after every step).
 
 #include <cuda_runtime.h>
 
@@ -13,16 +13,16 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
-#include <map>
 #include <memory>
-#include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "common.h"
 #include "kernels.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
+#include "tiles.h"
 
 using namespace ss;
 
@@ -35,7 +35,7 @@ using namespace ss;
 
 namespace {
 
-constexpr int kBlock = 256;
+constexpr int kBlock = kBlockThreads;
 
 struct Group {
     int mode;
@@ -54,49 +54,53 @@ struct ss_engine {
     cudaStream_t stream = nullptr;
     int precision = SS_F64, layout = SS_LAYOUT_CSR, integrator = SS_VERLET;
     int64_t N = 0, S = 0;
-    size_t elem = 8;               // sizeof(T)
-    size_t vec = 32;               // sizeof(T4)
 
     // host-side scalars (engine.py:190-194, 222-224)
     double dt = 1e-4, damping = 0.0, gravity[3] = {0, 0, 0};
     std::vector<Group> groups;
     std::vector<double> planes;    // 6 per plane
-    std::vector<double> m;         // masses
-    std::vector<uint8_t> fixed;
+    std::vector<double> m;         // masses (caller order)
+    std::vector<uint8_t> fixed;    // caller order
+    std::vector<int32_t> orig_of;  // device id -> caller id (empty: identity)
+    std::vector<float> base;       // fp32 base positions, device order, 4 per mass
     double t = 0.0;
     int64_t n = 0;
     bool has_prev = false;
     bool has_fext = false;
-    int64_t degenerate_host = 0;   // folded-in count
 
-    // device state
+    // device state (device order)
     std::vector<DevBuf> bufs;
     void *X[2] = {nullptr, nullptr};
     int cur = 0;
     void *V = nullptr;
-    void *P = nullptr;             // fp32 base positions
-    void *F = nullptr;             // f_ext
+    void *P = nullptr;
+    void *F = nullptr;
     void *XA = nullptr, *XB = nullptr, *VS = nullptr, *SV = nullptr, *SA = nullptr;  // RK4
     void *scale = nullptr;
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
     long long *d_div_step = nullptr;
     int *d_div_mass = nullptr;
-    void *d_acc = nullptr;         // forces scratch (double3 x N)
+    int *d_orig_of = nullptr;
+    void *d_acc = nullptr;
     void *d_tmp[2] = {nullptr, nullptr};
 
     // topology
     Layout lay;
+    TileLayout tl;
     void *k = nullptr, *l0 = nullptr, *e_k = nullptr, *e_l0 = nullptr;
     int *row = nullptr, *grp = nullptr, *e_other = nullptr, *e_grp = nullptr, *r_pos = nullptr,
         *cnt = nullptr;
     int2 *inc = nullptr;
+    unsigned char *d_blob = nullptr;
+    unsigned long long *d_toff = nullptr;
+    uint32_t blob_smem = 0, max_halo = 0;
+    size_t smem_bytes = 0;
     int64_t device_bytes = 0;
     int64_t launches = 0;
-    int64_t pending = 0;           // steps enqueued by ss_step_async and not yet synced
+    int64_t pending = 0;
     int64_t pending_n0 = 0;
     int pending_cur0 = 0;
-    double pending_t0 = 0.0;
 
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
@@ -116,29 +120,33 @@ struct ss_engine {
         *out = reinterpret_cast<P_ *>(p);
         return SS_OK;
     }
+
+    int64_t src_of(int64_t i) const { return orig_of.empty() ? i : orig_of[i]; }
 };
 
 namespace {
 
 // ------------------------------------------------------------ conversions
+// Host arrays are (N,3) f64 in caller order; device arrays are T4 in device
+// order (orig_of permutation).  fp64: (x, y, z, +-m); fp32: r = float(x - P).
 
-// Pack (N,3) f64 host positions into the device T4 representation.
-//   fp64: (x, y, z, +-m)             fp32: r = float(x - P), .w = +-m
 template <typename T, typename T4>
-void pack_positions(const ss_engine *h, const double *x, const float *base, T4 *out) {
+void pack_positions(const ss_engine *h, const double *x, T4 *out) {
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < h->N; ++i) {
+        const int64_t s = h->src_of(i);
         T4 o;
-        const double w = h->fixed[i] ? -h->m[i] : h->m[i];
+        const double w = h->fixed[s] ? -h->m[s] : h->m[s];
         if constexpr (std::is_same<T, float>::value) {
-            o.x = (float)(x[3 * i + 0] - (double)base[4 * i + 0]);
-            o.y = (float)(x[3 * i + 1] - (double)base[4 * i + 1]);
-            o.z = (float)(x[3 * i + 2] - (double)base[4 * i + 2]);
+            const float *b = h->base.data() + 4 * i;
+            o.x = (float)(x[3 * s + 0] - (double)b[0]);
+            o.y = (float)(x[3 * s + 1] - (double)b[1]);
+            o.z = (float)(x[3 * s + 2] - (double)b[2]);
             o.w = (float)w;
         } else {
-            o.x = x[3 * i + 0];
-            o.y = x[3 * i + 1];
-            o.z = x[3 * i + 2];
+            o.x = x[3 * s + 0];
+            o.y = x[3 * s + 1];
+            o.z = x[3 * s + 2];
             o.w = w;
         }
         out[i] = o;
@@ -146,58 +154,48 @@ void pack_positions(const ss_engine *h, const double *x, const float *base, T4 *
 }
 
 template <typename T, typename T4>
-void pack_vec(int64_t N, const double *v, T4 *out) {
+void pack_vec(const ss_engine *h, const double *v, T4 *out) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; i < h->N; ++i) {
+        const int64_t s = h->src_of(i);
         T4 o;
-        o.x = (T)v[3 * i + 0];
-        o.y = (T)v[3 * i + 1];
-        o.z = (T)v[3 * i + 2];
+        o.x = (T)v[3 * s + 0];
+        o.y = (T)v[3 * s + 1];
+        o.z = (T)v[3 * s + 2];
         o.w = (T)0;
         out[i] = o;
     }
 }
 
 template <typename T, typename T4>
-void unpack_positions(const ss_engine *h, const T4 *in, const float *base, double *x) {
+void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < h->N; ++i) {
+        const int64_t s = h->src_of(i);
         if constexpr (std::is_same<T, float>::value) {
-            x[3 * i + 0] = (double)base[4 * i + 0] + (double)in[i].x;
-            x[3 * i + 1] = (double)base[4 * i + 1] + (double)in[i].y;
-            x[3 * i + 2] = (double)base[4 * i + 2] + (double)in[i].z;
+            const float *b = h->base.data() + 4 * i;
+            x[3 * s + 0] = (double)b[0] + (double)in[i].x;
+            x[3 * s + 1] = (double)b[1] + (double)in[i].y;
+            x[3 * s + 2] = (double)b[2] + (double)in[i].z;
         } else {
-            x[3 * i + 0] = in[i].x;
-            x[3 * i + 1] = in[i].y;
-            x[3 * i + 2] = in[i].z;
+            x[3 * s + 0] = in[i].x;
+            x[3 * s + 1] = in[i].y;
+            x[3 * s + 2] = in[i].z;
         }
     }
 }
 
 template <typename T, typename T4>
-void unpack_vec(int64_t N, const T4 *in, double *v) {
+void unpack_vec(const ss_engine *h, const T4 *in, double *v) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < N; ++i) {
-        v[3 * i + 0] = (double)in[i].x;
-        v[3 * i + 1] = (double)in[i].y;
-        v[3 * i + 2] = (double)in[i].z;
+    for (int64_t i = 0; i < h->N; ++i) {
+        const int64_t s = h->src_of(i);
+        v[3 * s + 0] = (double)in[i].x;
+        v[3 * s + 1] = (double)in[i].y;
+        v[3 * s + 2] = (double)in[i].z;
     }
 }
 
-// The fp32 base positions live on the host too (needed to pack/unpack).
-struct HostBase {
-    std::vector<float> p;   // 4 per mass
-};
-std::mutex g_base_mu;
-std::map<const ss_engine *, HostBase> g_base;
-
-const float *host_base(const ss_engine *h) {
-    std::lock_guard<std::mutex> lk(g_base_mu);
-    auto it = g_base.find(h);
-    return it == g_base.end() ? nullptr : it->second.p.data();
-}
-
-// Upload a host array (pageable) into a device buffer on the engine stream.
 int upload(ss_engine *h, void *dst, const void *src, size_t bytes) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -211,10 +209,19 @@ int download(ss_engine *h, void *dst, const void *src, size_t bytes) {
 
 // ----------------------------------------------------------- actuation
 
-// Scale table for `count` steps starting at (t0, n0): the exact Python
-// expression of engine.py:250-259 (math.sin is libm sin).
-// Euler/Verlet: one evaluation time per step (self.t, which is t0 for the
-// first step and n*dt afterwards); RK4: t, t+dt/2, t+dt/2, t+dt.
+// Actuation scale of every group at time ts, the exact Python expression of
+// engine.py:250-259 (math.sin is libm sin; host code built -ffp-contract=off).
+void scales_at(const ss_engine *h, double ts, double *out) {
+    for (size_t g = 0; g < h->groups.size(); ++g) {
+        const Group &gr = h->groups[g];
+        out[g] = gr.mode == SS_CONSTANT_EXPANSION
+                     ? 1.0 + gr.amplitude
+                     : 1.0 + gr.amplitude * std::sin(2.0 * M_PI * gr.frequency * ts + gr.phase);
+    }
+}
+
+// Table for `count` steps starting at (t0, n0).  Euler/Verlet evaluate at
+// self.t (t0 for the first step, n*dt afterwards); RK4 at t, t+dt/2 (x2), t+dt.
 void build_scales(const ss_engine *h, int64_t count, int stages, double t0, int64_t n0,
                   std::vector<double> &out) {
     const size_t G = h->groups.size();
@@ -227,14 +234,7 @@ void build_scales(const ss_engine *h, int64_t count, int stages, double t0, int6
             st[2] = ts + 0.5 * h->dt;
             st[3] = ts + h->dt;
         }
-        for (int q = 0; q < stages; ++q)
-            for (size_t g = 0; g < G; ++g) {
-                const Group &gr = h->groups[g];
-                double sc;
-                if (gr.mode == SS_CONSTANT_EXPANSION) sc = 1.0 + gr.amplitude;
-                else sc = 1.0 + gr.amplitude * std::sin(2.0 * M_PI * gr.frequency * st[q] + gr.phase);
-                out[((size_t)s * stages + q) * G + g] = sc;
-            }
+        for (int q = 0; q < stages; ++q) scales_at(h, st[q], &out[((size_t)s * stages + q) * G]);
     }
 }
 
@@ -243,16 +243,12 @@ int upload_scales(ss_engine *h, const std::vector<double> &tab) {
     if (tab.empty()) return SS_OK;
     const size_t bytes = tab.size() * sizeof(T);
     if (bytes > h->scale_cap) {
-        if (h->scale) {
-            cudaFree(h->scale);
-            for (auto &b : h->bufs)
-                if (b.p == h->scale) { h->device_bytes -= (int64_t)b.bytes; b.p = nullptr; b.bytes = 0; }
-        }
         void *p;
-        int rc = h->alloc(&p, std::max<size_t>(bytes, 4096));
+        const size_t cap = std::max<size_t>(bytes, 4096);
+        int rc = h->alloc(&p, cap);
         if (rc) return rc;
-        h->scale = p;
-        h->scale_cap = std::max<size_t>(bytes, 4096);
+        h->scale = p;          // the old buffer stays owned by h->bufs until destruction
+        h->scale_cap = cap;
     }
     if constexpr (std::is_same<T, double>::value) {
         return upload(h, h->scale, tab.data(), bytes);
@@ -271,6 +267,7 @@ Params<T> base_params(const ss_engine *h) {
     p.n = (int)h->N;
     p.P = reinterpret_cast<const T4 *>(h->P);
     p.F = h->has_fext ? reinterpret_cast<const T4 *>(h->F) : nullptr;
+    p.orig_of = h->d_orig_of;
     Topology<T> &tp = p.topo;
     tp.row = h->row;
     tp.inc = h->inc;
@@ -285,6 +282,10 @@ Params<T> base_params(const ss_engine *h) {
     tp.cnt = h->cnt;
     tp.W = h->lay.W;
     tp.Wr = h->lay.Wr;
+    tp.blob = h->d_blob;
+    tp.toff = h->d_toff;
+    tp.blob_smem = h->blob_smem;
+    tp.max_halo = h->max_halo;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -306,19 +307,30 @@ Params<T> base_params(const ss_engine *h) {
     return p;
 }
 
+// Call fn(std::integral_constant<int, LAYOUT>{}) for the engine's layout.
+template <typename Fn>
+int with_layout(const ss_engine *h, Fn &&fn) {
+    switch (h->layout) {
+        case SS_LAYOUT_CSR: return fn(std::integral_constant<int, 1>{});
+        case SS_LAYOUT_ELL: return fn(std::integral_constant<int, 2>{});
+        default: return fn(std::integral_constant<int, 3>{});
+    }
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
     const int stages = h->integrator == SS_RK4 ? 4 : 1;
     const size_t G = h->groups.size();
-    std::vector<double> tab;
     if (G) {
+        std::vector<double> tab;
         build_scales(h, count, stages, h->t, h->n, tab);
         int rc = upload_scales<T>(h, tab);
         if (rc) return rc;
     }
     const int grid = (int)((h->N + kBlock - 1) / kBlock);
+    const size_t smem = LAYOUT == 3 ? h->smem_bytes : 0;
     Params<T> p = base_params<T>(h);
     const T *scale = reinterpret_cast<const T *>(h->scale);
     for (int64_t s = 0; s < count; ++s) {
@@ -336,8 +348,8 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.Vout = V;
             p.Xprev = Xo;
             p.bootstrap = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
-            if (h->integrator == SS_EULER) step_kernel<F32, 0, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
-            else step_kernel<F32, 1, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
+            if (h->integrator == SS_EULER) step_kernel<F32, 0, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            else step_kernel<F32, 1, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             h->launches += 1;
             h->cur ^= 1;
             if (h->integrator == SS_VERLET) h->has_prev = true;
@@ -348,22 +360,18 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.V0 = V;
             p.SV = reinterpret_cast<T4 *>(h->SV);
             p.SA = reinterpret_cast<T4 *>(h->SA);
-            // stage 1: (x0, v0) -> (XA, VS)
             p.scale = G ? scale + ((size_t)s * 4 + 0) * G : nullptr;
             p.X = Xc; p.V = V; p.Xout = XA; p.Vout = VS;
-            rk4_kernel<F32, 1, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
-            // stage 2: (XA, VS) -> (XB, VS)
+            rk4_kernel<F32, 1, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             p.scale = G ? scale + ((size_t)s * 4 + 1) * G : nullptr;
             p.X = XA; p.V = VS; p.Xout = XB; p.Vout = VS;
-            rk4_kernel<F32, 2, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
-            // stage 3: (XB, VS) -> (XA, VS)
+            rk4_kernel<F32, 2, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             p.scale = G ? scale + ((size_t)s * 4 + 2) * G : nullptr;
             p.X = XB; p.V = VS; p.Xout = XA; p.Vout = VS;
-            rk4_kernel<F32, 3, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
-            // stage 4: (XA, VS) -> (x0, v0) in place
+            rk4_kernel<F32, 3, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             p.scale = G ? scale + ((size_t)s * 4 + 3) * G : nullptr;
             p.X = XA; p.V = VS; p.Xout = Xc; p.Vout = V;
-            rk4_kernel<F32, 4, LAYOUT><<<grid, kBlock, 0, h->stream>>>(p);
+            rk4_kernel<F32, 4, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             h->launches += 4;
         }
     }
@@ -372,10 +380,23 @@ int launch_steps(ss_engine *h, int64_t count) {
 }
 
 int dispatch_steps(ss_engine *h, int64_t count) {
-    if (h->precision == SS_F32) {
-        return h->layout == SS_LAYOUT_ELL ? launch_steps<true, 2>(h, count) : launch_steps<true, 1>(h, count);
-    }
-    return h->layout == SS_LAYOUT_ELL ? launch_steps<false, 2>(h, count) : launch_steps<false, 1>(h, count);
+    return with_layout(h, [&](auto L) -> int {
+        return h->precision == SS_F32 ? launch_steps<true, decltype(L)::value>(h, count)
+                                      : launch_steps<false, decltype(L)::value>(h, count);
+    });
+}
+
+template <bool F32>
+int set_tile_smem(size_t bytes) {
+    const int b = (int)bytes;
+    CK(cudaFuncSetAttribute(step_kernel<F32, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(step_kernel<F32, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(forces_kernel<F32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    return SS_OK;
 }
 
 int reset_divergence(ss_engine *h) {
@@ -417,74 +438,120 @@ int finish_batch(ss_engine *h, int64_t count, int64_t n0, int cur0, ss_step_resu
     return SS_OK;
 }
 
+template <typename T>
+int up_vec(ss_engine *h, void **dst, const std::vector<T> &src) {
+    int r = h->alloc(dst, src.size() * sizeof(T));
+    if (r) return r;
+    return upload(h, *dst, src.data(), src.size() * sizeof(T));
+}
+
 template <bool F32>
-int create_impl(ss_engine *h, const ss_scene_desc *d) {
+int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
     const int64_t N = h->N, S = h->S;
     int rc;
-    // fp32 base positions
-    std::vector<float> base;
+    // ---- topology first: it may renumber the masses
+    int layout = want_layout;
+    if (layout == SS_LAYOUT_AUTO || layout == SS_LAYOUT_TILE) {
+        TileInput ti{N, S, d->si, d->sj, d->x, d->k, d->l0,
+                     (d->group && d->n_groups) ? d->group : nullptr, F32, 1};
+        rc = build_tiles(ti, h->tl);
+        if (rc == SS_OK) {
+            layout = SS_LAYOUT_TILE;
+        } else if (want_layout == SS_LAYOUT_TILE) {
+            return rc;
+        } else {
+            layout = SS_LAYOUT_CSR;
+            h->tl = TileLayout{};
+        }
+    }
+    h->layout = layout;
+    if (layout == SS_LAYOUT_TILE) {
+        bool identity = true;
+        for (int64_t i = 0; i < N && identity; ++i) identity = h->tl.orig_of[i] == i;
+        if (!identity) h->orig_of = h->tl.orig_of;
+    }
+    if (!h->orig_of.empty()) {
+        void *p;
+        if ((rc = up_vec(h, &p, h->orig_of))) return rc;
+        h->d_orig_of = reinterpret_cast<int *>(p);
+    }
+    // ---- fp32 base positions (device order)
     if (F32) {
-        base.resize((size_t)N * 4);
+        h->base.resize((size_t)N * 4);
         for (int64_t i = 0; i < N; ++i) {
-            for (int c = 0; c < 3; ++c) base[4 * i + c] = (float)d->x[3 * i + c];
-            base[4 * i + 3] = 0.f;
+            const int64_t s = h->src_of(i);
+            for (int c = 0; c < 3; ++c) h->base[4 * i + c] = (float)d->x[3 * s + c];
+            h->base[4 * i + 3] = 0.f;
         }
         if ((rc = h->alloc(&h->P, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = upload(h, h->P, base.data(), (size_t)N * sizeof(T4)))) return rc;
-        std::lock_guard<std::mutex> lk(g_base_mu);
-        g_base[h].p = base;
+        if ((rc = upload(h, h->P, h->base.data(), (size_t)N * sizeof(T4)))) return rc;
     }
     for (int b = 0; b < 2; ++b)
         if ((rc = h->alloc(&h->X[b], (size_t)N * sizeof(T4)))) return rc;
     if ((rc = h->alloc(&h->V, (size_t)N * sizeof(T4)))) return rc;
     if ((rc = h->alloc(&h->F, (size_t)N * sizeof(T4)))) return rc;
     if (h->integrator == SS_RK4) {
-        if ((rc = h->alloc(&h->XA, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = h->alloc(&h->XB, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = h->alloc(&h->VS, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = h->alloc(&h->SV, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = h->alloc(&h->SA, (size_t)N * sizeof(T4)))) return rc;
+        for (void **b : {&h->XA, &h->XB, &h->VS, &h->SV, &h->SA})
+            if ((rc = h->alloc(b, (size_t)N * sizeof(T4)))) return rc;
     }
     {
         std::vector<T4> tmp((size_t)N);
-        pack_positions<T, T4>(h, d->x, F32 ? base.data() : nullptr, tmp.data());
+        pack_positions<T, T4>(h, d->x, tmp.data());
         if ((rc = upload(h, h->X[0], tmp.data(), (size_t)N * sizeof(T4)))) return rc;
-        pack_vec<T, T4>(N, d->v, tmp.data());
+        pack_vec<T, T4>(h, d->v, tmp.data());
         if ((rc = upload(h, h->V, tmp.data(), (size_t)N * sizeof(T4)))) return rc;
         if (d->f_ext) {
-            pack_vec<T, T4>(N, d->f_ext, tmp.data());
+            pack_vec<T, T4>(h, d->f_ext, tmp.data());
             for (int64_t i = 0; i < 3 * N && !h->has_fext; ++i) h->has_fext = d->f_ext[i] != 0.0;
         } else {
             std::memset(tmp.data(), 0, (size_t)N * sizeof(T4));
         }
         if ((rc = upload(h, h->F, tmp.data(), (size_t)N * sizeof(T4)))) return rc;
     }
-    // topology
+    const bool has_g = d->group && !h->groups.empty();
+    if (layout == SS_LAYOUT_TILE) {
+        const TileLayout &L = h->tl;
+        void *p;
+        if ((rc = up_vec(h, &p, L.blob))) return rc;
+        h->d_blob = reinterpret_cast<unsigned char *>(p);
+        std::vector<unsigned long long> off(L.off.begin(), L.off.end());
+        if ((rc = up_vec(h, &p, off))) return rc;
+        h->d_toff = reinterpret_cast<unsigned long long *>(p);
+        h->blob_smem = (L.max_tile_bytes + 127u) & ~127u;
+        h->max_halo = L.max_halo;
+        h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4) * (F32 ? 2 : 1);
+        int dev_max = 0;
+        CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        if ((int64_t)h->smem_bytes > dev_max)
+            return ss::fail(SS_EINVAL, "tile needs %zu B of shared memory (> %d)", h->smem_bytes, dev_max);
+        if ((rc = set_tile_smem<F32>(h->smem_bytes))) return rc;
+        h->lay.canonical = L.canonical;
+        return SS_OK;
+    }
     LayoutInput li{N, S, d->si, d->sj};
-    int want = d->layout;
-    if ((rc = build_layout(li, want, h->lay))) return rc;
+    if ((rc = build_layout(li, layout, h->lay))) return rc;
     h->layout = h->lay.kind;
     auto up_typed = [&](void **dst, const std::vector<double> &src) -> int {
         std::vector<T> tv(src.begin(), src.end());
-        int r = h->alloc(dst, tv.size() * sizeof(T));
-        if (r) return r;
-        return upload(h, *dst, tv.data(), tv.size() * sizeof(T));
+        return up_vec(h, dst, tv);
     };
     auto up_int = [&](int **dst, const std::vector<int> &src) -> int {
-        int r = h->alloc(dst, src.size() * sizeof(int));
-        if (r) return r;
-        return upload(h, *dst, src.data(), src.size() * sizeof(int));
+        void *p;
+        int r = up_vec(h, &p, src);
+        *dst = reinterpret_cast<int *>(p);
+        return r;
     };
     if (h->layout == SS_LAYOUT_CSR) {
         if ((rc = up_int(&h->row, h->lay.row))) return rc;
-        if ((rc = h->alloc(&h->inc, h->lay.inc.size() * sizeof(int2)))) return rc;
-        if ((rc = upload(h, h->inc, h->lay.inc.data(), h->lay.inc.size() * sizeof(int2)))) return rc;
+        void *p;
+        if ((rc = up_vec(h, &p, h->lay.inc))) return rc;
+        h->inc = reinterpret_cast<int2 *>(p);
         std::vector<double> kv(d->k, d->k + S), lv(d->l0, d->l0 + S);
         if ((rc = up_typed(&h->k, kv))) return rc;
         if ((rc = up_typed(&h->l0, lv))) return rc;
-        if (d->group && h->groups.size()) {
+        if (has_g) {
             std::vector<int> g(d->group, d->group + S);
             if ((rc = up_int(&h->grp, g))) return rc;
         }
@@ -492,7 +559,6 @@ int create_impl(ss_engine *h, const ss_scene_desc *d) {
         const auto &L = h->lay;
         std::vector<double> ek(L.e_spring.size(), 0.0), el(L.e_spring.size(), 0.0);
         std::vector<int> eg;
-        const bool has_g = d->group && h->groups.size();
         if (has_g) eg.assign(L.e_spring.size(), -1);
         for (size_t q = 0; q < L.e_spring.size(); ++q) {
             const int64_t s = L.e_spring[q];
@@ -516,6 +582,86 @@ int64_t algorithmic_bytes(const ss_engine *h) {
     const int64_t per_spring = h->precision == SS_F32 ? 16 : 24;
     const int64_t per_mass = h->precision == SS_F32 ? 64 : 128;
     return per_spring * h->S + per_mass * h->N;
+}
+
+int sync_pending(ss_engine *h) {
+    if (!h->pending) return SS_OK;
+    int rc = ss_sync(h, nullptr);
+    return rc == SS_EDIVERGED ? SS_OK : rc;
+}
+
+template <bool F32>
+int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
+    using T = typename Prec<F32>::T;
+    using T4 = typename Prec<F32>::T4;
+    int rc;
+    std::vector<double> tab(h->groups.size());
+    if (!tab.empty()) {
+        scales_at(h, t, tab.data());
+        if ((rc = upload_scales<T>(h, tab))) return rc;
+    }
+    std::vector<T4> tx((size_t)h->N), tv((size_t)h->N);
+    pack_positions<T, T4>(h, x, tx.data());
+    pack_vec<T, T4>(h, v, tv.data());
+    if ((rc = upload(h, h->d_tmp[0], tx.data(), tx.size() * sizeof(T4)))) return rc;
+    if ((rc = upload(h, h->d_tmp[1], tv.data(), tv.size() * sizeof(T4)))) return rc;
+    Params<T> p = base_params<T>(h);
+    p.X = (const T4 *)h->d_tmp[0];
+    p.V = (const T4 *)h->d_tmp[1];
+    p.scale = tab.empty() ? nullptr : (const T *)h->scale;
+    p.acc_out = (V3<double> *)h->d_acc;
+    const int grid = (int)((h->N + kBlock - 1) / kBlock);
+    return with_layout(h, [&](auto L) -> int {
+        constexpr int LY = decltype(L)::value;
+        forces_kernel<F32, LY><<<grid, kBlock, LY == 3 ? h->smem_bytes : 0, h->stream>>>(p);
+        CK(cudaGetLastError());
+        return SS_OK;
+    });
+}
+
+template <bool F32>
+int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
+    using T = typename Prec<F32>::T;
+    using T4 = typename Prec<F32>::T4;
+    std::vector<T4> tmp((size_t)h->N);
+    const size_t bytes = (size_t)h->N * sizeof(T4);
+    int rc;
+    if (x) {
+        if ((rc = download(h, tmp.data(), h->X[h->cur], bytes))) return rc;
+        unpack_positions<T, T4>(h, tmp.data(), x);
+    }
+    if (v) {
+        if ((rc = download(h, tmp.data(), h->V, bytes))) return rc;
+        unpack_vec<T, T4>(h, tmp.data(), v);
+    }
+    if (x_prev && h->has_prev) {
+        if ((rc = download(h, tmp.data(), h->X[h->cur ^ 1], bytes))) return rc;
+        unpack_positions<T, T4>(h, tmp.data(), x_prev);
+    }
+    return SS_OK;
+}
+
+template <bool F32>
+int set_state_impl(ss_engine *h, const double *x, const double *v, const double *x_prev) {
+    using T = typename Prec<F32>::T;
+    using T4 = typename Prec<F32>::T4;
+    std::vector<T4> tmp((size_t)h->N);
+    const size_t bytes = (size_t)h->N * sizeof(T4);
+    int rc;
+    if (x) {
+        pack_positions<T, T4>(h, x, tmp.data());
+        if ((rc = upload(h, h->X[h->cur], tmp.data(), bytes))) return rc;
+    }
+    if (v) {
+        pack_vec<T, T4>(h, v, tmp.data());
+        if ((rc = upload(h, h->V, tmp.data(), bytes))) return rc;
+    }
+    if (x_prev) {
+        pack_positions<T, T4>(h, x_prev, tmp.data());
+        if ((rc = upload(h, h->X[h->cur ^ 1], tmp.data(), bytes))) return rc;
+        h->has_prev = true;
+    }
+    return SS_OK;
 }
 
 }  // namespace
@@ -551,6 +697,8 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
         return ss::fail(SS_EINVAL, "unknown integrator %d", d->integrator);
     if (d->precision != SS_F64 && d->precision != SS_F32)
         return ss::fail(SS_EINVAL, "unknown precision %d", d->precision);
+    if (d->layout < SS_LAYOUT_AUTO || d->layout > SS_LAYOUT_TILE)
+        return ss::fail(SS_EINVAL, "unknown layout %d", d->layout);
     if (d->n_planes < 0 || d->n_planes > kMaxPlanes)
         return ss::fail(SS_EINVAL, "at most %d contact planes are supported", kMaxPlanes);
     if (d->n_masses >= INT32_MAX || 2 * d->n_springs >= INT32_MAX)
@@ -587,23 +735,15 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
     if ((rc = h->alloc(&h->d_div_mass, sizeof(int)))) return rc;
     CK(cudaMemsetAsync(h->d_degenerate, 0, sizeof(unsigned long long), h->stream));
     if ((rc = reset_divergence(h.get()))) return rc;
-    rc = h->precision == SS_F32 ? create_impl<true>(h.get(), d) : create_impl<false>(h.get(), d);
-    if (rc) {
-        std::lock_guard<std::mutex> lk(g_base_mu);
-        g_base.erase(h.get());
-        return rc;
-    }
+    rc = h->precision == SS_F32 ? create_impl<true>(h.get(), d, d->layout)
+                                : create_impl<false>(h.get(), d, d->layout);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(h->stream));
     *out = h.release();
     return SS_OK;
 }
 
 int ss_destroy(ss_engine *h) {
-    if (!h) return SS_OK;
-    {
-        std::lock_guard<std::mutex> lk(g_base_mu);
-        g_base.erase(h);
-    }
     delete h;
     return SS_OK;
 }
@@ -611,25 +751,16 @@ int ss_destroy(ss_engine *h) {
 int ss_step(ss_engine *h, int64_t count, ss_step_result *res) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     CK(cudaSetDevice(h->device));
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc) return rc;
-    }
+    int rc = sync_pending(h);
+    if (rc) return rc;
     if (count <= 0) {
         if (res) *res = {0, h->n, h->t, -1, -1};
         return SS_OK;
     }
     const int64_t n0 = h->n;
     const int cur0 = h->cur;
-    const bool had_prev = h->has_prev;
-    int rc = dispatch_steps(h, count);
-    if (rc) return rc;
-    rc = finish_batch(h, count, n0, cur0, res);
-    if (rc == SS_EDIVERGED && h->integrator == SS_VERLET) {
-        // history exists iff at least one step committed
-        h->has_prev = had_prev || (h->n > n0);
-    }
-    return rc;
+    if ((rc = dispatch_steps(h, count))) return rc;
+    return finish_batch(h, count, n0, cur0, res);
 }
 
 int ss_step_async(ss_engine *h, int64_t count) {
@@ -639,13 +770,11 @@ int ss_step_async(ss_engine *h, int64_t count) {
     if (!h->pending) {
         h->pending_n0 = h->n;
         h->pending_cur0 = h->cur;
-        h->pending_t0 = h->t;
     }
-    // time bookkeeping for the scale table: advance n/t as if committed
     int rc = dispatch_steps(h, count);
     if (rc) return rc;
     h->pending += count;
-    h->n += count;
+    h->n += count;                   // provisional; ss_sync settles it
     h->t = (double)h->n * h->dt;
     return SS_OK;
 }
@@ -669,63 +798,17 @@ int ss_forces(ss_engine *h, const double *x, const double *v, double t, double *
               int64_t *degenerate_out) {
     if (!h || !x || !v || !acc_out) return ss::fail(SS_EINVAL, "ss_forces: null argument");
     CK(cudaSetDevice(h->device));
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc) return rc;
-    }
-    int rc;
+    int rc = sync_pending(h);
+    if (rc) return rc;
     const size_t vec = h->precision == SS_F32 ? sizeof(float4) : sizeof(double4);
     for (int b = 0; b < 2; ++b)
         if (!h->d_tmp[b] && (rc = h->alloc(&h->d_tmp[b], (size_t)h->N * vec))) return rc;
     if (!h->d_acc && (rc = h->alloc(&h->d_acc, (size_t)h->N * 3 * sizeof(double)))) return rc;
     unsigned long long before = 0;
     CK(cudaMemcpy(&before, h->d_degenerate, sizeof before, cudaMemcpyDeviceToHost));
-    // scale table at time t
-    std::vector<double> tab;
-    if (!h->groups.empty()) {
-        ss_engine tmp_view = {};
-        (void)tmp_view;
-        const size_t G = h->groups.size();
-        tab.resize(G);
-        for (size_t g = 0; g < G; ++g) {
-            const Group &gr = h->groups[g];
-            tab[g] = gr.mode == SS_CONSTANT_EXPANSION
-                         ? 1.0 + gr.amplitude
-                         : 1.0 + gr.amplitude * std::sin(2.0 * M_PI * gr.frequency * t + gr.phase);
-        }
-    }
-    const int grid = (int)((h->N + kBlock - 1) / kBlock);
-    if (h->precision == SS_F32) {
-        if ((rc = upload_scales<float>(h, tab))) return rc;
-        std::vector<float4> tx((size_t)h->N), tv((size_t)h->N);
-        pack_positions<float, float4>(h, x, host_base(h), tx.data());
-        pack_vec<float, float4>(h->N, v, tv.data());
-        if ((rc = upload(h, h->d_tmp[0], tx.data(), tx.size() * sizeof(float4)))) return rc;
-        if ((rc = upload(h, h->d_tmp[1], tv.data(), tv.size() * sizeof(float4)))) return rc;
-        Params<float> p = base_params<float>(h);
-        p.X = (const float4 *)h->d_tmp[0];
-        p.V = (const float4 *)h->d_tmp[1];
-        p.scale = tab.empty() ? nullptr : (const float *)h->scale;
-        p.acc_out = (V3<double> *)h->d_acc;
-        if (h->layout == SS_LAYOUT_ELL) forces_kernel<true, 2><<<grid, kBlock, 0, h->stream>>>(p);
-        else forces_kernel<true, 1><<<grid, kBlock, 0, h->stream>>>(p);
-    } else {
-        if ((rc = upload_scales<double>(h, tab))) return rc;
-        std::vector<double4> tx((size_t)h->N), tv((size_t)h->N);
-        pack_positions<double, double4>(h, x, nullptr, tx.data());
-        pack_vec<double, double4>(h->N, v, tv.data());
-        if ((rc = upload(h, h->d_tmp[0], tx.data(), tx.size() * sizeof(double4)))) return rc;
-        if ((rc = upload(h, h->d_tmp[1], tv.data(), tv.size() * sizeof(double4)))) return rc;
-        Params<double> p = base_params<double>(h);
-        p.X = (const double4 *)h->d_tmp[0];
-        p.V = (const double4 *)h->d_tmp[1];
-        p.scale = tab.empty() ? nullptr : (const double *)h->scale;
-        p.acc_out = (V3<double> *)h->d_acc;
-        if (h->layout == SS_LAYOUT_ELL) forces_kernel<false, 2><<<grid, kBlock, 0, h->stream>>>(p);
-        else forces_kernel<false, 1><<<grid, kBlock, 0, h->stream>>>(p);
-    }
+    rc = h->precision == SS_F32 ? forces_impl<true>(h, x, v, t) : forces_impl<false>(h, x, v, t);
+    if (rc) return rc;
     h->launches += 1;
-    CK(cudaGetLastError());
     if ((rc = download(h, acc_out, h->d_acc, (size_t)h->N * 3 * sizeof(double)))) return rc;
     unsigned long long after = 0;
     CK(cudaMemcpy(&after, h->d_degenerate, sizeof after, cudaMemcpyDeviceToHost));
@@ -736,44 +819,11 @@ int ss_forces(ss_engine *h, const double *x, const double *v, double t, double *
 int ss_get_state(ss_engine *h, double *x, double *v, double *x_prev, int *has_prev) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     CK(cudaSetDevice(h->device));
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc && rc != SS_EDIVERGED) return rc;
-    }
-    int rc;
-    const int64_t N = h->N;
+    int rc = sync_pending(h);
+    if (rc) return rc;
     if (has_prev) *has_prev = h->has_prev ? 1 : 0;
-    if (h->precision == SS_F32) {
-        std::vector<float4> tmp((size_t)N);
-        const float *base = host_base(h);
-        if (x) {
-            if ((rc = download(h, tmp.data(), h->X[h->cur], N * sizeof(float4)))) return rc;
-            unpack_positions<float, float4>(h, tmp.data(), base, x);
-        }
-        if (v) {
-            if ((rc = download(h, tmp.data(), h->V, N * sizeof(float4)))) return rc;
-            unpack_vec<float, float4>(N, tmp.data(), v);
-        }
-        if (x_prev && h->has_prev) {
-            if ((rc = download(h, tmp.data(), h->X[h->cur ^ 1], N * sizeof(float4)))) return rc;
-            unpack_positions<float, float4>(h, tmp.data(), base, x_prev);
-        }
-    } else {
-        std::vector<double4> tmp((size_t)N);
-        if (x) {
-            if ((rc = download(h, tmp.data(), h->X[h->cur], N * sizeof(double4)))) return rc;
-            unpack_positions<double, double4>(h, tmp.data(), nullptr, x);
-        }
-        if (v) {
-            if ((rc = download(h, tmp.data(), h->V, N * sizeof(double4)))) return rc;
-            unpack_vec<double, double4>(N, tmp.data(), v);
-        }
-        if (x_prev && h->has_prev) {
-            if ((rc = download(h, tmp.data(), h->X[h->cur ^ 1], N * sizeof(double4)))) return rc;
-            unpack_positions<double, double4>(h, tmp.data(), nullptr, x_prev);
-        }
-    }
-    return SS_OK;
+    return h->precision == SS_F32 ? get_state_impl<true>(h, x, v, x_prev)
+                                  : get_state_impl<false>(h, x, v, x_prev);
 }
 
 int ss_get_positions(ss_engine *h, double *x) { return ss_get_state(h, x, nullptr, nullptr, nullptr); }
@@ -781,58 +831,24 @@ int ss_get_positions(ss_engine *h, double *x) { return ss_get_state(h, x, nullpt
 int ss_set_state(ss_engine *h, const double *x, const double *v, const double *x_prev) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     CK(cudaSetDevice(h->device));
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc && rc != SS_EDIVERGED) return rc;
-    }
-    int rc;
-    const int64_t N = h->N;
-    if (h->precision == SS_F32) {
-        std::vector<float4> tmp((size_t)N);
-        const float *base = host_base(h);
-        if (x) {
-            pack_positions<float, float4>(h, x, base, tmp.data());
-            if ((rc = upload(h, h->X[h->cur], tmp.data(), N * sizeof(float4)))) return rc;
-        }
-        if (v) {
-            pack_vec<float, float4>(N, v, tmp.data());
-            if ((rc = upload(h, h->V, tmp.data(), N * sizeof(float4)))) return rc;
-        }
-        if (x_prev) {
-            pack_positions<float, float4>(h, x_prev, base, tmp.data());
-            if ((rc = upload(h, h->X[h->cur ^ 1], tmp.data(), N * sizeof(float4)))) return rc;
-        }
-    } else {
-        std::vector<double4> tmp((size_t)N);
-        if (x) {
-            pack_positions<double, double4>(h, x, nullptr, tmp.data());
-            if ((rc = upload(h, h->X[h->cur], tmp.data(), N * sizeof(double4)))) return rc;
-        }
-        if (v) {
-            pack_vec<double, double4>(N, v, tmp.data());
-            if ((rc = upload(h, h->V, tmp.data(), N * sizeof(double4)))) return rc;
-        }
-        if (x_prev) {
-            pack_positions<double, double4>(h, x_prev, nullptr, tmp.data());
-            if ((rc = upload(h, h->X[h->cur ^ 1], tmp.data(), N * sizeof(double4)))) return rc;
-        }
-    }
-    if (x_prev) h->has_prev = true;
-    return SS_OK;
+    int rc = sync_pending(h);
+    if (rc) return rc;
+    return h->precision == SS_F32 ? set_state_impl<true>(h, x, v, x_prev)
+                                  : set_state_impl<false>(h, x, v, x_prev);
 }
 
 int ss_clear_prev(ss_engine *h) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc && rc != SS_EDIVERGED) return rc;
-    }
+    int rc = sync_pending(h);
+    if (rc) return rc;
     h->has_prev = false;
     return SS_OK;
 }
 
 int ss_get_time(ss_engine *h, double *t, int64_t *n) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
+    int rc = sync_pending(h);
+    if (rc) return rc;
     if (t) *t = h->t;
     if (n) *n = h->n;
     return SS_OK;
@@ -840,10 +856,8 @@ int ss_get_time(ss_engine *h, double *t, int64_t *n) {
 
 int ss_set_time(ss_engine *h, double t, int64_t n) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc && rc != SS_EDIVERGED) return rc;
-    }
+    int rc = sync_pending(h);
+    if (rc) return rc;
     h->t = t;
     h->n = n;
     return SS_OK;
@@ -852,20 +866,18 @@ int ss_set_time(ss_engine *h, double t, int64_t n) {
 int ss_set_f_ext(ss_engine *h, const double *f) {
     if (!h || !f) return ss::fail(SS_EINVAL, "ss_set_f_ext: null argument");
     CK(cudaSetDevice(h->device));
-    if (h->pending) {
-        int rc = ss_sync(h, nullptr);
-        if (rc && rc != SS_EDIVERGED) return rc;
-    }
+    int rc = sync_pending(h);
+    if (rc) return rc;
     bool any = false;
     for (int64_t i = 0; i < 3 * h->N && !any; ++i) any = f[i] != 0.0;
     h->has_fext = any;
     if (h->precision == SS_F32) {
         std::vector<float4> tmp((size_t)h->N);
-        pack_vec<float, float4>(h->N, f, tmp.data());
+        pack_vec<float, float4>(h, f, tmp.data());
         return upload(h, h->F, tmp.data(), h->N * sizeof(float4));
     }
     std::vector<double4> tmp((size_t)h->N);
-    pack_vec<double, double4>(h->N, f, tmp.data());
+    pack_vec<double, double4>(h, f, tmp.data());
     return upload(h, h->F, tmp.data(), h->N * sizeof(double4));
 }
 
@@ -903,6 +915,7 @@ int ss_degenerate_count(ss_engine *h, int64_t *count) {
 
 int ss_get_info(ss_engine *h, ss_info *info) {
     if (!h || !info) return ss::fail(SS_EINVAL, "ss_get_info: null argument");
+    std::memset(info, 0, sizeof *info);
     info->n_masses = h->N;
     info->n_springs = h->S;
     info->precision = h->precision;
@@ -911,9 +924,20 @@ int ss_get_info(ss_engine *h, ss_info *info) {
     info->device = h->device;
     info->device_bytes = h->device_bytes;
     info->algorithmic_bytes_per_step = (double)algorithmic_bytes(h);
-    info->ell_width_own = h->lay.W;
-    info->ell_width_ref = h->lay.Wr;
-    info->canonical_order = h->lay.canonical ? 1 : 0;
+    if (h->layout == SS_LAYOUT_TILE) {
+        info->ell_width_own = h->tl.max_W;
+        info->ell_width_ref = h->tl.max_Wr;
+        info->canonical_order = h->tl.canonical ? 1 : 0;
+        info->tile_count = h->tl.n_tiles;
+        info->tile_blob_bytes = (int64_t)h->tl.blob.size();
+        info->tile_halo_ratio = h->tl.halo_ratio;
+        info->tile_foreign_frac = h->tl.foreign_frac;
+        info->smem_per_block = (int32_t)h->smem_bytes;
+    } else {
+        info->ell_width_own = h->lay.W;
+        info->ell_width_ref = h->lay.Wr;
+        info->canonical_order = h->lay.canonical ? 1 : 0;
+    }
     return SS_OK;
 }
 

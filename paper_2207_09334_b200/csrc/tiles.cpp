@@ -1,0 +1,300 @@
+// Host builder of the tiled incidence layout.
+//
+// Masses are renumbered into 4x8x8 bricks of the lattice (generic scenes:
+// bricks of quantised coordinates), and consecutive runs of kTile=256 new
+// ids form a tile, processed by one CTA.  Each spring is owned by its
+// endpoint with the lower ORIGINAL id and stored once, in the owner's tile,
+// as a record (other-endpoint local index u16, k, l0[, group]) in
+// sliced-ELL order.  The other endpoint reaches it through a 2-byte
+// reference: a slot in the same tile's record array, or (owner outside the
+// tile) an entry of the tile's short "foreign" record list.  Per mass the
+// kernel sums references then own records, both in ascending spring id —
+// the reference's serial summation order (_kernels.py:51-70) for every
+// "canonical" mass; a non-canonical mass lists all its incidences as
+// references in spring-id order.  The tile's halo (partners outside the
+// tile) is a list of global ids whose states the CTA stages into shared
+// memory once, so the hot loop reads nothing but shared memory.
+//
+// DRAM bytes per spring ~ 10 (own record) + 2 (ref) + ~0.3 x 10 (foreign
+// copy) + halo ids ~ 16 B in fp32: the SURVEY §8d algorithmic figure.
+
+#include "tiles.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "common.h"
+#include "springsim_b200.h"
+
+namespace ss {
+
+namespace {
+
+inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
+
+void brick_order(const TileInput &in, std::vector<int32_t> &orig_of) {
+    const int64_t N = in.N;
+    orig_of.resize(N);
+    std::iota(orig_of.begin(), orig_of.end(), 0);
+    if (!in.x || N <= kTile) return;
+    // cell size: shortest spring (the lattice pitch for voxel lattices)
+    double h = INFINITY;
+    for (int64_t s = 0; s < in.S; ++s) {
+        const double *a = in.x + 3 * in.si[s], *b = in.x + 3 * in.sj[s];
+        const double d = std::sqrt((b[0] - a[0]) * (b[0] - a[0]) + (b[1] - a[1]) * (b[1] - a[1]) +
+                                   (b[2] - a[2]) * (b[2] - a[2]));
+        if (d > 0 && d < h) h = d;
+    }
+    if (!(h > 0) || !std::isfinite(h)) return;
+    double lo[3] = {INFINITY, INFINITY, INFINITY};
+    for (int64_t i = 0; i < N; ++i)
+        for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], in.x[3 * i + c]);
+    std::vector<int64_t> cell((size_t)N * 3);
+    int64_t mx[3] = {0, 0, 0};
+    for (int64_t i = 0; i < N; ++i)
+        for (int c = 0; c < 3; ++c) {
+            const double q = std::floor((in.x[3 * i + c] - lo[c]) / h + 0.5);
+            const int64_t v = q < 0 ? 0 : (int64_t)q;
+            cell[3 * i + c] = v;
+            mx[c] = std::max(mx[c], v);
+        }
+    const int64_t B[3] = {4, 8, 8};
+    const int64_t nb1 = mx[1] / B[1] + 1, nb2 = mx[2] / B[2] + 1;
+    std::vector<uint64_t> key((size_t)N);
+    for (int64_t i = 0; i < N; ++i) {
+        const int64_t *c = &cell[3 * i];
+        const uint64_t brick = ((uint64_t)(c[0] / B[0]) * nb1 + (uint64_t)(c[1] / B[1])) * nb2 +
+                               (uint64_t)(c[2] / B[2]);
+        const uint64_t inner = (uint64_t)((c[0] % B[0]) * B[1] + (c[1] % B[1])) * B[2] + (c[2] % B[2]);
+        key[i] = (brick << 8) | inner;
+    }
+    std::stable_sort(orig_of.begin(), orig_of.end(),
+                     [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+}
+
+template <typename T>
+void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
+    std::memcpy(blob.data() + off, &v, sizeof(T));
+}
+
+}  // namespace
+
+int build_tiles(const TileInput &in, TileLayout &L) {
+    const int64_t N = in.N, S = in.S;
+    if (N >= (1ll << 31) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
+    L = TileLayout{};
+    if (in.order == 1) brick_order(in, L.orig_of);
+    else {
+        L.orig_of.resize(N);
+        std::iota(L.orig_of.begin(), L.orig_of.end(), 0);
+    }
+    L.new_of.assign(N, 0);
+    for (int64_t i = 0; i < N; ++i) L.new_of[L.orig_of[i]] = (int32_t)i;
+
+    // per-mass own / ref lists (new ids), each ascending in spring id
+    std::vector<int64_t> own_ptr(N + 1, 0), ref_ptr(N + 1, 0);
+    std::vector<int32_t> owner_new(S), other_new(S);
+    for (int64_t s = 0; s < S; ++s) {
+        const int64_t a = std::min(in.si[s], in.sj[s]), b = std::max(in.si[s], in.sj[s]);
+        owner_new[s] = L.new_of[a];
+        other_new[s] = L.new_of[b];
+        own_ptr[owner_new[s] + 1]++;
+        ref_ptr[other_new[s] + 1]++;
+    }
+    for (int64_t m = 0; m < N; ++m) {
+        own_ptr[m + 1] += own_ptr[m];
+        ref_ptr[m + 1] += ref_ptr[m];
+    }
+    std::vector<int32_t> own_sp(S), ref_sp(S);
+    std::vector<uint8_t> q_of(S);
+    {
+        std::vector<int64_t> oc(own_ptr.begin(), own_ptr.end() - 1), rc(ref_ptr.begin(), ref_ptr.end() - 1);
+        for (int64_t s = 0; s < S; ++s) {
+            const int64_t o = owner_new[s];
+            const int64_t q = oc[o] - own_ptr[o];
+            if (q > 255) return fail(SS_EINVAL, "a mass owns more than 255 springs (tiled layout)");
+            q_of[s] = (uint8_t)q;
+            own_sp[oc[o]++] = (int32_t)s;
+            ref_sp[rc[other_new[s]]++] = (int32_t)s;
+        }
+    }
+    std::vector<uint8_t> canon(N);
+    bool all_canon = true;
+    for (int64_t m = 0; m < N; ++m) {
+        const bool c = (ref_ptr[m + 1] == ref_ptr[m]) || (own_ptr[m + 1] == own_ptr[m]) ||
+                       ref_sp[ref_ptr[m + 1] - 1] < own_sp[own_ptr[m]];
+        canon[m] = c;
+        all_canon = all_canon && c;
+    }
+    L.canonical = all_canon;
+
+    const int64_t n_tiles = (N + kTile - 1) / kTile;
+    L.n_tiles = n_tiles;
+    std::vector<std::vector<uint8_t>> parts(n_tiles);
+    std::vector<uint32_t> tW(n_tiles), tWr(n_tiles), tH(n_tiles), tF(n_tiles);
+    std::vector<int64_t> tRefs(n_tiles);
+    const bool has_g = in.group != nullptr;
+    const size_t rs = in.f32 ? 4 : 8;
+    int err = 0;
+
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        if (err) continue;
+        const int64_t base = t * kTile;
+        const int n = (int)std::min<int64_t>(kTile, N - base);
+        int W = 1, Wr = 1;
+        std::vector<int32_t> halo;
+        for (int l = 0; l < n; ++l) {
+            const int64_t m = base + l;
+            const int no = (int)(own_ptr[m + 1] - own_ptr[m]);
+            const int nr = (int)(ref_ptr[m + 1] - ref_ptr[m]) + (canon[m] ? 0 : no);
+            W = std::max(W, no);
+            Wr = std::max(Wr, nr);
+            for (int64_t q = own_ptr[m]; q < own_ptr[m + 1]; ++q) {
+                const int32_t o = other_new[own_sp[q]];
+                if (o < base || o >= base + n) halo.push_back(o);
+            }
+            for (int64_t q = ref_ptr[m]; q < ref_ptr[m + 1]; ++q) {
+                const int32_t o = owner_new[ref_sp[q]];
+                if (o < base || o >= base + n) halo.push_back(o);
+            }
+        }
+        std::sort(halo.begin(), halo.end());
+        halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+        if (W > 127 || Wr > 255 || halo.size() + kTile > 65535) {
+#pragma omp atomic write
+            err = 1;
+            continue;
+        }
+        auto local_of = [&](int32_t g) -> uint16_t {
+            if (g >= base && g < base + n) return (uint16_t)(g - base);
+            const auto it = std::lower_bound(halo.begin(), halo.end(), g);
+            return (uint16_t)(kTile + (it - halo.begin()));
+        };
+        const int slices = (n + 31) / 32;
+        const uint32_t own_n = (uint32_t)slices * W * 32, ref_n = (uint32_t)slices * Wr * 32;
+        // foreign references (owner outside the tile)
+        std::vector<int32_t> foreign;          // spring ids
+        std::vector<uint16_t> refs(ref_n, 0xffff);
+        int64_t n_refs = 0;
+        for (int l = 0; l < n; ++l) {
+            const int64_t m = base + l;
+            // merged list for non-canonical masses
+            int q = 0;
+            auto emit = [&](int32_t s) {
+                const int32_t o = owner_new[s];
+                uint16_t v;
+                if (o >= base && o < base + n) {
+                    const int ol = (int)(o - base);
+                    v = (uint16_t)(((ol >> 5) * W + q_of[s]) * 32 + (ol & 31));
+                } else {
+                    v = (uint16_t)(0x8000 | foreign.size());
+                    foreign.push_back(s);
+                }
+                refs[((l >> 5) * Wr + q) * 32 + (l & 31)] = v;
+                ++q;
+                ++n_refs;
+            };
+            if (canon[m]) {
+                for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r) emit(ref_sp[r]);
+            } else {
+                int64_t a = ref_ptr[m], b = own_ptr[m];
+                while (a < ref_ptr[m + 1] || b < own_ptr[m + 1]) {
+                    if (b >= own_ptr[m + 1] || (a < ref_ptr[m + 1] && ref_sp[a] < own_sp[b])) emit(ref_sp[a++]);
+                    else emit(own_sp[b++]);
+                }
+            }
+        }
+        if (foreign.size() >= 0x8000) {
+#pragma omp atomic write
+            err = 2;
+            continue;
+        }
+        const uint32_t nf = (uint32_t)foreign.size();
+        TileHdr h{};
+        h.n = n; h.W = W; h.Wr = Wr; h.n_halo = (uint32_t)halo.size(); h.n_foreign = nf;
+        uint32_t off = align16(sizeof(TileHdr));
+        h.off_cnt = off; off = align16(off + kTile * 2);
+        h.off_oo = off;  off = align16(off + own_n * 2);
+        h.off_ok = off;  off = align16(off + own_n * rs);
+        h.off_ol = off;  off = align16(off + own_n * rs);
+        h.off_og = 0;
+        if (has_g) { h.off_og = off; off = align16(off + own_n); }
+        h.off_ref = off; off = align16(off + ref_n * 2);
+        h.off_fo = off;  off = align16(off + nf * 2);
+        h.off_fk = off;  off = align16(off + nf * rs);
+        h.off_fl = off;  off = align16(off + nf * rs);
+        h.off_fg = 0;
+        if (has_g) { h.off_fg = off; off = align16(off + nf); }
+        h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
+        h.bytes = off;
+        std::vector<uint8_t> &blob = parts[t];
+        blob.assign(off, 0);
+        std::memcpy(blob.data(), &h, sizeof h);
+        for (int l = 0; l < n; ++l) {
+            const int64_t m = base + l;
+            const int no = canon[m] ? (int)(own_ptr[m + 1] - own_ptr[m]) : 0;
+            const int nr = (int)(ref_ptr[m + 1] - ref_ptr[m]) + (canon[m] ? 0 : (int)(own_ptr[m + 1] - own_ptr[m]));
+            put<uint16_t>(blob, h.off_cnt + 2 * l, (uint16_t)(no | (nr << 8)));
+            for (int64_t q = own_ptr[m]; q < own_ptr[m + 1]; ++q) {
+                const int32_t s = own_sp[q];
+                const uint32_t slot = ((l >> 5) * W + (uint32_t)(q - own_ptr[m])) * 32 + (l & 31);
+                put<uint16_t>(blob, h.off_oo + 2 * slot, local_of(other_new[s]));
+                if (in.f32) {
+                    put<float>(blob, h.off_ok + 4 * slot, (float)in.k[s]);
+                    put<float>(blob, h.off_ol + 4 * slot, (float)in.l0[s]);
+                } else {
+                    put<double>(blob, h.off_ok + 8 * slot, in.k[s]);
+                    put<double>(blob, h.off_ol + 8 * slot, in.l0[s]);
+                }
+                if (has_g) put<int8_t>(blob, h.off_og + slot, (int8_t)in.group[s]);
+            }
+        }
+        std::memcpy(blob.data() + h.off_ref, refs.data(), refs.size() * 2);
+        for (uint32_t f = 0; f < nf; ++f) {
+            const int32_t s = foreign[f];
+            put<uint16_t>(blob, h.off_fo + 2 * f, local_of(owner_new[s]));
+            if (in.f32) {
+                put<float>(blob, h.off_fk + 4 * f, (float)in.k[s]);
+                put<float>(blob, h.off_fl + 4 * f, (float)in.l0[s]);
+            } else {
+                put<double>(blob, h.off_fk + 8 * f, in.k[s]);
+                put<double>(blob, h.off_fl + 8 * f, in.l0[s]);
+            }
+            if (has_g) put<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
+        }
+        std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
+        tW[t] = W; tWr[t] = Wr; tH[t] = (uint32_t)halo.size(); tF[t] = nf; tRefs[t] = n_refs;
+    }
+    if (err == 1) return fail(SS_EINVAL, "tile exceeds layout limits (degree or halo too large)");
+    if (err == 2) return fail(SS_EINVAL, "tile has too many foreign references");
+    if (in.group) {
+        for (int64_t s = 0; s < S; ++s)
+            if (in.group[s] > 127) return fail(SS_EINVAL, "at most 128 actuation groups in the tiled layout");
+    }
+
+    L.off.assign(n_tiles + 1, 0);
+    for (int64_t t = 0; t < n_tiles; ++t) L.off[t + 1] = L.off[t] + parts[t].size();
+    L.blob.resize(L.off[n_tiles]);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n_tiles; ++t)
+        std::memcpy(L.blob.data() + L.off[t], parts[t].data(), parts[t].size());
+    double hsum = 0, fsum = 0, rsum = 0;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        L.max_tile_bytes = std::max<uint32_t>(L.max_tile_bytes, (uint32_t)parts[t].size());
+        L.max_halo = std::max(L.max_halo, tH[t]);
+        L.max_W = std::max<int>(L.max_W, (int)tW[t]);
+        L.max_Wr = std::max<int>(L.max_Wr, (int)tWr[t]);
+        const int n = (int)std::min<int64_t>(kTile, N - t * kTile);
+        hsum += (double)(n + tH[t]) / n;
+        fsum += tF[t];
+        rsum += (double)tRefs[t];
+    }
+    L.halo_ratio = hsum / (double)n_tiles;
+    L.foreign_frac = rsum > 0 ? fsum / rsum : 0.0;
+    return SS_OK;
+}
+
+}  // namespace ss

@@ -51,7 +51,8 @@ RK4 = "rk4"
 INTEGRATORS = (EULER, VERLET, RK4)
 
 PRECISIONS = ("f64", "f32")
-LAYOUTS = {"auto": _lib.SS_LAYOUT_AUTO, "csr": _lib.SS_LAYOUT_CSR, "ell": _lib.SS_LAYOUT_ELL}
+LAYOUTS = {"auto": _lib.SS_LAYOUT_AUTO, "csr": _lib.SS_LAYOUT_CSR, "ell": _lib.SS_LAYOUT_ELL,
+           "tile": _lib.SS_LAYOUT_TILE}
 
 DEGENERATE_LENGTH = 1e-12          # _kernels.py:23
 _INTEG = {EULER: _lib.SS_EULER, VERLET: _lib.SS_VERLET, RK4: _lib.SS_RK4}

@@ -26,7 +26,7 @@ def run_engine(case, layout, precision="f64"):
     return d, eng
 
 
-@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("layout", ["csr", "ell", "tile"])
 @pytest.mark.parametrize("case", golden_cases())
 def test_fp64_bitwise_vs_reference(case, layout):
     d, eng = run_engine(case, layout)
@@ -42,7 +42,7 @@ def test_fp64_bitwise_vs_reference(case, layout):
         assert eng.degenerate_springs == int(d[f"deg_{c}"])
 
 
-@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("layout", ["csr", "ell", "tile"])
 @pytest.mark.parametrize("case", [c for c in golden_cases() if "degenerate" not in c])
 def test_fp32_within_tolerance(case, layout):
     d, eng = run_engine(case, layout, precision="f32")
@@ -57,7 +57,7 @@ def test_fp32_within_tolerance(case, layout):
         assert err <= FP32_TOL, (case, layout, c, err)
 
 
-@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("layout", ["csr", "ell", "tile"])
 def test_divergence_names_mass_and_step(layout):
     d = load_golden("divergence_euler")
     eng = Engine(golden_scene(d), integrator="euler", layout=layout)
@@ -71,7 +71,7 @@ def test_divergence_names_mass_and_step(layout):
     assert eng.v.tobytes() == d["v_div"].tobytes()
 
 
-@pytest.mark.parametrize("layout", ["csr", "ell"])
+@pytest.mark.parametrize("layout", ["csr", "ell", "tile"])
 def test_forces_bitwise(layout):
     d = load_golden("forces_block6")
     eng = Engine(golden_scene(d), layout=layout)
