@@ -177,6 +177,10 @@ typedef struct ss_info {
 } ss_info;
 int ss_get_info(ss_engine *h, ss_info *info);
 
+/* Host-only: build the tiled layout of a scene description (no device
+ * needed) and report its statistics in `info`. */
+int ss_plan(const ss_scene_desc *desc, ss_info *info);
+
 /* Kernel launches issued so far (for the bench's gpu_launches claim). */
 int64_t ss_launch_count(ss_engine *h);
 

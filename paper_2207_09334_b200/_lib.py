@@ -84,6 +84,7 @@ SIGNATURES = {
     "ss_degenerate_count": (C.c_int, [C.c_void_p, _i64p]),
     "ss_get_info": (C.c_int, [C.c_void_p, C.POINTER(Info)]),
     "ss_launch_count": (C.c_int64, [C.c_void_p]),
+    "ss_plan": (C.c_int, [C.POINTER(SceneDesc), C.POINTER(Info)]),
     "ss_lattice_box": (C.c_int, [_dp, _dp, C.c_double, C.c_double, C.c_double,
                                  C.c_int64, C.c_int64, _i64p, _i64p, _i64p,
                                  _dp, _i64p, _i64p, _dp, _dp, _i64p]),

@@ -54,6 +54,7 @@ struct ss_engine {
     cudaStream_t stream = nullptr;
     int precision = SS_F64, layout = SS_LAYOUT_CSR, integrator = SS_VERLET;
     int64_t N = 0, S = 0;
+    int64_t ND = 0;                // device mass slots (TILE: padded to whole tiles)
 
     // host-side scalars (engine.py:190-194, 222-224)
     double dt = 1e-4, damping = 0.0, gravity[3] = {0, 0, 0};
@@ -94,6 +95,7 @@ struct ss_engine {
     int2 *inc = nullptr;
     unsigned char *d_blob = nullptr;
     unsigned long long *d_toff = nullptr;
+    unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     int64_t device_bytes = 0;
@@ -122,6 +124,7 @@ struct ss_engine {
     }
 
     int64_t src_of(int64_t i) const { return orig_of.empty() ? i : orig_of[i]; }
+    int grid() const { return (int)((ND + kBlockThreads - 1) / kBlockThreads); }
 };
 
 namespace {
@@ -133,9 +136,13 @@ namespace {
 template <typename T, typename T4>
 void pack_positions(const ss_engine *h, const double *x, T4 *out) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->N; ++i) {
+    for (int64_t i = 0; i < h->ND; ++i) {
         const int64_t s = h->src_of(i);
-        T4 o;
+        T4 o{};
+        if (s < 0) {                 // padding slot
+            out[i] = o;
+            continue;
+        }
         const double w = h->fixed[s] ? -h->m[s] : h->m[s];
         if constexpr (std::is_same<T, float>::value) {
             const float *b = h->base.data() + 4 * i;
@@ -156,9 +163,13 @@ void pack_positions(const ss_engine *h, const double *x, T4 *out) {
 template <typename T, typename T4>
 void pack_vec(const ss_engine *h, const double *v, T4 *out) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->N; ++i) {
+    for (int64_t i = 0; i < h->ND; ++i) {
         const int64_t s = h->src_of(i);
-        T4 o;
+        T4 o{};
+        if (s < 0) {
+            out[i] = o;
+            continue;
+        }
         o.x = (T)v[3 * s + 0];
         o.y = (T)v[3 * s + 1];
         o.z = (T)v[3 * s + 2];
@@ -170,8 +181,9 @@ void pack_vec(const ss_engine *h, const double *v, T4 *out) {
 template <typename T, typename T4>
 void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->N; ++i) {
+    for (int64_t i = 0; i < h->ND; ++i) {
         const int64_t s = h->src_of(i);
+        if (s < 0) continue;
         if constexpr (std::is_same<T, float>::value) {
             const float *b = h->base.data() + 4 * i;
             x[3 * s + 0] = (double)b[0] + (double)in[i].x;
@@ -188,8 +200,9 @@ void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
 template <typename T, typename T4>
 void unpack_vec(const ss_engine *h, const T4 *in, double *v) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->N; ++i) {
+    for (int64_t i = 0; i < h->ND; ++i) {
         const int64_t s = h->src_of(i);
+        if (s < 0) continue;
         v[3 * s + 0] = (double)in[i].x;
         v[3 * s + 1] = (double)in[i].y;
         v[3 * s + 2] = (double)in[i].z;
@@ -264,7 +277,7 @@ template <typename T>
 Params<T> base_params(const ss_engine *h) {
     using T4 = typename Params<T>::T4;
     Params<T> p{};
-    p.n = (int)h->N;
+    p.n = (int)h->ND;
     p.P = reinterpret_cast<const T4 *>(h->P);
     p.F = h->has_fext ? reinterpret_cast<const T4 *>(h->F) : nullptr;
     p.orig_of = h->d_orig_of;
@@ -284,6 +297,7 @@ Params<T> base_params(const ss_engine *h) {
     tp.Wr = h->lay.Wr;
     tp.blob = h->d_blob;
     tp.toff = h->d_toff;
+    tp.tsplit = h->d_tsplit;
     tp.blob_smem = h->blob_smem;
     tp.max_halo = h->max_halo;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
@@ -313,7 +327,9 @@ int with_layout(const ss_engine *h, Fn &&fn) {
     switch (h->layout) {
         case SS_LAYOUT_CSR: return fn(std::integral_constant<int, 1>{});
         case SS_LAYOUT_ELL: return fn(std::integral_constant<int, 2>{});
-        default: return fn(std::integral_constant<int, 3>{});
+        default:
+            if (h->tl.canonical && h->groups.empty()) return fn(std::integral_constant<int, 4>{});
+            return fn(std::integral_constant<int, 3>{});
     }
 }
 
@@ -329,8 +345,8 @@ int launch_steps(ss_engine *h, int64_t count) {
         int rc = upload_scales<T>(h, tab);
         if (rc) return rc;
     }
-    const int grid = (int)((h->N + kBlock - 1) / kBlock);
-    const size_t smem = LAYOUT == 3 ? h->smem_bytes : 0;
+    const int grid = h->grid();
+    const size_t smem = LAYOUT >= 3 ? h->smem_bytes : 0;
     Params<T> p = base_params<T>(h);
     const T *scale = reinterpret_cast<const T *>(h->scale);
     for (int64_t s = 0; s < count; ++s) {
@@ -386,17 +402,23 @@ int dispatch_steps(ss_engine *h, int64_t count) {
     });
 }
 
+template <bool F32, int LY>
+int set_tile_smem_ly(size_t bytes) {
+    const int b = (int)bytes;
+    CK(cudaFuncSetAttribute(step_kernel<F32, 0, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(step_kernel<F32, 1, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 1, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 2, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 3, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(rk4_kernel<F32, 4, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(forces_kernel<F32, LY>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    return SS_OK;
+}
+
 template <bool F32>
 int set_tile_smem(size_t bytes) {
-    const int b = (int)bytes;
-    CK(cudaFuncSetAttribute(step_kernel<F32, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(step_kernel<F32, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(rk4_kernel<F32, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(rk4_kernel<F32, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(rk4_kernel<F32, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(rk4_kernel<F32, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(forces_kernel<F32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    return SS_OK;
+    int rc = set_tile_smem_ly<F32, 3>(bytes);
+    return rc ? rc : set_tile_smem_ly<F32, 4>(bytes);
 }
 
 int reset_divergence(ss_engine *h) {
@@ -467,11 +489,12 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         }
     }
     h->layout = layout;
+    h->ND = N;
     if (layout == SS_LAYOUT_TILE) {
-        bool identity = true;
-        for (int64_t i = 0; i < N && identity; ++i) identity = h->tl.orig_of[i] == i;
-        if (!identity) h->orig_of = h->tl.orig_of;
+        h->orig_of = h->tl.orig_of;        // padded slot order
+        h->ND = (int64_t)h->orig_of.size();
     }
+    const int64_t ND = h->ND;
     if (!h->orig_of.empty()) {
         void *p;
         if ((rc = up_vec(h, &p, h->orig_of))) return rc;
@@ -479,36 +502,37 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     }
     // ---- fp32 base positions (device order)
     if (F32) {
-        h->base.resize((size_t)N * 4);
-        for (int64_t i = 0; i < N; ++i) {
+        h->base.assign((size_t)ND * 4, 0.f);
+        for (int64_t i = 0; i < ND; ++i) {
             const int64_t s = h->src_of(i);
+            if (s < 0) continue;
             for (int c = 0; c < 3; ++c) h->base[4 * i + c] = (float)d->x[3 * s + c];
-            h->base[4 * i + 3] = 0.f;
         }
-        if ((rc = h->alloc(&h->P, (size_t)N * sizeof(T4)))) return rc;
-        if ((rc = upload(h, h->P, h->base.data(), (size_t)N * sizeof(T4)))) return rc;
+        if ((rc = h->alloc(&h->P, (size_t)ND * sizeof(T4)))) return rc;
+        if ((rc = upload(h, h->P, h->base.data(), (size_t)ND * sizeof(T4)))) return rc;
     }
     for (int b = 0; b < 2; ++b)
-        if ((rc = h->alloc(&h->X[b], (size_t)N * sizeof(T4)))) return rc;
-    if ((rc = h->alloc(&h->V, (size_t)N * sizeof(T4)))) return rc;
-    if ((rc = h->alloc(&h->F, (size_t)N * sizeof(T4)))) return rc;
+        if ((rc = h->alloc(&h->X[b], (size_t)ND * sizeof(T4)))) return rc;
+    if ((rc = h->alloc(&h->V, (size_t)ND * sizeof(T4)))) return rc;
+    if ((rc = h->alloc(&h->F, (size_t)ND * sizeof(T4)))) return rc;
     if (h->integrator == SS_RK4) {
         for (void **b : {&h->XA, &h->XB, &h->VS, &h->SV, &h->SA})
-            if ((rc = h->alloc(b, (size_t)N * sizeof(T4)))) return rc;
+            if ((rc = h->alloc(b, (size_t)ND * sizeof(T4)))) return rc;
     }
     {
-        std::vector<T4> tmp((size_t)N);
+        std::vector<T4> tmp((size_t)ND);
         pack_positions<T, T4>(h, d->x, tmp.data());
-        if ((rc = upload(h, h->X[0], tmp.data(), (size_t)N * sizeof(T4)))) return rc;
+        if ((rc = upload(h, h->X[0], tmp.data(), (size_t)ND * sizeof(T4)))) return rc;
+        if ((rc = upload(h, h->X[1], tmp.data(), (size_t)ND * sizeof(T4)))) return rc;
         pack_vec<T, T4>(h, d->v, tmp.data());
-        if ((rc = upload(h, h->V, tmp.data(), (size_t)N * sizeof(T4)))) return rc;
+        if ((rc = upload(h, h->V, tmp.data(), (size_t)ND * sizeof(T4)))) return rc;
         if (d->f_ext) {
             pack_vec<T, T4>(h, d->f_ext, tmp.data());
             for (int64_t i = 0; i < 3 * N && !h->has_fext; ++i) h->has_fext = d->f_ext[i] != 0.0;
         } else {
-            std::memset(tmp.data(), 0, (size_t)N * sizeof(T4));
+            std::memset(tmp.data(), 0, (size_t)ND * sizeof(T4));
         }
-        if ((rc = upload(h, h->F, tmp.data(), (size_t)N * sizeof(T4)))) return rc;
+        if ((rc = upload(h, h->F, tmp.data(), (size_t)ND * sizeof(T4)))) return rc;
     }
     const bool has_g = d->group && !h->groups.empty();
     if (layout == SS_LAYOUT_TILE) {
@@ -519,6 +543,8 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         std::vector<unsigned long long> off(L.off.begin(), L.off.end());
         if ((rc = up_vec(h, &p, off))) return rc;
         h->d_toff = reinterpret_cast<unsigned long long *>(p);
+        if ((rc = up_vec(h, &p, L.split))) return rc;
+        h->d_tsplit = reinterpret_cast<unsigned int *>(p);
         h->blob_smem = (L.max_tile_bytes + 127u) & ~127u;
         h->max_halo = L.max_halo;
         h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4) * (F32 ? 2 : 1);
@@ -600,7 +626,7 @@ int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
         scales_at(h, t, tab.data());
         if ((rc = upload_scales<T>(h, tab))) return rc;
     }
-    std::vector<T4> tx((size_t)h->N), tv((size_t)h->N);
+    std::vector<T4> tx((size_t)h->ND), tv((size_t)h->ND);
     pack_positions<T, T4>(h, x, tx.data());
     pack_vec<T, T4>(h, v, tv.data());
     if ((rc = upload(h, h->d_tmp[0], tx.data(), tx.size() * sizeof(T4)))) return rc;
@@ -610,10 +636,10 @@ int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
     p.V = (const T4 *)h->d_tmp[1];
     p.scale = tab.empty() ? nullptr : (const T *)h->scale;
     p.acc_out = (V3<double> *)h->d_acc;
-    const int grid = (int)((h->N + kBlock - 1) / kBlock);
+    const int grid = h->grid();
     return with_layout(h, [&](auto L) -> int {
         constexpr int LY = decltype(L)::value;
-        forces_kernel<F32, LY><<<grid, kBlock, LY == 3 ? h->smem_bytes : 0, h->stream>>>(p);
+        forces_kernel<F32, LY><<<grid, kBlock, LY >= 3 ? h->smem_bytes : 0, h->stream>>>(p);
         CK(cudaGetLastError());
         return SS_OK;
     });
@@ -623,8 +649,8 @@ template <bool F32>
 int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
-    std::vector<T4> tmp((size_t)h->N);
-    const size_t bytes = (size_t)h->N * sizeof(T4);
+    std::vector<T4> tmp((size_t)h->ND);
+    const size_t bytes = (size_t)h->ND * sizeof(T4);
     int rc;
     if (x) {
         if ((rc = download(h, tmp.data(), h->X[h->cur], bytes))) return rc;
@@ -645,8 +671,8 @@ template <bool F32>
 int set_state_impl(ss_engine *h, const double *x, const double *v, const double *x_prev) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
-    std::vector<T4> tmp((size_t)h->N);
-    const size_t bytes = (size_t)h->N * sizeof(T4);
+    std::vector<T4> tmp((size_t)h->ND);
+    const size_t bytes = (size_t)h->ND * sizeof(T4);
     int rc;
     if (x) {
         pack_positions<T, T4>(h, x, tmp.data());
@@ -802,7 +828,7 @@ int ss_forces(ss_engine *h, const double *x, const double *v, double t, double *
     if (rc) return rc;
     const size_t vec = h->precision == SS_F32 ? sizeof(float4) : sizeof(double4);
     for (int b = 0; b < 2; ++b)
-        if (!h->d_tmp[b] && (rc = h->alloc(&h->d_tmp[b], (size_t)h->N * vec))) return rc;
+        if (!h->d_tmp[b] && (rc = h->alloc(&h->d_tmp[b], (size_t)h->ND * vec))) return rc;
     if (!h->d_acc && (rc = h->alloc(&h->d_acc, (size_t)h->N * 3 * sizeof(double)))) return rc;
     unsigned long long before = 0;
     CK(cudaMemcpy(&before, h->d_degenerate, sizeof before, cudaMemcpyDeviceToHost));
@@ -872,13 +898,13 @@ int ss_set_f_ext(ss_engine *h, const double *f) {
     for (int64_t i = 0; i < 3 * h->N && !any; ++i) any = f[i] != 0.0;
     h->has_fext = any;
     if (h->precision == SS_F32) {
-        std::vector<float4> tmp((size_t)h->N);
+        std::vector<float4> tmp((size_t)h->ND);
         pack_vec<float, float4>(h, f, tmp.data());
-        return upload(h, h->F, tmp.data(), h->N * sizeof(float4));
+        return upload(h, h->F, tmp.data(), h->ND * sizeof(float4));
     }
-    std::vector<double4> tmp((size_t)h->N);
+    std::vector<double4> tmp((size_t)h->ND);
     pack_vec<double, double4>(h, f, tmp.data());
-    return upload(h, h->F, tmp.data(), h->N * sizeof(double4));
+    return upload(h, h->F, tmp.data(), h->ND * sizeof(double4));
 }
 
 int ss_set_damping(ss_engine *h, double damping) {
@@ -944,3 +970,36 @@ int ss_get_info(ss_engine *h, ss_info *info) {
 int64_t ss_launch_count(ss_engine *h) { return h ? h->launches : 0; }
 
 }  // extern "C"
+
+// Host-only planning: build the tiled layout of a scene without touching the
+// device and report its statistics (used by tests and to size shards).
+extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
+    if (!d || !info) return ss::fail(SS_EINVAL, "ss_plan: null argument");
+    if (d->n_masses <= 0 || !d->x || (d->n_springs && (!d->si || !d->sj || !d->k || !d->l0)))
+        return ss::fail(SS_EINVAL, "ss_plan: incomplete scene");
+    const bool f32 = d->precision == SS_F32;
+    TileInput ti{d->n_masses, d->n_springs, d->si, d->sj, d->x, d->k, d->l0,
+                 (d->group && d->n_groups) ? d->group : nullptr, f32, 1};
+    TileLayout tl;
+    int rc = build_tiles(ti, tl);
+    if (rc) return rc;
+    std::memset(info, 0, sizeof *info);
+    info->n_masses = d->n_masses;
+    info->n_springs = d->n_springs;
+    info->precision = d->precision;
+    info->layout = SS_LAYOUT_TILE;
+    info->integrator = d->integrator;
+    info->ell_width_own = tl.max_W;
+    info->ell_width_ref = tl.max_Wr;
+    info->canonical_order = tl.canonical ? 1 : 0;
+    info->tile_count = tl.n_tiles;
+    info->tile_blob_bytes = (int64_t)tl.blob.size();
+    info->tile_halo_ratio = tl.halo_ratio;
+    info->tile_foreign_frac = tl.foreign_frac;
+    const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
+    info->smem_per_block =
+        (int32_t)(128 + ((tl.max_tile_bytes + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec * (f32 ? 2 : 1));
+    const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
+    info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
+    return SS_OK;
+}

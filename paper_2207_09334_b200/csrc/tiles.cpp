@@ -34,44 +34,83 @@ namespace {
 
 inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
 
-void brick_order(const TileInput &in, std::vector<int32_t> &orig_of) {
+// Device slot order: tile t owns slots [256t, 256t+256); real masses fill a
+// tile's first n slots, the rest are padding (-1).  With order == 1 the
+// masses are sorted into 4x8x8 bricks of quantised coordinates and whole
+// bricks are packed into tiles, so tiles never straddle brick boundaries.
+void tile_order(const TileInput &in, std::vector<int32_t> &orig_of) {
     const int64_t N = in.N;
-    orig_of.resize(N);
-    std::iota(orig_of.begin(), orig_of.end(), 0);
-    if (!in.x || N <= kTile) return;
-    // cell size: shortest spring (the lattice pitch for voxel lattices)
-    double h = INFINITY;
-    for (int64_t s = 0; s < in.S; ++s) {
-        const double *a = in.x + 3 * in.si[s], *b = in.x + 3 * in.sj[s];
-        const double d = std::sqrt((b[0] - a[0]) * (b[0] - a[0]) + (b[1] - a[1]) * (b[1] - a[1]) +
-                                   (b[2] - a[2]) * (b[2] - a[2]));
-        if (d > 0 && d < h) h = d;
-    }
-    if (!(h > 0) || !std::isfinite(h)) return;
-    double lo[3] = {INFINITY, INFINITY, INFINITY};
-    for (int64_t i = 0; i < N; ++i)
-        for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], in.x[3 * i + c]);
-    std::vector<int64_t> cell((size_t)N * 3);
-    int64_t mx[3] = {0, 0, 0};
-    for (int64_t i = 0; i < N; ++i)
-        for (int c = 0; c < 3; ++c) {
-            const double q = std::floor((in.x[3 * i + c] - lo[c]) / h + 0.5);
-            const int64_t v = q < 0 ? 0 : (int64_t)q;
-            cell[3 * i + c] = v;
-            mx[c] = std::max(mx[c], v);
+    std::vector<int32_t> sorted(N);
+    std::iota(sorted.begin(), sorted.end(), 0);
+    std::vector<uint64_t> brick_of;
+    bool bricks = false;
+    if (in.order == 1 && in.x && N > kTile) {
+        // cell size: shortest spring (the lattice pitch for voxel lattices)
+        double h = INFINITY;
+        for (int64_t s = 0; s < in.S; ++s) {
+            const double *a = in.x + 3 * in.si[s], *b = in.x + 3 * in.sj[s];
+            const double d = std::sqrt((b[0] - a[0]) * (b[0] - a[0]) + (b[1] - a[1]) * (b[1] - a[1]) +
+                                       (b[2] - a[2]) * (b[2] - a[2]));
+            if (d > 0 && d < h) h = d;
         }
-    const int64_t B[3] = {4, 8, 8};
-    const int64_t nb1 = mx[1] / B[1] + 1, nb2 = mx[2] / B[2] + 1;
-    std::vector<uint64_t> key((size_t)N);
-    for (int64_t i = 0; i < N; ++i) {
-        const int64_t *c = &cell[3 * i];
-        const uint64_t brick = ((uint64_t)(c[0] / B[0]) * nb1 + (uint64_t)(c[1] / B[1])) * nb2 +
-                               (uint64_t)(c[2] / B[2]);
-        const uint64_t inner = (uint64_t)((c[0] % B[0]) * B[1] + (c[1] % B[1])) * B[2] + (c[2] % B[2]);
-        key[i] = (brick << 8) | inner;
+        if (h > 0 && std::isfinite(h)) {
+            double lo[3] = {INFINITY, INFINITY, INFINITY};
+            for (int64_t i = 0; i < N; ++i)
+                for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], in.x[3 * i + c]);
+            std::vector<int64_t> cell((size_t)N * 3);
+            int64_t mx[3] = {0, 0, 0};
+            for (int64_t i = 0; i < N; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    const double q = std::floor((in.x[3 * i + c] - lo[c]) / h + 0.5);
+                    const int64_t v = q < 0 ? 0 : (int64_t)q;
+                    cell[3 * i + c] = v;
+                    mx[c] = std::max(mx[c], v);
+                }
+            const int64_t B[3] = {4, 8, 8};
+            const int64_t nb1 = mx[1] / B[1] + 1, nb2 = mx[2] / B[2] + 1;
+            std::vector<uint64_t> key((size_t)N);
+            brick_of.resize(N);
+            for (int64_t i = 0; i < N; ++i) {
+                const int64_t *c = &cell[3 * i];
+                const uint64_t brick = ((uint64_t)(c[0] / B[0]) * nb1 + (uint64_t)(c[1] / B[1])) * nb2 +
+                                       (uint64_t)(c[2] / B[2]);
+                const uint64_t inner =
+                    (uint64_t)((c[0] % B[0]) * B[1] + (c[1] % B[1])) * B[2] + (c[2] % B[2]);
+                brick_of[i] = brick;
+                key[i] = (brick << 8) | inner;
+            }
+            std::stable_sort(sorted.begin(), sorted.end(),
+                             [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+            bricks = true;
+        }
     }
-    std::stable_sort(orig_of.begin(), orig_of.end(),
-                     [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    orig_of.clear();
+    orig_of.reserve((size_t)N + N / 4 + kTile);
+    auto pad_tile = [&]() {
+        while (orig_of.size() % kTile) orig_of.push_back(-1);
+    };
+    if (!bricks) {
+        orig_of.assign(sorted.begin(), sorted.end());
+        pad_tile();
+        return;
+    }
+    int64_t i = 0;
+    while (i < N) {
+        int64_t j = i;
+        while (j < N && brick_of[sorted[j]] == brick_of[sorted[i]]) ++j;
+        const int64_t size = j - i;
+        const int64_t fill = (int64_t)(orig_of.size() % kTile);
+        if (size > kTile) {
+            pad_tile();
+            for (int64_t q = i; q < j; ++q) orig_of.push_back(sorted[q]);
+            pad_tile();
+        } else {
+            if (fill && fill + size > kTile) pad_tile();
+            for (int64_t q = i; q < j; ++q) orig_of.push_back(sorted[q]);
+        }
+        i = j;
+    }
+    pad_tile();
 }
 
 template <typename T>
@@ -83,18 +122,16 @@ void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 
 int build_tiles(const TileInput &in, TileLayout &L) {
     const int64_t N = in.N, S = in.S;
-    if (N >= (1ll << 31) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
+    if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
-    if (in.order == 1) brick_order(in, L.orig_of);
-    else {
-        L.orig_of.resize(N);
-        std::iota(L.orig_of.begin(), L.orig_of.end(), 0);
-    }
-    L.new_of.assign(N, 0);
-    for (int64_t i = 0; i < N; ++i) L.new_of[L.orig_of[i]] = (int32_t)i;
+    tile_order(in, L.orig_of);
+    const int64_t D = (int64_t)L.orig_of.size();          // device slots, multiple of kTile
+    L.new_of.assign(N, -1);
+    for (int64_t i = 0; i < D; ++i)
+        if (L.orig_of[i] >= 0) L.new_of[L.orig_of[i]] = (int32_t)i;
 
-    // per-mass own / ref lists (new ids), each ascending in spring id
-    std::vector<int64_t> own_ptr(N + 1, 0), ref_ptr(N + 1, 0);
+    // per-slot own / ref lists, each ascending in spring id
+    std::vector<int64_t> own_ptr(D + 1, 0), ref_ptr(D + 1, 0);
     std::vector<int32_t> owner_new(S), other_new(S);
     for (int64_t s = 0; s < S; ++s) {
         const int64_t a = std::min(in.si[s], in.sj[s]), b = std::max(in.si[s], in.sj[s]);
@@ -103,7 +140,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
         own_ptr[owner_new[s] + 1]++;
         ref_ptr[other_new[s] + 1]++;
     }
-    for (int64_t m = 0; m < N; ++m) {
+    for (int64_t m = 0; m < D; ++m) {
         own_ptr[m + 1] += own_ptr[m];
         ref_ptr[m + 1] += ref_ptr[m];
     }
@@ -120,9 +157,9 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             ref_sp[rc[other_new[s]]++] = (int32_t)s;
         }
     }
-    std::vector<uint8_t> canon(N);
+    std::vector<uint8_t> canon(D);
     bool all_canon = true;
-    for (int64_t m = 0; m < N; ++m) {
+    for (int64_t m = 0; m < D; ++m) {
         const bool c = (ref_ptr[m + 1] == ref_ptr[m]) || (own_ptr[m + 1] == own_ptr[m]) ||
                        ref_sp[ref_ptr[m + 1] - 1] < own_sp[own_ptr[m]];
         canon[m] = c;
@@ -130,10 +167,10 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     }
     L.canonical = all_canon;
 
-    const int64_t n_tiles = (N + kTile - 1) / kTile;
+    const int64_t n_tiles = D / kTile;
     L.n_tiles = n_tiles;
     std::vector<std::vector<uint8_t>> parts(n_tiles);
-    std::vector<uint32_t> tW(n_tiles), tWr(n_tiles), tH(n_tiles), tF(n_tiles);
+    std::vector<uint32_t> tW(n_tiles), tWr(n_tiles), tH(n_tiles), tF(n_tiles), tSplit(n_tiles), tN(n_tiles);
     std::vector<int64_t> tRefs(n_tiles);
     const bool has_g = in.group != nullptr;
     const size_t rs = in.f32 ? 4 : 8;
@@ -143,7 +180,8 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     for (int64_t t = 0; t < n_tiles; ++t) {
         if (err) continue;
         const int64_t base = t * kTile;
-        const int n = (int)std::min<int64_t>(kTile, N - base);
+        int n = 0;
+        while (n < kTile && L.orig_of[base + n] >= 0) ++n;
         int W = 1, Wr = 1;
         std::vector<int32_t> halo;
         for (int l = 0; l < n; ++l) {
@@ -187,8 +225,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
                 const int32_t o = owner_new[s];
                 uint16_t v;
                 if (o >= base && o < base + n) {
-                    const int ol = (int)(o - base);
-                    v = (uint16_t)(((ol >> 5) * W + q_of[s]) * 32 + (ol & 31));
+                    v = (uint16_t)(((uint32_t)q_of[s] << 8) | (uint32_t)(o - base));
                 } else {
                     v = (uint16_t)(0x8000 | foreign.size());
                     foreign.push_back(s);
@@ -213,22 +250,23 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             continue;
         }
         const uint32_t nf = (uint32_t)foreign.size();
+        bool tile_canon = true;
+        for (int l = 0; l < n; ++l) tile_canon = tile_canon && canon[base + l];
         TileHdr h{};
         h.n = n; h.W = W; h.Wr = Wr; h.n_halo = (uint32_t)halo.size(); h.n_foreign = nf;
+        h.canonical = tile_canon ? 1u : 0u;
         uint32_t off = align16(sizeof(TileHdr));
+        h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
         h.off_cnt = off; off = align16(off + kTile * 2);
         h.off_oo = off;  off = align16(off + own_n * 2);
-        h.off_ok = off;  off = align16(off + own_n * rs);
-        h.off_ol = off;  off = align16(off + own_n * rs);
+        h.off_okl = off; off = align16(off + own_n * 2 * rs);
         h.off_og = 0;
         if (has_g) { h.off_og = off; off = align16(off + own_n); }
         h.off_ref = off; off = align16(off + ref_n * 2);
         h.off_fo = off;  off = align16(off + nf * 2);
-        h.off_fk = off;  off = align16(off + nf * rs);
-        h.off_fl = off;  off = align16(off + nf * rs);
+        h.off_fkl = off; off = align16(off + nf * 2 * rs);
         h.off_fg = 0;
         if (has_g) { h.off_fg = off; off = align16(off + nf); }
-        h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
         h.bytes = off;
         std::vector<uint8_t> &blob = parts[t];
         blob.assign(off, 0);
@@ -243,11 +281,11 @@ int build_tiles(const TileInput &in, TileLayout &L) {
                 const uint32_t slot = ((l >> 5) * W + (uint32_t)(q - own_ptr[m])) * 32 + (l & 31);
                 put<uint16_t>(blob, h.off_oo + 2 * slot, local_of(other_new[s]));
                 if (in.f32) {
-                    put<float>(blob, h.off_ok + 4 * slot, (float)in.k[s]);
-                    put<float>(blob, h.off_ol + 4 * slot, (float)in.l0[s]);
+                    put<float>(blob, h.off_okl + 8 * slot, (float)in.k[s]);
+                    put<float>(blob, h.off_okl + 8 * slot + 4, (float)in.l0[s]);
                 } else {
-                    put<double>(blob, h.off_ok + 8 * slot, in.k[s]);
-                    put<double>(blob, h.off_ol + 8 * slot, in.l0[s]);
+                    put<double>(blob, h.off_okl + 16 * slot, in.k[s]);
+                    put<double>(blob, h.off_okl + 16 * slot + 8, in.l0[s]);
                 }
                 if (has_g) put<int8_t>(blob, h.off_og + slot, (int8_t)in.group[s]);
             }
@@ -257,16 +295,18 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             const int32_t s = foreign[f];
             put<uint16_t>(blob, h.off_fo + 2 * f, local_of(owner_new[s]));
             if (in.f32) {
-                put<float>(blob, h.off_fk + 4 * f, (float)in.k[s]);
-                put<float>(blob, h.off_fl + 4 * f, (float)in.l0[s]);
+                put<float>(blob, h.off_fkl + 8 * f, (float)in.k[s]);
+                put<float>(blob, h.off_fkl + 8 * f + 4, (float)in.l0[s]);
             } else {
-                put<double>(blob, h.off_fk + 8 * f, in.k[s]);
-                put<double>(blob, h.off_fl + 8 * f, in.l0[s]);
+                put<double>(blob, h.off_fkl + 16 * f, in.k[s]);
+                put<double>(blob, h.off_fkl + 16 * f + 8, in.l0[s]);
             }
             if (has_g) put<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
         }
         std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
         tW[t] = W; tWr[t] = Wr; tH[t] = (uint32_t)halo.size(); tF[t] = nf; tRefs[t] = n_refs;
+        tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);   // n-1 in the top byte
+        tN[t] = n;
     }
     if (err == 1) return fail(SS_EINVAL, "tile exceeds layout limits (degree or halo too large)");
     if (err == 2) return fail(SS_EINVAL, "tile has too many foreign references");
@@ -275,6 +315,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             if (in.group[s] > 127) return fail(SS_EINVAL, "at most 128 actuation groups in the tiled layout");
     }
 
+    L.split = tSplit;
     L.off.assign(n_tiles + 1, 0);
     for (int64_t t = 0; t < n_tiles; ++t) L.off[t + 1] = L.off[t] + parts[t].size();
     L.blob.resize(L.off[n_tiles]);
@@ -287,7 +328,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
         L.max_halo = std::max(L.max_halo, tH[t]);
         L.max_W = std::max<int>(L.max_W, (int)tW[t]);
         L.max_Wr = std::max<int>(L.max_Wr, (int)tWr[t]);
-        const int n = (int)std::min<int64_t>(kTile, N - t * kTile);
+        const int n = (int)tN[t];
         hsum += (double)(n + tH[t]) / n;
         fsum += tF[t];
         rsum += (double)tRefs[t];

@@ -9,12 +9,17 @@ namespace ss {
 constexpr int kTile = 256;            // masses per tile == threads per CTA
 
 // Per-tile blob header (all offsets in bytes from the tile start, 16-B aligned).
+// Section order: header | halo ids | counts | own other | own (k,l0) | own grp |
+// refs | foreign owner | foreign (k,l0) | foreign grp.  [0, off_cnt) is copied
+// first so the halo gather overlaps the record stream.
+//   ref value: bit 15 set  -> foreign record index (bits 0-14)
+//              bit 15 clear-> in-tile record: owner local id (bits 0-7), slot q (bits 8-14)
 struct TileHdr {
     uint32_t n, W, Wr, n_halo;
     uint32_t n_foreign, bytes, off_cnt, off_oo;
-    uint32_t off_ok, off_ol, off_og, off_ref;
-    uint32_t off_fo, off_fk, off_fl, off_fg;
-    uint32_t off_halo, pad0, pad1, pad2;
+    uint32_t off_okl, off_og, off_ref, off_fo;
+    uint32_t off_fkl, off_fg, off_halo, canonical;
+    uint32_t pad0, pad1, pad2, pad3;
 };
 static_assert(sizeof(TileHdr) == 80, "TileHdr must stay 80 bytes");
 
@@ -33,6 +38,7 @@ struct TileLayout {
     std::vector<int32_t> new_of;    // original id -> new id
     std::vector<uint8_t> blob;      // concatenated tiles
     std::vector<uint64_t> off;      // n_tiles + 1 byte offsets into blob
+    std::vector<uint32_t> split;    // per tile: bytes of the first copy (header + halo ids)
     int64_t n_tiles = 0;
     uint32_t max_tile_bytes = 0;
     uint32_t max_halo = 0;

@@ -599,6 +599,35 @@ class Engine:
             raise ValueError(f"unknown command op {op!r}")
 
 
+def plan(scene, precision: str = "f32") -> dict:
+    """Host-only statistics of the tiled device layout of ``scene`` (no GPU needed):
+    tile count, halo ratio, foreign-reference fraction, streamed record bytes,
+    shared memory per CTA, algorithmic bytes per step."""
+    arr = scene_arrays(scene)
+    keep = {
+        "x": np.ascontiguousarray(arr.x, dtype=np.float64),
+        "si": np.ascontiguousarray(arr.si, dtype=np.int64),
+        "sj": np.ascontiguousarray(arr.sj, dtype=np.int64),
+        "k": np.ascontiguousarray(arr.k, dtype=np.float64),
+        "l0": np.ascontiguousarray(arr.l0, dtype=np.float64),
+        "group": np.ascontiguousarray(arr.group, dtype=np.int32),
+    }
+    d = _lib.SceneDesc()
+    d.n_masses = keep["x"].shape[0]
+    d.n_springs = keep["si"].shape[0]
+    d.x = _lib.dptr(keep["x"])
+    d.si = _lib.i64ptr(keep["si"])
+    d.sj = _lib.i64ptr(keep["sj"])
+    d.k = _lib.dptr(keep["k"])
+    d.l0 = _lib.dptr(keep["l0"])
+    d.group = _lib.i32ptr(keep["group"])
+    d.n_groups = len(arr.group_params)
+    d.precision = _lib.SS_F32 if precision == "f32" else _lib.SS_F64
+    inf = _lib.Info()
+    _lib.check(_lib.lib().ss_plan(C.byref(d), C.byref(inf)), "ss_plan")
+    return {f: getattr(inf, f) for f, _ in _lib.Info._fields_}
+
+
 def total_force(scene, mass_id: int, t: float = 0.0, **engine_kwargs) -> np.ndarray:
     """Total force on one mass at rest state (engine.py:469-473)."""
     engine = Engine(scene, integrator=EULER, mode=SERIAL, **engine_kwargs)

@@ -130,6 +130,22 @@ def test_library_exports_every_declared_symbol():
     assert lib.ss_abi_version() == 1
 
 
+def test_tile_plan_statistics_on_host():
+    """The tiled layout of a brick-aligned cube: tiles follow 4x8x8 bricks,
+    so the halo ratio and the foreign-reference fraction stay near the
+    brick's geometric values (6*10*10/256 = 2.34; 4.05 of 13 references = 31%)."""
+    from paper_2207_09334_b200.engine import plan
+    info = plan(L.block_scene(31))          # 32^3 masses: exact bricks
+    assert info["tile_count"] == 32 ** 3 // 256
+    assert info["canonical_order"] == 1
+    assert info["tile_halo_ratio"] <= 2.4
+    assert info["tile_foreign_frac"] <= 0.32
+    ragged = plan(L.block_scene(29))        # 30^3 masses: partial bricks
+    assert ragged["tile_halo_ratio"] <= 2.6
+    assert ragged["tile_foreign_frac"] <= 0.32
+    assert ragged["smem_per_block"] <= 76 * 1024
+
+
 def test_engine_without_gpu_fails_loudly():
     """No CPU fallback: on a host without a device, construction raises."""
     if _lib.device_count() > 0:

@@ -21,6 +21,6 @@ for prec in os.environ.get("PRECS", "f32,f64").split(","):
             gbs = info["algorithmic_bytes_per_step"] / (us * 1e-6) / 1e9
             r = dict(prec=prec, layout=layout, integ=integ, us_per_substep=round(us, 2),
                      springs_per_s=scene.spring_count / (us * 1e-6), algo_GBs=round(gbs, 1),
-                     W=info["ell_width_own"], Wr=info["ell_width_ref"])
+                     W=info["ell_width_own"], Wr=info["ell_width_ref"], smem=info["smem_per_block"], halo=round(info["tile_halo_ratio"],3), foreign=round(info["tile_foreign_frac"],3), blob_MB=round(info["tile_blob_bytes"]/1e6,1))
             print(json.dumps(r), flush=True)
             eng.close()
