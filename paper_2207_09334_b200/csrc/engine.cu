@@ -20,6 +20,7 @@
 
 #include "common.h"
 #include "kernels.cuh"
+#include "pipe_kernel.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
 #include "tiles.h"
@@ -98,6 +99,8 @@ struct ss_engine {
     unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
+    size_t pipe_smem = 0;          // persistent pipelined kernel (fp32 Euler/Verlet), 0 = off
+    int pipe_grid = 0;
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -300,6 +303,9 @@ Params<T> base_params(const ss_engine *h) {
     tp.tsplit = h->d_tsplit;
     tp.blob_smem = h->blob_smem;
     tp.max_halo = h->max_halo;
+    tp.n_tiles = (int)h->tl.n_tiles;
+    tp.head_smem = (h->tl.max_head_bytes + 127u) & ~127u;
+    tp.rest_smem = (h->tl.max_rest_bytes + 127u) & ~127u;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -364,8 +370,19 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.Vout = V;
             p.Xprev = Xo;
             p.bootstrap = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
+            if constexpr (F32 && LAYOUT >= 3) {
+                if (h->pipe_smem) {
+                    constexpr bool CANON = LAYOUT == 4, GROUPS = LAYOUT == 3;
+                    if (h->integrator == SS_EULER)
+                        tile_pipe_kernel<0, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
+                    else
+                        tile_pipe_kernel<1, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
+                    goto launched;
+                }
+            }
             if (h->integrator == SS_EULER) step_kernel<F32, 0, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
             else step_kernel<F32, 1, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+        launched:
             h->launches += 1;
             h->cur ^= 1;
             if (h->integrator == SS_VERLET) h->has_prev = true;
@@ -553,6 +570,26 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         if ((int64_t)h->smem_bytes > dev_max)
             return ss::fail(SS_EINVAL, "tile needs %zu B of shared memory (> %d)", h->smem_bytes, dev_max);
         if ((rc = set_tile_smem<F32>(h->smem_bytes))) return rc;
+        if constexpr (F32) {
+            // persistent pipelined kernel: 3 heads + 2 record buffers + 2 state
+            // stages + partial sums
+            const size_t slots = kTile + L.max_halo;
+            const size_t head = (L.max_head_bytes + 127u) & ~127u, rest = (L.max_rest_bytes + 127u) & ~127u;
+            const size_t pipe = 128 + 3 * head + 2 * rest + 2 * (2 * slots + 2 * kTile) * sizeof(float4) +
+                                kTile * sizeof(float4);
+            int sms = 0;
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+            const char *env = getenv("SS_PIPE");      // opt-in: see DESIGN.md §3.4
+            if ((int64_t)pipe <= dev_max && (env && env[0] == '1') && h->integrator != SS_RK4) {
+                h->pipe_smem = pipe;
+                h->pipe_grid = (int)std::min<int64_t>(L.n_tiles, sms);
+                const int b = (int)pipe;
+                CK(cudaFuncSetAttribute(tile_pipe_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_pipe_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_pipe_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_pipe_kernel<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+        }
         h->lay.canonical = L.canonical;
         return SS_OK;
     }

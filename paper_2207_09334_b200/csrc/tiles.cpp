@@ -325,6 +325,9 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     double hsum = 0, fsum = 0, rsum = 0;
     for (int64_t t = 0; t < n_tiles; ++t) {
         L.max_tile_bytes = std::max<uint32_t>(L.max_tile_bytes, (uint32_t)parts[t].size());
+        const uint32_t head = tSplit[t] & 0xffffffu;
+        L.max_head_bytes = std::max<uint32_t>(L.max_head_bytes, head);
+        L.max_rest_bytes = std::max<uint32_t>(L.max_rest_bytes, (uint32_t)parts[t].size() - head);
         L.max_halo = std::max(L.max_halo, tH[t]);
         L.max_W = std::max<int>(L.max_W, (int)tW[t]);
         L.max_Wr = std::max<int>(L.max_Wr, (int)tWr[t]);

@@ -41,6 +41,8 @@ struct TileLayout {
     std::vector<uint32_t> split;    // per tile: bytes of the first copy (header + halo ids)
     int64_t n_tiles = 0;
     uint32_t max_tile_bytes = 0;
+    uint32_t max_head_bytes = 0;    // [0, split): header + halo ids
+    uint32_t max_rest_bytes = 0;    // [split, bytes): counts + records + refs
     uint32_t max_halo = 0;
     int max_W = 0, max_Wr = 0;
     bool canonical = true;
