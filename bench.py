@@ -100,6 +100,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic(workload: str, precision: str, layout: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json), or None if this config was not profiled."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    entry = json.load(open(p)).get(f"{workload}/{precision}/{layout}")
+    return None if entry is None else entry["bytes"]
+
+
 def cpu_sample(scene, target_s=12.0, max_steps=40, threads=None):
     """Time the oracle's restatement of the reference's parallel-det mode
     (Alg. 1 slot schedule, OpenMP) on the host: bounded sample of Verlet steps."""
@@ -223,22 +233,27 @@ def run_single(args):
                "sample": f"{csteps} Verlet steps ({cwall:.1f} s) of the same {S}-spring cube, "
                          f"reference parallel-det Alg.1 schedule restated in C/OpenMP"}
 
+    workload = f"cube_n{cells}_10M_springs_excited_verlet" if cells == 91 else f"cube_n{cells}_excited_verlet"
+    layout_name = {1: "csr", 2: "ell", 3: "tile"}[info["layout"]]
     line = {
         "metric": "spring updates/sec (springs x steps / s)", "value": value,
         "unit": "spring-updates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if args.precision == "f32" else "f64",
         "data": "synthetic",
-        "config": {"workload": f"cube_n{cells}_10M_springs_excited_verlet" if cells == 91
-                   else f"cube_n{cells}_excited_verlet",
+        "config": {"workload": workload,
                    "cells": cells, "springs": S, "masses": N, "substeps_per_step": sub,
                    "integrator": "verlet", "precision": args.precision,
-                   "layout": {1: "csr", 2: "ell"}[info["layout"]],
+                   "layout": layout_name,
+                   "tile_halo_ratio": round(info["tile_halo_ratio"], 3),
+                   "tile_foreign_frac": round(info["tile_foreign_frac"], 3),
+                   "records_bytes_per_step": info["tile_blob_bytes"],
                    "device_bytes": info["device_bytes"],
                    "l2": "inputs larger than L2 (working set %.0f MB > 126 MB)" % (info["device_bytes"] / 1e6),
                    "parallelism": "single-gpu"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak,
+                     "traffic": profiled_traffic(workload, args.precision, layout_name),
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo,
                      "avg_launch_us": per_launch_s * 1e6},
