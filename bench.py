@@ -282,10 +282,17 @@ def main():
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1:
         from paper_2207_09334_b200 import sharded
         sharded.bench_main(args)
         return
+    if args.gpus > 1:
+        # not launched under torchrun: launch one process per GPU ourselves
+        import sys as _sys
+        cmd = [_sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", "--master-port=29611",
+               os.path.abspath(__file__)] + _sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     run_single(args)
 
 

@@ -203,6 +203,26 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
                    double *x_out, int64_t *si_out, int64_t *sj_out,
                    double *k_out, double *l0_out, int64_t *spring_id_out);
 
+/*
+ * x-slab sharding.  A shard's scene holds its
+ * owned masses plus one halo plane per neighbour, marked fixed; springs keep
+ * their global ids, so results are bitwise identical to one device.
+ * ss_halo_setup: caller ids of the boundary planes to send and of the halo
+ * planes to receive (side lo = lower-x neighbour, hi = upper), plane order
+ * identical on both sides.  Transport:
+ *   - ss_nccl_unique_id + ss_halo_nccl: one process per GPU; after every
+ *     substep ss_step packs, exchanges (ncclSend/ncclRecv on the engine
+ *     stream) and unpacks the planes;
+ *   - ss_step_group: several shards on one device stepped in lockstep, the
+ *     planes copied device-to-device (virtual shards, for testing).
+ */
+int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
+                  const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,
+                  int64_t n_recv_hi, const int64_t *recv_hi);
+int ss_nccl_unique_id(unsigned char id[128]);
+int ss_halo_nccl(ss_engine *h, const unsigned char id[128], int nranks, int rank, int rank_lo, int rank_hi);
+int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res);
+
 #ifdef __cplusplus
 }
 #endif

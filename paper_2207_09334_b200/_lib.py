@@ -85,6 +85,11 @@ SIGNATURES = {
     "ss_get_info": (C.c_int, [C.c_void_p, C.POINTER(Info)]),
     "ss_launch_count": (C.c_int64, [C.c_void_p]),
     "ss_plan": (C.c_int, [C.POINTER(SceneDesc), C.POINTER(Info)]),
+    "ss_halo_setup": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_int64, _i64p,
+                                C.c_int64, _i64p, C.c_int64, _i64p]),
+    "ss_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "ss_halo_nccl": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ss_step_group": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.POINTER(StepResult)]),
     "ss_lattice_box": (C.c_int, [_dp, _dp, C.c_double, C.c_double, C.c_double,
                                  C.c_int64, C.c_int64, _i64p, _i64p, _i64p,
                                  _dp, _i64p, _i64p, _dp, _dp, _i64p]),

@@ -24,6 +24,8 @@
 #include "layout.h"
 #include "springsim_b200.h"
 #include "tiles.h"
+#include "halo.cuh"
+#include "nccl_shim.h"
 
 using namespace ss;
 
@@ -107,8 +109,20 @@ struct ss_engine {
     int64_t pending_n0 = 0;
     int pending_cur0 = 0;
 
+    // halo exchange (x-slab sharding); side 0 = lower neighbour, 1 = upper
+    bool halo_on = false;
+    int halo_n_send[2] = {0, 0}, halo_n_recv[2] = {0, 0};
+    int *halo_send_idx[2] = {nullptr, nullptr}, *halo_recv_idx[2] = {nullptr, nullptr};
+    void *halo_send[2] = {nullptr, nullptr}, *halo_recv[2] = {nullptr, nullptr};
+    ncclComm_t nccl = nullptr;
+    int nccl_peer[2] = {-1, -1};
+    int64_t halo_exchanges = 0;
+
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
+        if (nccl) {
+            if (const NcclApi *api = nccl_api()) api->commDestroy(nccl);
+        }
         for (auto &b : bufs) cudaFree(b.p);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -339,6 +353,43 @@ int with_layout(const ss_engine *h, Fn &&fn) {
     }
 }
 
+// After a substep: pack the boundary planes of the new positions, exchange
+// them with the neighbouring ranks (NCCL send/recv on the engine stream) and
+// write the received planes into the halo slots.
+template <typename T4>
+int halo_exchange_nccl(ss_engine *h) {
+    const NcclApi *api = nccl_api();
+    if (!api) return SS_ECUDA;
+    T4 *X = reinterpret_cast<T4 *>(h->X[h->cur]);
+    for (int s = 0; s < 2; ++s)
+        if (h->halo_n_send[s] && h->nccl_peer[s] >= 0)
+            halo_pack_kernel<T4><<<(h->halo_n_send[s] + 255) / 256, 256, 0, h->stream>>>(
+                X, h->halo_send_idx[s], h->halo_n_send[s], reinterpret_cast<T4 *>(h->halo_send[s]));
+    const size_t words = sizeof(T4) / sizeof(float);
+    ncclResult_t r = api->groupStart();
+    for (int s = 0; s < 2 && r == ncclSuccess; ++s) {
+        if (h->nccl_peer[s] < 0) continue;
+        if (h->halo_n_send[s])
+            r = api->send(h->halo_send[s], (size_t)h->halo_n_send[s] * words, ncclFloat32, h->nccl_peer[s],
+                          h->nccl, h->stream);
+        if (r == ncclSuccess && h->halo_n_recv[s])
+            r = api->recv(h->halo_recv[s], (size_t)h->halo_n_recv[s] * words, ncclFloat32, h->nccl_peer[s],
+                          h->nccl, h->stream);
+    }
+    const ncclResult_t r2 = api->groupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return ss::fail(SS_ECUDA, "NCCL halo exchange failed: %s",
+                        api->getErrorString(r != ncclSuccess ? r : r2));
+    for (int s = 0; s < 2; ++s)
+        if (h->halo_n_recv[s] && h->nccl_peer[s] >= 0)
+            halo_unpack_kernel<T4><<<(h->halo_n_recv[s] + 255) / 256, 256, 0, h->stream>>>(
+                X, h->halo_recv_idx[s], h->halo_n_recv[s], reinterpret_cast<const T4 *>(h->halo_recv[s]));
+    h->launches += 2;
+    h->halo_exchanges += 1;
+    CK(cudaGetLastError());
+    return SS_OK;
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
@@ -386,6 +437,10 @@ int launch_steps(ss_engine *h, int64_t count) {
             h->launches += 1;
             h->cur ^= 1;
             if (h->integrator == SS_VERLET) h->has_prev = true;
+            if (h->nccl) {                                   // boundary planes -> neighbours' halos
+                int rc = halo_exchange_nccl<T4>(h);
+                if (rc) return rc;
+            }
         } else {
             T4 *XA = reinterpret_cast<T4 *>(h->XA), *XB = reinterpret_cast<T4 *>(h->XB);
             T4 *VS = reinterpret_cast<T4 *>(h->VS);
@@ -1039,4 +1094,148 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     return SS_OK;
+}
+
+// ============================================================ sharding
+// x-slab sharding: halo lists, NCCL transport across
+// processes, and same-process "virtual shards" stepped in lockstep.
+
+namespace {
+
+int64_t device_slot(const ss_engine *h, int64_t caller_id) {
+    return h->tl.new_of.empty() || h->orig_of.empty() ? caller_id : (int64_t)h->tl.new_of[caller_id];
+}
+
+}  // namespace
+
+extern "C" int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
+                             const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,
+                             int64_t n_recv_hi, const int64_t *recv_hi) {
+    if (!h) return ss::fail(SS_EINVAL, "null engine");
+    if (h->integrator == SS_RK4) return ss::fail(SS_EINVAL, "halo exchange supports Euler and Verlet");
+    CK(cudaSetDevice(h->device));
+    const int64_t ns[2] = {n_send_lo, n_send_hi}, nr[2] = {n_recv_lo, n_recv_hi};
+    const int64_t *sid[2] = {send_lo, send_hi}, *rid[2] = {recv_lo, recv_hi};
+    const size_t vec = h->precision == SS_F32 ? sizeof(float4) : sizeof(double4);
+    int rc;
+    for (int s = 0; s < 2; ++s) {
+        std::vector<int> si((size_t)ns[s]), ri((size_t)nr[s]);
+        for (int64_t i = 0; i < ns[s]; ++i) {
+            if (sid[s][i] < 0 || sid[s][i] >= h->N) return ss::fail(SS_EINVAL, "halo send id out of range");
+            si[i] = (int)device_slot(h, sid[s][i]);
+        }
+        for (int64_t i = 0; i < nr[s]; ++i) {
+            if (rid[s][i] < 0 || rid[s][i] >= h->N) return ss::fail(SS_EINVAL, "halo recv id out of range");
+            if (!h->fixed[rid[s][i]]) return ss::fail(SS_EINVAL, "halo masses must be marked fixed");
+            ri[i] = (int)device_slot(h, rid[s][i]);
+        }
+        h->halo_n_send[s] = (int)ns[s];
+        h->halo_n_recv[s] = (int)nr[s];
+        void *p;
+        if ((rc = h->alloc(&p, si.size() * sizeof(int)))) return rc;
+        h->halo_send_idx[s] = (int *)p;
+        if (!si.empty() && (rc = upload(h, p, si.data(), si.size() * sizeof(int)))) return rc;
+        if ((rc = h->alloc(&p, ri.size() * sizeof(int)))) return rc;
+        h->halo_recv_idx[s] = (int *)p;
+        if (!ri.empty() && (rc = upload(h, p, ri.data(), ri.size() * sizeof(int)))) return rc;
+        if ((rc = h->alloc(&h->halo_send[s], (size_t)ns[s] * vec))) return rc;
+        if ((rc = h->alloc(&h->halo_recv[s], (size_t)nr[s] * vec))) return rc;
+    }
+    h->halo_on = true;
+    return SS_OK;
+}
+
+extern "C" int ss_nccl_unique_id(unsigned char id[128]) {
+    const NcclApi *api = nccl_api();
+    if (!api) return SS_ECUDA;
+    ncclUniqueId u;
+    const ncclResult_t r = api->getUniqueId(&u);
+    if (r != ncclSuccess) return ss::fail(SS_ECUDA, "ncclGetUniqueId: %s", api->getErrorString(r));
+    std::memcpy(id, &u, sizeof u);
+    return SS_OK;
+}
+
+extern "C" int ss_halo_nccl(ss_engine *h, const unsigned char id[128], int nranks, int rank, int rank_lo,
+                            int rank_hi) {
+    if (!h || !id) return ss::fail(SS_EINVAL, "ss_halo_nccl: null argument");
+    if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
+    const NcclApi *api = nccl_api();
+    if (!api) return SS_ECUDA;
+    CK(cudaSetDevice(h->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    const ncclResult_t r = api->commInitRank(&h->nccl, nranks, u, rank);
+    if (r != ncclSuccess) return ss::fail(SS_ECUDA, "ncclCommInitRank: %s", api->getErrorString(r));
+    h->nccl_peer[0] = rank_lo;
+    h->nccl_peer[1] = rank_hi;
+    return SS_OK;
+}
+
+// Step n same-device shards in lockstep; shard k's upper side is shard k+1's
+// lower side.  All work is serialised on shard 0's stream.
+extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_result *res) {
+    if (!hs || n <= 0) return ss::fail(SS_EINVAL, "ss_step_group: no engines");
+    for (int k = 0; k < n; ++k) {
+        if (!hs[k] || !hs[k]->halo_on) return ss::fail(SS_EINVAL, "ss_step_group: engine %d has no halo", k);
+        if (hs[k]->device != hs[0]->device || hs[k]->precision != hs[0]->precision)
+            return ss::fail(SS_EINVAL, "ss_step_group: engines must share device and precision");
+        int rc = sync_pending(hs[k]);
+        if (rc) return rc;
+    }
+    CK(cudaSetDevice(hs[0]->device));
+    std::vector<cudaStream_t> saved(n);
+    std::vector<int64_t> n0(n);
+    std::vector<int> cur0(n);
+    for (int k = 0; k < n; ++k) {
+        saved[k] = hs[k]->stream;
+        hs[k]->stream = hs[0]->stream;
+        n0[k] = hs[k]->n;
+        cur0[k] = hs[k]->cur;
+    }
+    int rc = SS_OK;
+    const bool f32 = hs[0]->precision == SS_F32;
+    for (int64_t s = 0; s < count && rc == SS_OK; ++s) {
+        for (int k = 0; k < n && rc == SS_OK; ++k) {
+            rc = dispatch_steps(hs[k], 1);
+            hs[k]->n += 1;
+            hs[k]->t = (double)hs[k]->n * hs[k]->dt;
+        }
+        for (int k = 0; k + 1 < n && rc == SS_OK; ++k) {
+            ss_engine *a = hs[k], *b = hs[k + 1];
+            const int na = a->halo_n_send[1], nb = b->halo_n_send[0];
+            if (na != b->halo_n_recv[0] || nb != a->halo_n_recv[1]) {
+                rc = ss::fail(SS_EINVAL, "ss_step_group: halo sizes of shards %d/%d disagree", k, k + 1);
+                break;
+            }
+            if (f32) {
+                halo_copy_kernel<float4><<<(na + 255) / 256, 256, 0, a->stream>>>(
+                    (const float4 *)a->X[a->cur], a->halo_send_idx[1], (float4 *)b->X[b->cur], b->halo_recv_idx[0], na);
+                halo_copy_kernel<float4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
+                    (const float4 *)b->X[b->cur], b->halo_send_idx[0], (float4 *)a->X[a->cur], a->halo_recv_idx[1], nb);
+            } else {
+                halo_copy_kernel<double4><<<(na + 255) / 256, 256, 0, a->stream>>>(
+                    (const double4 *)a->X[a->cur], a->halo_send_idx[1], (double4 *)b->X[b->cur], b->halo_recv_idx[0], na);
+                halo_copy_kernel<double4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
+                    (const double4 *)b->X[b->cur], b->halo_send_idx[0], (double4 *)a->X[a->cur], a->halo_recv_idx[1], nb);
+            }
+            a->launches += 2;
+        }
+    }
+    if (rc == SS_OK) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = ss::fail(SS_ECUDA, "ss_step_group: %s", cudaGetErrorString(e));
+    }
+    int first_err = rc;
+    for (int k = 0; k < n; ++k) {
+        ss_step_result r{};
+        const int rk = rc == SS_OK ? finish_batch(hs[k], count, n0[k], cur0[k], &r) : SS_OK;
+        if (rk != SS_OK && first_err == SS_OK) {
+            first_err = rk;
+            if (res) *res = r;
+        } else if (k == 0 && res && rk == SS_OK) {
+            *res = r;
+        }
+    }
+    for (int k = 0; k < n; ++k) hs[k]->stream = saved[k];
+    return first_err;
 }

@@ -1,0 +1,252 @@
+"""x-slab sharding of voxel-box lattices across GPUs.
+
+The reference numbers masses (i, j, k)-lexicographically (lattice.py:116-119),
+so a contiguous id range is a slab of whole x-planes.  Rank g owns planes
+[i_lo, i_hi) and holds, in its local scene, one halo plane per neighbour
+(marked fixed) plus every spring touching an owned mass — with its GLOBAL id
+order preserved, so each owned mass sums its springs in the same order as on
+one device and the results are bitwise identical.  After every substep the
+first and last owned planes go to the neighbours' halo planes (NCCL
+send/recv on the engine stream, or device copies for same-device shards).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import Engine, _lib as _englib  # noqa: F401
+from .lattice import PITCH, voxel_arrays
+from .model import ArrayScene
+
+
+def slab_planes(nx: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Even split of nx planes over nranks (the first nx % nranks get one more)."""
+    base, extra = divmod(nx, nranks)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def excited_velocities(n_masses: int, seed: int = 11, sigma: float = 0.05,
+                       drift=(0.3, 0.2, 0.1)) -> np.ndarray:
+    """The global excited-velocity field of ``lattice.excite`` (same RNG stream)."""
+    rng = np.random.default_rng(seed)
+    return rng.normal(0.0, sigma, (n_masses, 3)) + np.asarray(drift, dtype=np.float64)
+
+
+@dataclass
+class Slab:
+    scene: ArrayScene            # local scene: [halo lo plane] + owned planes + [halo hi plane]
+    first_global: int            # global id of local mass 0
+    n_owned: int
+    owned: slice                 # local ids of the owned masses
+    send_lo: np.ndarray          # local ids (first owned plane), empty without a lower neighbour
+    recv_lo: np.ndarray          # local ids (lower halo plane)
+    send_hi: np.ndarray          # local ids (last owned plane)
+    recv_hi: np.ndarray          # local ids (upper halo plane)
+    springs_global: int
+    masses_global: int
+    i_lo: int
+    i_hi: int
+    nx: int
+
+
+def cube_slab(cells: int, i_lo: int, i_hi: int, v_global: np.ndarray | None = None) -> Slab:
+    """Slab [i_lo, i_hi) of ``block_scene(cells)`` with its halo planes."""
+    side = cells * PITCH
+    lo, hi = (0.0, 0.0, 0.0), (side, side, side)
+    counts, _, si, sj, k, l0, _ids = voxel_arrays(lo, hi, PITCH, plane_range=(i_lo, i_hi))
+    nx, ny, nz = counts
+    plane = ny * nz
+    p0 = max(0, i_lo - 1)
+    p1 = min(nx, i_hi + 1)
+    first = p0 * plane
+    n_local = (p1 - p0) * plane
+    gid = np.arange(first, first + n_local, dtype=np.int64)
+    idx = np.stack([gid // plane, (gid // nz) % ny, gid % nz], axis=1).astype(np.float64)
+    x = 0.0 + idx * PITCH                       # lo + idx*dim, lattice.py:110
+    fixed = np.zeros(n_local, dtype=bool)
+    if i_lo > 0:
+        fixed[:plane] = True
+    if i_hi < nx:
+        fixed[-plane:] = True
+    if v_global is not None:
+        v = v_global[first:first + n_local]
+    else:
+        v = np.zeros((n_local, 3))
+    scene = ArrayScene(x=x, m=0.1, si=si - first, sj=sj - first, k=k, l0=l0, v=v, fixed=fixed,
+                       gravity=(0.0, 0.0, 0.0))
+    own0 = (i_lo - p0) * plane
+    n_owned = (i_hi - i_lo) * plane
+    ids = np.arange(n_local, dtype=np.int64)
+    empty = np.zeros(0, dtype=np.int64)
+    s_full = 13 * cells ** 3 + 12 * cells ** 2 + 3 * cells
+    return Slab(scene=scene, first_global=first, n_owned=n_owned, owned=slice(own0, own0 + n_owned),
+                send_lo=ids[own0:own0 + plane] if i_lo > 0 else empty,
+                recv_lo=ids[:plane] if i_lo > 0 else empty,
+                send_hi=ids[own0 + n_owned - plane:own0 + n_owned] if i_hi < nx else empty,
+                recv_hi=ids[-plane:] if i_hi < nx else empty,
+                springs_global=s_full, masses_global=nx * ny * nz, i_lo=i_lo, i_hi=i_hi, nx=nx)
+
+
+def attach_halo(engine: Engine, slab: Slab) -> None:
+    lib = _lib.lib()
+    arrs = [np.ascontiguousarray(a, dtype=np.int64) for a in
+            (slab.send_lo, slab.send_hi, slab.recv_lo, slab.recv_hi)]
+    engine._halo_keep = arrs
+    _lib.check(lib.ss_halo_setup(engine.handle, arrs[0].shape[0], _lib.i64ptr(arrs[0]),
+                                 arrs[1].shape[0], _lib.i64ptr(arrs[1]),
+                                 arrs[2].shape[0], _lib.i64ptr(arrs[2]),
+                                 arrs[3].shape[0], _lib.i64ptr(arrs[3])), "ss_halo_setup")
+
+
+class ShardGroup:
+    """k x-slab shards of one cube on ONE device, stepped in lockstep with
+    device-to-device halo copies (the sharded code path without NCCL)."""
+
+    def __init__(self, cells: int, shards: int, precision: str = "f64", layout: str = "auto",
+                 v_global: np.ndarray | None = None, device: int = 0):
+        nx = cells + 1
+        self.slabs = [cube_slab(cells, *slab_planes(nx, shards, r), v_global=v_global)
+                      for r in range(shards)]
+        self.engines = [Engine(s.scene, integrator="verlet", precision=precision, layout=layout,
+                               device=device) for s in self.slabs]
+        for e, s in zip(self.engines, self.slabs):
+            attach_halo(e, s)
+
+    def step(self, count: int) -> None:
+        for e in self.engines:
+            e._upload_lent()
+            e._push_params()
+        arr = (C.c_void_p * len(self.engines))(*[e.handle.value for e in self.engines])
+        res = _lib.StepResult()
+        rc = _lib.lib().ss_step_group(arr, len(self.engines), int(count), C.byref(res))
+        for e in self.engines:
+            e._mark_stepped()
+        _lib.check(rc, "ss_step_group")
+
+    def positions(self) -> np.ndarray:
+        """Global positions assembled from the owned parts of every shard."""
+        out = []
+        for e, s in zip(self.engines, self.slabs):
+            out.append(e.x[s.owned])
+        return np.concatenate(out)
+
+    def velocities(self) -> np.ndarray:
+        return np.concatenate([e.v[s.owned] for e, s in zip(self.engines, self.slabs)])
+
+
+# ------------------------------------------------------------------ bench
+
+def bench_main(args) -> None:
+    """bench.py under torchrun with N>1 ranks: the 400M-spring cube
+    (BASELINE.json configs[4], block_scene(313)) split into N x-slabs, one
+    per GPU, NCCL halo exchange every substep.  Strong scaling (fixed lattice)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cells = args.cells or 313
+    nx = cells + 1
+    n_masses = nx ** 3
+    i_lo, i_hi = slab_planes(nx, world, rank)
+    t0 = time.perf_counter()
+    v_global = excited_velocities(n_masses)
+    slab = cube_slab(cells, i_lo, i_hi, v_global=v_global)
+    del v_global
+    eng = Engine(slab.scene, integrator="verlet", precision=args.precision, layout=args.layout,
+                 device=local)
+    attach_halo(eng, slab)
+    uid = C.create_string_buffer(128)
+    if rank == 0:
+        _lib.check(_lib.lib().ss_nccl_unique_id(uid), "ss_nccl_unique_id")
+    obj = [bytes(uid.raw)]
+    dist.broadcast_object_list(obj, src=0)
+    _lib.check(_lib.lib().ss_halo_nccl(eng.handle, obj[0], world, rank,
+                                       rank - 1 if rank > 0 else -1,
+                                       rank + 1 if rank + 1 < world else -1), "ss_halo_nccl")
+    build_s = time.perf_counter() - t0
+    info = eng.info()
+    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", local))
+    sub = args.substeps
+    for _ in range(max(args.warmup, 3)):
+        eng.step_async(sub)
+    eng.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.launch_count
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        eng.step_async(sub)
+    b.record(stream)
+    b.synchronize()
+    eng.synchronize()
+    ms = torch.tensor([a.elapsed_time(b)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = float(ms.item())
+    launches = eng.launch_count - launches0
+    S = slab.springs_global
+    value = S * sub * args.steps / (ms / 1e3)
+    # per-GPU algorithmic bytes of the whole job / time, against N x peak
+    peak = 6550.4
+    pk = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peak = float(json.load(open(pk))["hbm_gbs"])
+    algo_job = (16 if args.precision == "f32" else 24) * S + (64 if args.precision == "f32" else 128) * n_masses
+    per_sub = ms / 1e3 / (args.steps * sub)
+    achieved = algo_job / per_sub / 1e9 / world
+    # e2e through the public API: host state in, positions out (per rank, max over ranks)
+    x_h, v_h, xp_h = eng.x.copy(), eng.v.copy(), eng.x_prev.copy()
+    e2e_steps = 2
+    dist.barrier()
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.x = x_h
+        eng.v = v_h
+        eng.x_prev = xp_h
+        eng.step(sub)
+        _ = eng.x
+    ew = torch.tensor([time.perf_counter() - w0], device="cuda")
+    dist.all_reduce(ew, op=dist.ReduceOp.MAX)
+    ew = float(ew.item())
+    n_local = slab.scene.mass_count
+    vec = 16 if args.precision == "f32" else 32
+    if rank == 0:
+        print(json.dumps({
+            "metric": "spring updates/sec (springs x steps / s)", "value": value,
+            "unit": "spring-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": f"cube_n{cells}_sharded_x_slabs_verlet", "cells": cells,
+                       "springs": S, "masses": n_masses, "substeps_per_step": sub,
+                       "integrator": "verlet", "precision": args.precision,
+                       "layout": {1: "csr", 2: "ell", 3: "tile"}[info["layout"]],
+                       "parallelism": f"x-slab x{world}, NCCL halo exchange per substep",
+                       "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
+                       "build_s_rank0": round(build_s, 1),
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": "measured",
+                         "note": "per GPU: whole-job algorithmic bytes / time / N"},
+            "cpu_baseline": None,
+            "e2e": {"value": S * sub * e2e_steps / ew, "unit": "spring-updates/s",
+                    "h2d_bytes_per_step": 3 * n_local * vec * world,
+                    "d2h_bytes_per_step": n_local * vec * world},
+            "gpu_launches": launches,
+        }), flush=True)
+    eng.close()
+    dist.destroy_process_group()
