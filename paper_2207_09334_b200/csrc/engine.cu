@@ -624,7 +624,9 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
         if ((int64_t)h->smem_bytes > dev_max)
             return ss::fail(SS_EINVAL, "tile needs %zu B of shared memory (> %d)", h->smem_bytes, dev_max);
-        if ((rc = set_tile_smem<F32>(h->smem_bytes))) return rc;
+        // the attribute is a per-function permission shared by every engine in
+        // the process: grant the device maximum, never a per-engine size
+        if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
         if constexpr (F32) {
             // persistent pipelined kernel: 3 heads + 2 record buffers + 2 state
             // stages + partial sums
@@ -638,7 +640,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if ((int64_t)pipe <= dev_max && (env && env[0] == '1') && h->integrator != SS_RK4) {
                 h->pipe_smem = pipe;
                 h->pipe_grid = (int)std::min<int64_t>(L.n_tiles, sms);
-                const int b = (int)pipe;
+                const int b = dev_max;
                 CK(cudaFuncSetAttribute(tile_pipe_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 CK(cudaFuncSetAttribute(tile_pipe_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 CK(cudaFuncSetAttribute(tile_pipe_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));

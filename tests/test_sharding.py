@@ -119,7 +119,9 @@ def test_nccl_transport_self_loop():
     cells = 5
     nx = cells + 1
     s = cube_slab(cells, 1, nx - 1, v_global=excited_velocities(nx ** 3))
-    eng = Engine(s.scene, precision="f32")
+    # fp64: absolute positions travel (in fp32 only the displacement r does,
+    # which is consistent only between the two copies of the SAME mass)
+    eng = Engine(s.scene, precision="f64")
     attach_halo(eng, s)
     uid = C.create_string_buffer(128)
     _lib.check(_lib.lib().ss_nccl_unique_id(uid))
