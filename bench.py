@@ -46,7 +46,8 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons, 100 ms samples time-stamped on
+    arrival; ``summary()`` keeps the samples inside the marked timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -55,7 +56,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -71,7 +73,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def start(self):
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
+        time.sleep(0.25)                 # let the sample covering the end arrive
 
     def __exit__(self, *exc):
         if self.proc:
@@ -84,7 +93,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo = (self.t0 or 0.0) - 0.05
+        hi = (self.t1 or time.time()) + 0.15
+        for ts, ln in self.lines:
+            if not lo <= ts <= hi:
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -97,7 +110,8 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round((self.t1 or 0) - (self.t0 or 0), 3)}
 
 
 def profiled_traffic(workload: str, precision: str, layout: str):
@@ -193,11 +207,14 @@ def run_single(args):
     end = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
+        time.sleep(0.3)                  # sampler up before the timed region
+        clk.start()
         start.record(stream)
         for _ in range(args.steps):
             eng.step_async(sub)
         end.record(stream)
         end.synchronize()
+        clk.stop()
     eng.synchronize()
     ms = start.elapsed_time(end)
     launches = eng.launch_count - launches0
@@ -269,7 +286,7 @@ def run_single(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cells", type=int, default=0)
@@ -277,12 +294,18 @@ def main():
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--layout", default="auto", choices=["auto", "csr", "ell"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the x-slab sharded path even on one rank (400M cube by default)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or args.sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29612")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         from paper_2207_09334_b200 import sharded
         sharded.bench_main(args)
         return

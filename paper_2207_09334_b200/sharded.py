@@ -160,12 +160,17 @@ def bench_main(args) -> None:
     nx = cells + 1
     n_masses = nx ** 3
     i_lo, i_hi = slab_planes(nx, world, rank)
+    import sys
     t0 = time.perf_counter()
     v_global = excited_velocities(n_masses)
     slab = cube_slab(cells, i_lo, i_hi, v_global=v_global)
     del v_global
+    t1 = time.perf_counter()
     eng = Engine(slab.scene, integrator="verlet", precision=args.precision, layout=args.layout,
                  device=local)
+    print(f"[rank {rank}] planes [{i_lo},{i_hi}) {slab.scene.spring_count} springs: "
+          f"slab build {t1 - t0:.1f} s, engine {time.perf_counter() - t1:.1f} s", file=sys.stderr,
+          flush=True)
     attach_halo(eng, slab)
     uid = C.create_string_buffer(128)
     if rank == 0:
