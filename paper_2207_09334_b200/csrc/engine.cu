@@ -16,6 +16,7 @@
 #include <memory>
 #include <type_traits>
 #include <utility>
+#include <string>
 #include <vector>
 
 #include "common.h"
@@ -102,6 +103,7 @@ struct ss_engine {
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     size_t pipe_smem = 0;          // persistent pipelined kernel (fp32 Euler/Verlet), 0 = off
+    size_t step2_smem = 0;         // 512-thread tile kernel (fp32 Euler/Verlet), 0 = off
     int pipe_grid = 0;
     int64_t device_bytes = 0;
     int64_t launches = 0;
@@ -338,6 +340,7 @@ Params<T> base_params(const ss_engine *h) {
     p.degenerate = h->d_degenerate;
     p.div_step = h->d_div_step;
     p.div_mass = h->d_div_mass;
+    if (const char *dbg = getenv("SS_DEBUG")) p.debug = atoi(dbg);   // timing experiments only
     return p;
 }
 
@@ -428,6 +431,14 @@ int launch_steps(ss_engine *h, int64_t count) {
                         tile_pipe_kernel<0, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
                     else
                         tile_pipe_kernel<1, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
+                    goto launched;
+                }
+                if (h->step2_smem) {
+                    constexpr bool CANON = LAYOUT == 4, GROUPS = LAYOUT == 3;
+                    if (h->integrator == SS_EULER)
+                        tile_step2_kernel<0, CANON, GROUPS><<<grid, kPipeThreads, h->step2_smem, h->stream>>>(p);
+                    else
+                        tile_step2_kernel<1, CANON, GROUPS><<<grid, kPipeThreads, h->step2_smem, h->stream>>>(p);
                     goto launched;
                 }
             }
@@ -574,11 +585,17 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     }
     // ---- fp32 base positions (device order)
     if (F32) {
+        // P = X0 snapped to a power-of-two grid q with |P| <= 2^22 q: every
+        // difference P_o - P_m (and P - tile anchor) is exact in fp32, and
+        // r = x - P keeps the residual plus the motion.
+        double amax = 1.0;
+        for (int64_t i = 0; i < 3 * N; ++i) amax = std::max(amax, std::fabs(d->x[i]));
+        const double q = std::ldexp(1.0, (int)std::ceil(std::log2(amax)) - 22);
         h->base.assign((size_t)ND * 4, 0.f);
         for (int64_t i = 0; i < ND; ++i) {
             const int64_t s = h->src_of(i);
             if (s < 0) continue;
-            for (int c = 0; c < 3; ++c) h->base[4 * i + c] = (float)d->x[3 * s + c];
+            for (int c = 0; c < 3; ++c) h->base[4 * i + c] = (float)(std::nearbyint(d->x[3 * s + c] / q) * q);
         }
         if ((rc = h->alloc(&h->P, (size_t)ND * sizeof(T4)))) return rc;
         if ((rc = upload(h, h->P, h->base.data(), (size_t)ND * sizeof(T4)))) return rc;
@@ -619,7 +636,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         h->d_tsplit = reinterpret_cast<unsigned int *>(p);
         h->blob_smem = (L.max_tile_bytes + 127u) & ~127u;
         h->max_halo = L.max_halo;
-        h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4) * (F32 ? 2 : 1);
+        h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4);   // one staged vector per mass
         int dev_max = 0;
         CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
         if ((int64_t)h->smem_bytes > dev_max)
@@ -636,8 +653,20 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                 kTile * sizeof(float4);
             int sms = 0;
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-            const char *env = getenv("SS_PIPE");      // opt-in: see DESIGN.md §3.4
-            if ((int64_t)pipe <= dev_max && (env && env[0] == '1') && h->integrator != SS_RK4) {
+            // kernel choice for fp32 Euler/Verlet on tiles:
+            // SS_KERNEL=step2 (default, 512 threads/tile), step1 (256), pipe (persistent)
+            const char *kenv = getenv("SS_KERNEL");
+            const std::string kname = kenv ? kenv : "step2";
+            if (kname == "step2" && h->integrator != SS_RK4 &&
+                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
+                h->step2_smem = h->smem_bytes + kTile * sizeof(float4);
+                const int b = dev_max;
+                CK(cudaFuncSetAttribute(tile_step2_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_step2_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_step2_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_step2_kernel<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+            if ((int64_t)pipe <= dev_max && kname == "pipe" && h->integrator != SS_RK4) {
                 h->pipe_smem = pipe;
                 h->pipe_grid = (int)std::min<int64_t>(L.n_tiles, sms);
                 const int b = dev_max;
@@ -1092,7 +1121,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     info->tile_foreign_frac = tl.foreign_frac;
     const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
     info->smem_per_block =
-        (int32_t)(128 + ((tl.max_tile_bytes + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec * (f32 ? 2 : 1));
+        (int32_t)(128 + ((tl.max_tile_bytes + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec);
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     return SS_OK;

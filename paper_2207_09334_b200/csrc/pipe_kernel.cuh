@@ -1,19 +1,18 @@
-// Persistent, software-pipelined tile kernel (fp32 production mode, Euler /
-// Verlet).  DESIGN.md §3.4.
+// 512-thread tile kernels (fp32 production mode, Euler / Verlet).  DESIGN.md §3.4.
 //
-// One 512-thread CTA per SM walks its tiles t = blockIdx.x + i*gridDim.x.
-// Each tile blob is fetched by the TMA engine in two pieces: the small head
-// (header + halo id list, triple-buffered, issued two tiles ahead) and the
-// records (double-buffered, issued one tile ahead).  While tile i is being
-// computed, tile i+1's records stream in and cp.async gathers tile i+1's own
-// and halo states (its head landed an iteration earlier), so DRAM streaming,
-// L2 gathers and arithmetic overlap instead of alternating.
+// Two threads per tile mass: threads 0..255 sum the references of mass
+// l = tid, threads 256..511 the own records of mass l = tid-256 (whole warps
+// per role, no divergence).  The two partial sums are combined in a fixed
+// order (refs + own), so results are deterministic and identical across
+// launch shapes and shardings.  Per-incidence arithmetic is
+// spring_term<true>; the integrator epilogue is step_kernel's.
 //
-// Threads 0..255 sum the references of mass l = tid, threads 256..511 the own
-// records of mass l = tid-256 (whole warps per role, no divergence); the two
-// partial sums are combined in a fixed order (refs + own): deterministic.
-// Per-incidence arithmetic is spring_term<true>; the integrator epilogue uses
-// the same expressions as step_kernel.
+//  tile_step2_kernel : one tile per CTA (like step_kernel<.., TILE>), 16
+//                      warps per CTA -> twice the resident warps per SM.
+//  tile_pipe_kernel  : persistent, one CTA per SM; TMA heads triple-buffered,
+//                      TMA records and cp.async states double-buffered, so
+//                      tile i+1 streams in while tile i computes (opt-in:
+//                      SS_PIPE=1).
 #pragma once
 
 #include "kernels.cuh"
@@ -28,11 +27,235 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Shared-memory carve-up (all pointers derived arithmetically from the
-// extern __shared__ base, so the compiler keeps them in the shared window
-// and emits LDS/STS): [barriers | 3 heads | 2 record buffers | 2 x state | partials]
+// Partial spring sum of tile mass l for this thread's role (0 refs, 1 own).
+// `bl` is the blob base the section offsets are relative to.
+template <bool CANON, bool GROUPS>
+__device__ __forceinline__ V3<float> split_sum(const Params<float> &p, const TileHdr *h, const unsigned char *bl,
+                                               const float4 *sX, const float4 *sP, int l, int role,
+                                               float4 x4, float4 p4) {
+    V3<float> sum = {0.f, 0.f, 0.f};
+    unsigned deg = 0;
+    const V3<float> xm = {x4.x, x4.y, x4.z}, pm = {p4.x, p4.y, p4.z};
+    const int W = (int)h->W, Wr = (int)h->Wr;
+    const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + h->off_cnt)[l];
+    const uint16_t *oo = reinterpret_cast<const uint16_t *>(bl + h->off_oo);
+    const float2 *okl = reinterpret_cast<const float2 *>(bl + h->off_okl);
+    const int8_t *og = h->off_og ? reinterpret_cast<const int8_t *>(bl + h->off_og) : nullptr;
+    if (role == 0) {
+        const int n_ref = cnt >> 8;
+        const uint16_t *fo = reinterpret_cast<const uint16_t *>(bl + h->off_fo);
+        const float2 *fkl = reinterpret_cast<const float2 *>(bl + h->off_fkl);
+        const int8_t *fg = h->off_fg ? reinterpret_cast<const int8_t *>(bl + h->off_fg) : nullptr;
+        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + (l >> 5) * Wr * 32 + (l & 31);
+#pragma unroll 2
+        for (int q = 0; q < n_ref; ++q) {
+            const uint32_t v = rf[q * 32];
+            const bool foreign = (v & 0x8000u) != 0;
+            const uint32_t ol = v & 0xffu;
+            const uint32_t slot = ((ol >> 5) * W + (v >> 8)) * 32 + (ol & 31u);
+            const uint32_t idx = foreign ? (v & 0x7fffu) : slot;
+            const float2 kl = foreign ? fkl[idx] : okl[idx];
+            int o;
+            bool mine = false;
+            if constexpr (CANON) {
+                o = foreign ? (int)fo[idx] : (int)ol;
+            } else {
+                mine = !foreign && (int)ol == l;
+                o = foreign ? (int)fo[idx] : (mine ? (int)oo[slot] : (int)ol);
+            }
+            float l0 = kl.y;
+            if constexpr (GROUPS) {
+                if (og) {
+                    const int g = foreign ? fg[idx] : og[idx];
+                    if (g >= 0) l0 = l0 * p.scale[g];
+                }
+            }
+            spring_term<true>(sX[o], sP[o], xm, pm, kl.x, l0, sum, mine, deg);
+        }
+    } else {
+        const int n_own = cnt & 0xff;
+        const int base = (l >> 5) * W * 32 + (l & 31);
+#pragma unroll 2
+        for (int q = 0; q < n_own; ++q) {
+            const int slot = base + q * 32;
+            const int o = oo[slot];
+            const float2 kl = okl[slot];
+            float l0 = kl.y;
+            if constexpr (GROUPS) {
+                if (og) {
+                    const int g = og[slot];
+                    if (g >= 0) l0 = l0 * p.scale[g];
+                }
+            }
+            spring_term<true>(sX[o], sP[o], xm, pm, kl.x, l0, sum, true, deg);
+        }
+    }
+    flush_degenerate(p.degenerate, deg);
+    return sum;
+}
+
+// External forces + Euler/Verlet update + restore fixed + store + finiteness
+// check of device mass m (engine.py:273-328, 297-301, 375-381).
+template <int INTEG>
+__device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V3<float> sum, float4 x4,
+                                                float4 p4, float4 v4, float4 xp4, bool need_prev) {
+    const float mass = fabsf(x4.w);
+    const bool fixed = signbit(x4.w);
+    const V3<float> xa = {p4.x + x4.x, p4.y + x4.y, p4.z + x4.z};
+    const V3<float> f = add_external<true>(p, m, sum, xa, v4, mass);
+    float xn[3], vn[3];
+    const float x[3] = {x4.x, x4.y, x4.z};
+    const float v[3] = {v4.x, v4.y, v4.z};
+    const float fc[3] = {f.x, f.y, f.z};
+    if constexpr (INTEG == 0) {
+        const float dtm = p.dt / mass;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            xn[c] = x[c] + p.dt * v[c];
+            vn[c] = v[c] + dtm * fc[c];
+            if (p.damped) vn[c] = vn[c] * p.one_minus_d;
+        }
+    } else {
+        const float coef = p.dt2_over / mass;
+        if (!need_prev) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                xn[c] = (x[c] + p.dt * v[c]) + 0.5f * (coef * fc[c]);
+                vn[c] = v[c];
+            }
+        } else {
+            const float xp[3] = {xp4.x, xp4.y, xp4.z};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float acc = coef * fc[c];
+                if (p.damped) xn[c] = (x[c] + p.one_minus_d * (x[c] - xp[c])) + acc;
+                else          xn[c] = (2.f * x[c] - xp[c]) + acc;
+                vn[c] = (xn[c] - xp[c]) / p.two_dt;
+            }
+        }
+    }
+    if (fixed) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { xn[c] = x[c]; vn[c] = v[c]; }
+    }
+    p.Xout[m] = make_float4(xn[0], xn[1], xn[2], x4.w);
+    p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
+    if (!(finite3<true>(xn[0], xn[1], xn[2]) && finite3<true>(vn[0], vn[1], vn[2])))
+        flag_divergence<true>(p, m);
+}
+
+// --------------------------------------------------- one tile per CTA, 512 threads
+
+// Role-split partial spring sum of tile mass l from the staged tile-local
+// positions y (stage_tile<true>): role 0 the references, role 1 the own records.
+template <bool CANON, bool GROUPS>
+__device__ __forceinline__ V3<float> split_sum_y(const Params<float> &p, const TileCtx<true> &c, int l,
+                                                 int role) {
+    V3<float> sum = {0.f, 0.f, 0.f};
+    unsigned deg = 0;
+    const TileHdr *h = c.h;
+    const unsigned char *bl = c.blob;
+    const float4 y = c.sX[l];
+    const V3<float> ym = {y.x, y.y, y.z};
+    const int W = (int)h->W, Wr = (int)h->Wr;
+    const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + h->off_cnt)[l];
+    const uint16_t *oo = reinterpret_cast<const uint16_t *>(bl + h->off_oo);
+    const float2 *okl = reinterpret_cast<const float2 *>(bl + h->off_okl);
+    const int8_t *og = h->off_og ? reinterpret_cast<const int8_t *>(bl + h->off_og) : nullptr;
+    if (role == 0) {
+        const int n_ref = cnt >> 8;
+        const uint16_t *fo = reinterpret_cast<const uint16_t *>(bl + h->off_fo);
+        const float2 *fkl = reinterpret_cast<const float2 *>(bl + h->off_fkl);
+        const int8_t *fg = h->off_fg ? reinterpret_cast<const int8_t *>(bl + h->off_fg) : nullptr;
+        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + (l >> 5) * Wr * 32 + (l & 31);
+#pragma unroll 2
+        for (int q = 0; q < n_ref; ++q) {
+            const uint32_t v = rf[q * 32];
+            const bool foreign = (v & 0x8000u) != 0;
+            const uint32_t ol = v & 0xffu;
+            const uint32_t slot = ((ol >> 5) * W + (v >> 8)) * 32 + (ol & 31u);
+            const uint32_t idx = foreign ? (v & 0x7fffu) : slot;
+            const float2 kl = foreign ? fkl[idx] : okl[idx];
+            int o;
+            bool mine = false;
+            if constexpr (CANON) {
+                o = foreign ? (int)fo[idx] : (int)ol;
+            } else {
+                mine = !foreign && (int)ol == l;
+                o = foreign ? (int)fo[idx] : (mine ? (int)oo[slot] : (int)ol);
+            }
+            float l0 = kl.y;
+            if constexpr (GROUPS) {
+                if (og) {
+                    const int g = foreign ? fg[idx] : og[idx];
+                    if (g >= 0) l0 = l0 * p.scale[g];
+                }
+            }
+            spring_term_y(c.sX[o], ym, kl.x, l0, sum, mine, deg);
+        }
+    } else {
+        const int n_own = cnt & 0xff;
+        const int base = (l >> 5) * W * 32 + (l & 31);
+#pragma unroll 2
+        for (int q = 0; q < n_own; ++q) {
+            const int slot = base + q * 32;
+            const float2 kl = okl[slot];
+            float l0 = kl.y;
+            if constexpr (GROUPS) {
+                if (og) {
+                    const int g = og[slot];
+                    if (g >= 0) l0 = l0 * p.scale[g];
+                }
+            }
+            spring_term_y(c.sX[oo[slot]], ym, kl.x, l0, sum, true, deg);
+        }
+    }
+    flush_degenerate(p.degenerate, deg);
+    return sum;
+}
+
+template <int INTEG, bool CANON, bool GROUPS>
+__global__ void __launch_bounds__(kPipeThreads, 3) tile_step2_kernel(Params<float> p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (*p.div_step < p.step) return;                       // grid-uniform
+    const Topology<float> &t = p.topo;
+    const int tid = threadIdx.x;
+    const int role = tid >> 8;
+    const int l = tid & (kTile - 1);
+    const int m = blockIdx.x * kTile + l;
+    const int n = (int)(__ldg(t.tsplit + blockIdx.x) >> 24) + 1;
+    const bool active = l < n;
+    const bool need_prev = INTEG == 1 && !p.bootstrap;
+    // the epilogue thread (role 0) prefetches V and x_prev before the staging
+    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f), xp4 = v4;
+    if (active && role == 0) {
+        v4 = p.V[m];
+        if (need_prev) xp4 = p.Xprev[m];
+    }
+    const TileCtx<true> ctx = stage_tile<true>(p, smem, m, active && role == 0);
+    float4 *part = ctx.sX + (kTile + t.max_halo);
+    V3<float> sum = {0.f, 0.f, 0.f};
+    if (active) {
+        if (p.debug != 1) sum = split_sum_y<CANON, GROUPS>(p, ctx, l, role);
+        if (role == 1) part[l] = make_float4(sum.x, sum.y, sum.z, 0.f);
+    }
+    __syncthreads();
+    if (active && role == 0) {
+        const float4 pr = part[l];
+        sum.x += pr.x;
+        sum.y += pr.y;
+        sum.z += pr.z;
+        integrate_store<INTEG>(p, m, sum, ctx.own_x, ctx.own_p, v4, xp4, need_prev);
+    }
+}
+
+// ------------------------------------------------------- persistent, pipelined
+
+// Shared-memory carve-up (pointers derived arithmetically from the extern
+// __shared__ base so the compiler emits LDS/STS):
+// [barriers | 3 heads | 2 record buffers | 2 x state | partials]
 struct PipeGeom {
-    uint32_t head, rest, slots;       // bytes per head / records buffer, state slots
+    uint32_t head, rest, slots;
     __device__ __forceinline__ unsigned char *head_buf(unsigned char *smem, int k) const {
         return smem + 128 + k * head;
     }
@@ -51,7 +274,6 @@ __device__ __forceinline__ uint32_t tile_split(const Topology<float> &t, int til
     return t.tsplit[tile] & 0xffffffu;
 }
 
-// thread 0: TMA of tile `tile`'s head (header + halo ids) / records
 __device__ __forceinline__ void pipe_issue_head(const Topology<float> &t, int tile, unsigned char *dst,
                                                 uint64_t *bar) {
     bulk_copy(dst, t.blob + t.toff[tile], tile_split(t, tile), bar);
@@ -97,7 +319,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) tile_pipe_kernel(Params<float
     if (*p.div_step < p.step) return;                       // grid-uniform
     const Topology<float> &t = p.topo;
     const int tid = threadIdx.x;
-    const int role = tid >> 8;                              // 0 refs + epilogue, 1 own records
+    const int role = tid >> 8;
     const int l = tid & (kTile - 1);
     uint64_t *hbar = reinterpret_cast<uint64_t *>(smem);    // 3 head barriers
     uint64_t *rbar = hbar + 3;                              // 2 record barriers
@@ -143,135 +365,30 @@ __global__ void __launch_bounds__(kPipeThreads, 1) tile_pipe_kernel(Params<float
                                      stn + 2 * G.slots, stn + 2 * G.slots + kTile, need_prev);
         }
         mbar_wait(rbar + b2, (uint32_t)(i >> 1) & 1u);      // records of tile i
-        // ---- forces from shared memory
-        const unsigned char *head = G.head_buf(smem, b3);
-        const TileHdr *h = reinterpret_cast<const TileHdr *>(head);
+        const TileHdr *h = reinterpret_cast<const TileHdr *>(G.head_buf(smem, b3));
         const unsigned char *bl = G.rest_buf(smem, b2) - tile_split(t, tile);   // offsets are blob-relative
         const float4 *sX = G.state(smem, b2), *sP = sX + G.slots;
         const float4 *sV = sX + 2 * G.slots, *sXp = sX + 2 * G.slots + kTile;
         const int n = (int)h->n;
-        const int W = (int)h->W, Wr = (int)h->Wr;
         V3<float> sum = {0.f, 0.f, 0.f};
-        unsigned deg = 0;
         float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), p4 = x4;
         if (l < n) {
             x4 = sX[l];
             p4 = sP[l];
-            const V3<float> xm = {x4.x, x4.y, x4.z}, pm = {p4.x, p4.y, p4.z};
-            const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + h->off_cnt)[l];
-            const uint16_t *oo = reinterpret_cast<const uint16_t *>(bl + h->off_oo);
-            const float2 *okl = reinterpret_cast<const float2 *>(bl + h->off_okl);
-            const int8_t *og = h->off_og ? reinterpret_cast<const int8_t *>(bl + h->off_og) : nullptr;
-            if (role == 0) {
-                const int n_ref = cnt >> 8;
-                const uint16_t *fo = reinterpret_cast<const uint16_t *>(bl + h->off_fo);
-                const float2 *fkl = reinterpret_cast<const float2 *>(bl + h->off_fkl);
-                const int8_t *fg = h->off_fg ? reinterpret_cast<const int8_t *>(bl + h->off_fg) : nullptr;
-                const uint16_t *rf =
-                    reinterpret_cast<const uint16_t *>(bl + h->off_ref) + (l >> 5) * Wr * 32 + (l & 31);
-#pragma unroll 2
-                for (int q = 0; q < n_ref; ++q) {
-                    const uint32_t v = rf[q * 32];
-                    const bool foreign = (v & 0x8000u) != 0;
-                    const uint32_t ol = v & 0xffu;
-                    const uint32_t slot = ((ol >> 5) * W + (v >> 8)) * 32 + (ol & 31u);
-                    const uint32_t idx = foreign ? (v & 0x7fffu) : slot;
-                    const float2 kl = foreign ? fkl[idx] : okl[idx];
-                    int o;
-                    bool mine = false;
-                    if constexpr (CANON) {
-                        o = foreign ? (int)fo[idx] : (int)ol;
-                    } else {
-                        mine = !foreign && (int)ol == l;
-                        o = foreign ? (int)fo[idx] : (mine ? (int)oo[slot] : (int)ol);
-                    }
-                    float l0 = kl.y;
-                    if constexpr (GROUPS) {
-                        if (og) {
-                            const int g = foreign ? fg[idx] : og[idx];
-                            if (g >= 0) l0 = l0 * p.scale[g];
-                        }
-                    }
-                    spring_term<true>(sX[o], sP[o], xm, pm, kl.x, l0, sum, mine, deg);
-                }
-            } else {
-                const int n_own = cnt & 0xff;
-                const int base = (l >> 5) * W * 32 + (l & 31);
-#pragma unroll 2
-                for (int q = 0; q < n_own; ++q) {
-                    const int slot = base + q * 32;
-                    const int o = oo[slot];
-                    const float2 kl = okl[slot];
-                    float l0 = kl.y;
-                    if constexpr (GROUPS) {
-                        if (og) {
-                            const int g = og[slot];
-                            if (g >= 0) l0 = l0 * p.scale[g];
-                        }
-                    }
-                    spring_term<true>(sX[o], sP[o], xm, pm, kl.x, l0, sum, true, deg);
-                }
-                part[l] = make_float4(sum.x, sum.y, sum.z, 0.f);
-            }
+            sum = split_sum<CANON, GROUPS>(p, h, bl, sX, sP, l, role, x4, p4);
+            if (role == 1) part[l] = make_float4(sum.x, sum.y, sum.z, 0.f);
         }
-        flush_degenerate(p.degenerate, deg);
-        __syncthreads();                                    // own-record partials visible
-        // ---- epilogue (role 0): combine, external forces, integrate
+        __syncthreads();
         if (role == 0 && l < n) {
             const float4 pr = part[l];
             sum.x += pr.x;
             sum.y += pr.y;
             sum.z += pr.z;
-            const int m = tile * kTile + l;
-            const float mass = fabsf(x4.w);
-            const bool fixed = signbit(x4.w);
-            const float4 v4 = sV[l];
-            const V3<float> xa = {p4.x + x4.x, p4.y + x4.y, p4.z + x4.z};
-            const V3<float> f = add_external<true>(p, m, sum, xa, v4, mass);
-            float xn[3], vn[3];
-            const float x[3] = {x4.x, x4.y, x4.z};
-            const float v[3] = {v4.x, v4.y, v4.z};
-            const float fc[3] = {f.x, f.y, f.z};
-            if constexpr (INTEG == 0) {
-                const float dtm = p.dt / mass;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    xn[c] = x[c] + p.dt * v[c];
-                    vn[c] = v[c] + dtm * fc[c];
-                    if (p.damped) vn[c] = vn[c] * p.one_minus_d;
-                }
-            } else {
-                const float coef = p.dt2_over / mass;
-                if (!need_prev) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        xn[c] = (x[c] + p.dt * v[c]) + 0.5f * (coef * fc[c]);
-                        vn[c] = v[c];
-                    }
-                } else {
-                    const float4 xp4 = sXp[l];
-                    const float xp[3] = {xp4.x, xp4.y, xp4.z};
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float acc = coef * fc[c];
-                        if (p.damped) xn[c] = (x[c] + p.one_minus_d * (x[c] - xp[c])) + acc;
-                        else          xn[c] = (2.f * x[c] - xp[c]) + acc;
-                        vn[c] = (xn[c] - xp[c]) / p.two_dt;
-                    }
-                }
-            }
-            if (fixed) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) { xn[c] = x[c]; vn[c] = v[c]; }
-            }
-            p.Xout[m] = make_float4(xn[0], xn[1], xn[2], x4.w);
-            p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
-            if (!(finite3<true>(xn[0], xn[1], xn[2]) && finite3<true>(vn[0], vn[1], vn[2])))
-                flag_divergence<true>(p, m);
+            integrate_store<INTEG>(p, tile * kTile + l, sum, x4, p4, sV[l], sXp[l], need_prev);
         }
         cp_async_wait_all();                                // tile i+1's state landed
         __syncthreads();                                    // stage i free
-        if (tid == 0 && i + 2 < n_mine)                     // records of tile i+2 into the freed buffer
+        if (tid == 0 && i + 2 < n_mine)
             pipe_issue_rest(t, tile + 2 * stride, G.rest_buf(smem, b2), rbar + b2);
     }
 }
