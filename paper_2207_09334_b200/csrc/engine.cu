@@ -22,6 +22,8 @@
 #include "common.h"
 #include "kernels.cuh"
 #include "pipe_kernel.cuh"
+#include "once_kernel.cuh"
+#include "fast_kernel.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
 #include "tiles.h"
@@ -104,6 +106,10 @@ struct ss_engine {
     size_t smem_bytes = 0;
     size_t pipe_smem = 0;          // persistent pipelined kernel (fp32 Euler/Verlet), 0 = off
     size_t step2_smem = 0;         // 512-thread tile kernel (fp32 Euler/Verlet), 0 = off
+    size_t once_smem = 0;          // spring-once tile kernel (fp32 Euler/Verlet), 0 = off
+    int once_minb = 3;             // its register budget: 2 or 3 resident CTAs per SM
+    size_t fast_smem = 0;          // record-pass tile kernel (fp32 Euler/Verlet), 0 = off
+    size_t lean_smem = 0;          // one-thread-per-mass spring-once tile kernel (fp32 Euler/Verlet, default)
     int pipe_grid = 0;
     int64_t device_bytes = 0;
     int64_t launches = 0;
@@ -433,6 +439,34 @@ int launch_steps(ss_engine *h, int64_t count) {
                         tile_pipe_kernel<1, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
                     goto launched;
                 }
+                if (h->lean_smem) {
+                    constexpr bool GROUPS = LAYOUT == 3;
+                    if (h->integrator == SS_EULER)
+                        tile_lean_kernel<0, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
+                    else
+                        tile_lean_kernel<1, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
+                    goto launched;
+                }
+                if (h->fast_smem) {
+                    constexpr bool GROUPS = LAYOUT == 3;
+                    if (h->integrator == SS_EULER)
+                        tile_fast_kernel<0, GROUPS><<<grid, kPipeThreads, h->fast_smem, h->stream>>>(p);
+                    else
+                        tile_fast_kernel<1, GROUPS><<<grid, kPipeThreads, h->fast_smem, h->stream>>>(p);
+                    goto launched;
+                }
+                if (h->once_smem) {
+                    constexpr bool GROUPS = LAYOUT == 3;
+                    const bool euler = h->integrator == SS_EULER;
+                    if (h->once_minb == 2) {
+                        if (euler) tile_once_kernel<0, GROUPS, 2><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
+                        else       tile_once_kernel<1, GROUPS, 2><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
+                    } else {
+                        if (euler) tile_once_kernel<0, GROUPS, 3><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
+                        else       tile_once_kernel<1, GROUPS, 3><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
+                    }
+                    goto launched;
+                }
                 if (h->step2_smem) {
                     constexpr bool CANON = LAYOUT == 4, GROUPS = LAYOUT == 3;
                     if (h->integrator == SS_EULER)
@@ -654,9 +688,45 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             int sms = 0;
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
             // kernel choice for fp32 Euler/Verlet on tiles:
-            // SS_KERNEL=step2 (default, 512 threads/tile), step1 (256), pipe (persistent)
+            // SS_KERNEL=lean (default: spring-once, one thread per mass), fast
+            // (record pass + mass pass, 512 threads/tile),
+            // once (spring-once mass-centric), step2 (512 threads, per-endpoint
+            // gather), step1 (256), pipe (persistent)
             const char *kenv = getenv("SS_KERNEL");
-            const std::string kname = kenv ? kenv : "step2";
+            const std::string kname = kenv ? kenv : "lean";
+            if (kname == "lean" && h->integrator != SS_RK4 && !L.has_self &&
+                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
+                h->lean_smem = h->smem_bytes + kTile * sizeof(float4);
+                const int b = dev_max;
+                CK(cudaFuncSetAttribute(tile_lean_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_lean_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_lean_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_lean_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+            if (kname == "fast" && h->integrator != SS_RK4 && !L.has_self &&
+                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
+                h->fast_smem = h->smem_bytes + kTile * sizeof(float4);
+                const int b = dev_max;
+                CK(cudaFuncSetAttribute(tile_fast_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_fast_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_fast_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_fast_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+            if (kname == "once" && h->integrator != SS_RK4 && L.canonical &&
+                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
+                h->once_smem = h->smem_bytes + kTile * sizeof(float4);
+                const int b = dev_max;
+                const char *mb = getenv("SS_ONCE_MINB");     // CTAs/SM the registers are budgeted for
+                h->once_minb = mb ? atoi(mb) : 3;
+                CK(cudaFuncSetAttribute(tile_once_kernel<0, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<0, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<1, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<0, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<1, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<0, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_once_kernel<1, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
             if (kname == "step2" && h->integrator != SS_RK4 &&
                 (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
                 h->step2_smem = h->smem_bytes + kTile * sizeof(float4);

@@ -46,13 +46,13 @@ __device__ __forceinline__ V3<float> split_sum(const Params<float> &p, const Til
         const uint16_t *fo = reinterpret_cast<const uint16_t *>(bl + h->off_fo);
         const float2 *fkl = reinterpret_cast<const float2 *>(bl + h->off_fkl);
         const int8_t *fg = h->off_fg ? reinterpret_cast<const int8_t *>(bl + h->off_fg) : nullptr;
-        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + (l >> 5) * Wr * 32 + (l & 31);
+        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + ell_slot(l, 0, Wr, h->slice_log2);
 #pragma unroll 2
         for (int q = 0; q < n_ref; ++q) {
-            const uint32_t v = rf[q * 32];
+            const uint32_t v = rf[q << h->slice_log2];
             const bool foreign = (v & 0x8000u) != 0;
             const uint32_t ol = v & 0xffu;
-            const uint32_t slot = ((ol >> 5) * W + (v >> 8)) * 32 + (ol & 31u);
+            const uint32_t slot = ell_slot(ol, v >> 8, W, h->slice_log2);
             const uint32_t idx = foreign ? (v & 0x7fffu) : slot;
             const float2 kl = foreign ? fkl[idx] : okl[idx];
             int o;
@@ -74,10 +74,10 @@ __device__ __forceinline__ V3<float> split_sum(const Params<float> &p, const Til
         }
     } else {
         const int n_own = cnt & 0xff;
-        const int base = (l >> 5) * W * 32 + (l & 31);
+        const int base = ell_slot(l, 0, W, h->slice_log2);
 #pragma unroll 2
         for (int q = 0; q < n_own; ++q) {
-            const int slot = base + q * 32;
+            const int slot = base + (q << h->slice_log2);
             const int o = oo[slot];
             const float2 kl = okl[slot];
             float l0 = kl.y;
@@ -167,13 +167,13 @@ __device__ __forceinline__ V3<float> split_sum_y(const Params<float> &p, const T
         const uint16_t *fo = reinterpret_cast<const uint16_t *>(bl + h->off_fo);
         const float2 *fkl = reinterpret_cast<const float2 *>(bl + h->off_fkl);
         const int8_t *fg = h->off_fg ? reinterpret_cast<const int8_t *>(bl + h->off_fg) : nullptr;
-        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + (l >> 5) * Wr * 32 + (l & 31);
+        const uint16_t *rf = reinterpret_cast<const uint16_t *>(bl + h->off_ref) + ell_slot(l, 0, Wr, h->slice_log2);
 #pragma unroll 2
         for (int q = 0; q < n_ref; ++q) {
-            const uint32_t v = rf[q * 32];
+            const uint32_t v = rf[q << h->slice_log2];
             const bool foreign = (v & 0x8000u) != 0;
             const uint32_t ol = v & 0xffu;
-            const uint32_t slot = ((ol >> 5) * W + (v >> 8)) * 32 + (ol & 31u);
+            const uint32_t slot = ell_slot(ol, v >> 8, W, h->slice_log2);
             const uint32_t idx = foreign ? (v & 0x7fffu) : slot;
             const float2 kl = foreign ? fkl[idx] : okl[idx];
             int o;
@@ -195,10 +195,10 @@ __device__ __forceinline__ V3<float> split_sum_y(const Params<float> &p, const T
         }
     } else {
         const int n_own = cnt & 0xff;
-        const int base = (l >> 5) * W * 32 + (l & 31);
+        const int base = ell_slot(l, 0, W, h->slice_log2);
 #pragma unroll 2
         for (int q = 0; q < n_own; ++q) {
-            const int slot = base + q * 32;
+            const int slot = base + (q << h->slice_log2);
             const float2 kl = okl[slot];
             float l0 = kl.y;
             if constexpr (GROUPS) {

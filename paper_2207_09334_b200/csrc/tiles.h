@@ -12,6 +12,10 @@ constexpr int kTile = 256;            // masses per tile == threads per CTA
 // Section order: header | halo ids | counts | own other | own (k,l0) | own grp |
 // refs | foreign owner | foreign (k,l0) | foreign grp.  [0, off_cnt) is copied
 // first so the halo gather overlaps the record stream.
+// fp32 builds (any summation order is within the production tolerance)
+// treat every mass as canonical and list a mass's foreign references before
+// its in-tile ones; off_nf holds the per-mass count of the leading foreign
+// references, so the spring-once kernel can split its two reference passes.
 //   ref value: bit 15 set  -> foreign record index (bits 0-14)
 //              bit 15 clear-> in-tile record: owner local id (bits 0-7), slot q (bits 8-14)
 struct TileHdr {
@@ -19,7 +23,10 @@ struct TileHdr {
     uint32_t n_foreign, bytes, off_cnt, off_oo;
     uint32_t off_okl, off_og, off_ref, off_fo;
     uint32_t off_fkl, off_fg, off_halo, canonical;
-    uint32_t pad0, pad1, pad2, pad3;
+    uint32_t off_nf;       // u8 per mass: leading foreign refs (fp32 builds)
+    uint32_t slice_log2;   // sliced-ELL slice of 2^slice_log2 masses (fp64 builds 5, fp32 builds 8)
+    uint32_t off_fl;       // u8 per foreign record: its tile-local partner
+    uint32_t pad3;
 };
 static_assert(sizeof(TileHdr) == 80, "TileHdr must stay 80 bytes");
 
@@ -32,6 +39,17 @@ struct TileInput {
     bool f32;                    // record precision
     int order;                   // 0 identity, 1 brick
 };
+
+// Sliced-ELL position of entry q of tile mass l (slices of 2^sl masses, W
+// entries per slice row).  fp32 builds use sl = 8 (one slice per tile), so
+// slot = q*256 + l and an in-tile reference value (q << 8 | owner) IS the
+// owner's record slot.
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline uint32_t ell_slot(uint32_t l, uint32_t q, uint32_t W, uint32_t sl) {
+    return (((l >> sl) * W + q) << sl) | (l & ((1u << sl) - 1u));
+}
 
 struct TileLayout {
     std::vector<int32_t> orig_of;   // new id -> original id (empty: identity)
@@ -46,6 +64,7 @@ struct TileLayout {
     uint32_t max_halo = 0;
     int max_W = 0, max_Wr = 0;
     bool canonical = true;
+    bool has_self = false;          // a spring joins a mass to itself
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };
