@@ -55,7 +55,8 @@ class Info(C.Structure):
                 ("ell_width_own", C.c_int32), ("ell_width_ref", C.c_int32),
                 ("canonical_order", C.c_int32), ("smem_per_block", C.c_int32),
                 ("tile_count", C.c_int64), ("tile_blob_bytes", C.c_int64),
-                ("tile_halo_ratio", C.c_double), ("tile_foreign_frac", C.c_double)]
+                ("tile_halo_ratio", C.c_double), ("tile_foreign_frac", C.c_double),
+                ("tile_kernel", C.c_int32), ("kernel_smem", C.c_int32)]
 
 
 # Every symbol include/springsim_b200.h declares, with its ctypes signature.

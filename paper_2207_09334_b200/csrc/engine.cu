@@ -21,9 +21,7 @@
 
 #include "common.h"
 #include "kernels.cuh"
-#include "pipe_kernel.cuh"
-#include "once_kernel.cuh"
-#include "fast_kernel.cuh"
+#include "tile_f32.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
 #include "tiles.h"
@@ -86,6 +84,7 @@ struct ss_engine {
     void *scale = nullptr;
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
+    unsigned long long *d_prof = nullptr;      // 16 phase-cycle counters (SS_PROF)
     long long *d_div_step = nullptr;
     int *d_div_mass = nullptr;
     int *d_orig_of = nullptr;
@@ -104,13 +103,9 @@ struct ss_engine {
     unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
-    size_t pipe_smem = 0;          // persistent pipelined kernel (fp32 Euler/Verlet), 0 = off
-    size_t step2_smem = 0;         // 512-thread tile kernel (fp32 Euler/Verlet), 0 = off
-    size_t once_smem = 0;          // spring-once tile kernel (fp32 Euler/Verlet), 0 = off
-    int once_minb = 3;             // its register budget: 2 or 3 resident CTAs per SM
-    size_t fast_smem = 0;          // record-pass tile kernel (fp32 Euler/Verlet), 0 = off
-    size_t lean_smem = 0;          // one-thread-per-mass spring-once tile kernel (fp32 Euler/Verlet, default)
-    int pipe_grid = 0;
+    size_t ws_smem = 0;            // persistent warp-specialized tile kernel (fp32 Euler/Verlet), 0 = off
+    int ws_grid = 0;
+    size_t lean_smem = 0;          // one-tile-per-CTA spring-once kernel (fp32 Euler/Verlet), 0 = off
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -326,8 +321,6 @@ Params<T> base_params(const ss_engine *h) {
     tp.blob_smem = h->blob_smem;
     tp.max_halo = h->max_halo;
     tp.n_tiles = (int)h->tl.n_tiles;
-    tp.head_smem = (h->tl.max_head_bytes + 127u) & ~127u;
-    tp.rest_smem = (h->tl.max_rest_bytes + 127u) & ~127u;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -344,6 +337,7 @@ Params<T> base_params(const ss_engine *h) {
         p.pfric[q] = (T)h->planes[6 * q + 5];
     }
     p.degenerate = h->d_degenerate;
+    p.prof = getenv("SS_PROF") ? h->d_prof : nullptr;
     p.div_step = h->d_div_step;
     p.div_mass = h->d_div_mass;
     if (const char *dbg = getenv("SS_DEBUG")) p.debug = atoi(dbg);   // timing experiments only
@@ -431,12 +425,12 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.Xprev = Xo;
             p.bootstrap = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
             if constexpr (F32 && LAYOUT >= 3) {
-                if (h->pipe_smem) {
-                    constexpr bool CANON = LAYOUT == 4, GROUPS = LAYOUT == 3;
+                if (h->ws_smem) {
+                    constexpr bool GROUPS = LAYOUT == 3;
                     if (h->integrator == SS_EULER)
-                        tile_pipe_kernel<0, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
+                        tile_ws_kernel<0, GROUPS><<<h->ws_grid, kWsThreads, h->ws_smem, h->stream>>>(p);
                     else
-                        tile_pipe_kernel<1, CANON, GROUPS><<<h->pipe_grid, kPipeThreads, h->pipe_smem, h->stream>>>(p);
+                        tile_ws_kernel<1, GROUPS><<<h->ws_grid, kWsThreads, h->ws_smem, h->stream>>>(p);
                     goto launched;
                 }
                 if (h->lean_smem) {
@@ -445,34 +439,6 @@ int launch_steps(ss_engine *h, int64_t count) {
                         tile_lean_kernel<0, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
                     else
                         tile_lean_kernel<1, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
-                    goto launched;
-                }
-                if (h->fast_smem) {
-                    constexpr bool GROUPS = LAYOUT == 3;
-                    if (h->integrator == SS_EULER)
-                        tile_fast_kernel<0, GROUPS><<<grid, kPipeThreads, h->fast_smem, h->stream>>>(p);
-                    else
-                        tile_fast_kernel<1, GROUPS><<<grid, kPipeThreads, h->fast_smem, h->stream>>>(p);
-                    goto launched;
-                }
-                if (h->once_smem) {
-                    constexpr bool GROUPS = LAYOUT == 3;
-                    const bool euler = h->integrator == SS_EULER;
-                    if (h->once_minb == 2) {
-                        if (euler) tile_once_kernel<0, GROUPS, 2><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
-                        else       tile_once_kernel<1, GROUPS, 2><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
-                    } else {
-                        if (euler) tile_once_kernel<0, GROUPS, 3><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
-                        else       tile_once_kernel<1, GROUPS, 3><<<grid, kPipeThreads, h->once_smem, h->stream>>>(p);
-                    }
-                    goto launched;
-                }
-                if (h->step2_smem) {
-                    constexpr bool CANON = LAYOUT == 4, GROUPS = LAYOUT == 3;
-                    if (h->integrator == SS_EULER)
-                        tile_step2_kernel<0, CANON, GROUPS><<<grid, kPipeThreads, h->step2_smem, h->stream>>>(p);
-                    else
-                        tile_step2_kernel<1, CANON, GROUPS><<<grid, kPipeThreads, h->step2_smem, h->stream>>>(p);
                     goto launched;
                 }
             }
@@ -679,71 +645,33 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         // the process: grant the device maximum, never a per-engine size
         if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
         if constexpr (F32) {
-            // persistent pipelined kernel: 3 heads + 2 record buffers + 2 state
-            // stages + partial sums
-            const size_t slots = kTile + L.max_halo;
-            const size_t head = (L.max_head_bytes + 127u) & ~127u, rest = (L.max_rest_bytes + 127u) & ~127u;
-            const size_t pipe = 128 + 3 * head + 2 * rest + 2 * (2 * slots + 2 * kTile) * sizeof(float4) +
-                                kTile * sizeof(float4);
+            // kernel choice for fp32 Euler/Verlet on tiles (DESIGN.md §4):
+            // SS_KERNEL=ws (default: persistent warp-specialized, one CTA per
+            // SM), lean (one tile per CTA; also the fallback when the 3-stage
+            // ring does not fit), step1 (kernels.cuh step_kernel).  The tile
+            // kernels need an fp32 build without self-springs.
             int sms = 0;
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-            // kernel choice for fp32 Euler/Verlet on tiles (DESIGN.md §3.4):
-            // SS_KERNEL=lean (default: spring-once, one thread per mass), fast
-            // (record pass + mass pass, 512 threads/tile),
-            // once (spring-once mass-centric), step2 (512 threads, per-endpoint
-            // gather), step1 (256), pipe (persistent)
             const char *kenv = getenv("SS_KERNEL");
-            const std::string kname = kenv ? kenv : "lean";
-            if (kname == "lean" && h->integrator != SS_RK4 && !L.has_self &&
-                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
-                h->lean_smem = h->smem_bytes + kTile * sizeof(float4);
-                const int b = dev_max;
+            const std::string kname = kenv ? kenv : "ws";
+            const bool tile_ok = h->integrator != SS_RK4 && !L.has_self;
+            const size_t ws = 128 + kWsStages * ws_stage_bytes(h->blob_smem, L.max_halo);
+            const int b = dev_max;
+            if (kname == "ws" && tile_ok && (int64_t)ws <= dev_max && L.n_tiles >= 2 * (int64_t)sms) {
+                h->ws_smem = ws;
+                h->ws_grid = sms;
+                CK(cudaFuncSetAttribute(tile_ws_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_ws_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_ws_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                CK(cudaFuncSetAttribute(tile_ws_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+            if ((kname == "lean" || (kname == "ws" && !h->ws_smem)) && tile_ok &&
+                (int64_t)h->smem_bytes <= dev_max) {
+                h->lean_smem = h->smem_bytes;
                 CK(cudaFuncSetAttribute(tile_lean_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 CK(cudaFuncSetAttribute(tile_lean_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 CK(cudaFuncSetAttribute(tile_lean_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 CK(cudaFuncSetAttribute(tile_lean_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-            }
-            if (kname == "fast" && h->integrator != SS_RK4 && !L.has_self &&
-                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
-                h->fast_smem = h->smem_bytes + kTile * sizeof(float4);
-                const int b = dev_max;
-                CK(cudaFuncSetAttribute(tile_fast_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_fast_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_fast_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_fast_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-            }
-            if (kname == "once" && h->integrator != SS_RK4 && L.canonical &&
-                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
-                h->once_smem = h->smem_bytes + kTile * sizeof(float4);
-                const int b = dev_max;
-                const char *mb = getenv("SS_ONCE_MINB");     // CTAs/SM the registers are budgeted for
-                h->once_minb = mb ? atoi(mb) : 3;
-                CK(cudaFuncSetAttribute(tile_once_kernel<0, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<0, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<1, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<0, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<1, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<0, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_once_kernel<1, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-            }
-            if (kname == "step2" && h->integrator != SS_RK4 &&
-                (int64_t)(h->smem_bytes + kTile * sizeof(float4)) <= dev_max) {
-                h->step2_smem = h->smem_bytes + kTile * sizeof(float4);
-                const int b = dev_max;
-                CK(cudaFuncSetAttribute(tile_step2_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_step2_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_step2_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_step2_kernel<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-            }
-            if ((int64_t)pipe <= dev_max && kname == "pipe" && h->integrator != SS_RK4) {
-                h->pipe_smem = pipe;
-                h->pipe_grid = (int)std::min<int64_t>(L.n_tiles, sms);
-                const int b = dev_max;
-                CK(cudaFuncSetAttribute(tile_pipe_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_pipe_kernel<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_pipe_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_pipe_kernel<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
         h->lay.canonical = L.canonical;
@@ -950,6 +878,8 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     int rc;
     if ((rc = h->alloc(&h->d_degenerate, sizeof(unsigned long long)))) return rc;
+    if ((rc = h->alloc(&h->d_prof, 16 * sizeof(unsigned long long)))) return rc;
+    CK(cudaMemsetAsync(h->d_prof, 0, 16 * sizeof(unsigned long long), h->stream));
     if ((rc = h->alloc(&h->d_div_step, sizeof(long long)))) return rc;
     if ((rc = h->alloc(&h->d_div_mass, sizeof(int)))) return rc;
     CK(cudaMemsetAsync(h->d_degenerate, 0, sizeof(unsigned long long), h->stream));
@@ -1152,6 +1082,8 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
+        info->tile_kernel = h->ws_smem ? 2 : (h->lean_smem ? 1 : 0);
+        info->kernel_smem = (int32_t)(h->ws_smem ? h->ws_smem : (h->lean_smem ? h->lean_smem : h->smem_bytes));
     } else {
         info->ell_width_own = h->lay.W;
         info->ell_width_ref = h->lay.Wr;
@@ -1161,6 +1093,15 @@ int ss_get_info(ss_engine *h, ss_info *info) {
 }
 
 int64_t ss_launch_count(ss_engine *h) { return h ? h->launches : 0; }
+
+// Development aid (not part of the public header): the SS_PROF phase-cycle
+// counters of the tile kernels.
+int ss_debug_prof(ss_engine *h, unsigned long long *out16) {
+    if (!h || !out16) return ss::fail(SS_EINVAL, "ss_debug_prof: null argument");
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(out16, h->d_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return SS_OK;
+}
 
 }  // extern "C"
 
@@ -1194,6 +1135,8 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
         (int32_t)(128 + ((tl.max_tile_bytes + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec);
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
+    info->kernel_smem = (int32_t)(128 + kWsStages * ws_stage_bytes((tl.max_tile_bytes + 127u) & ~127u, tl.max_halo));
+    info->tile_kernel = f32 && info->kernel_smem <= 232448 ? 2 : 1;   // B200 opt-in maximum per CTA
     return SS_OK;
 }
 

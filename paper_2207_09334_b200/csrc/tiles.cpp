@@ -34,6 +34,8 @@ namespace {
 
 inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
 
+}  // namespace
+
 // Device slot order: tile t owns slots [256t, 256t+256); real masses fill a
 // tile's first n slots, the rest are padding (-1).  With order == 1 the
 // masses are sorted into 4x8x8 bricks of quantised coordinates and whole
@@ -113,6 +115,8 @@ void tile_order(const TileInput &in, std::vector<int32_t> &orig_of) {
     pad_tile();
 }
 
+namespace {
+
 template <typename T>
 void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
     std::memcpy(blob.data() + off, &v, sizeof(T));
@@ -121,6 +125,7 @@ void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 }  // namespace
 
 int build_tiles(const TileInput &in, TileLayout &L) {
+    if (in.f32) return build_tiles_f32(in, L);
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
@@ -160,8 +165,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     std::vector<uint8_t> canon(D);
     bool all_canon = true;
     for (int64_t m = 0; m < D; ++m) {
-        // fp32: summation order is free (tolerance mode), every mass is canonical
-        const bool c = in.f32 || (ref_ptr[m + 1] == ref_ptr[m]) || (own_ptr[m + 1] == own_ptr[m]) ||
+        const bool c = (ref_ptr[m + 1] == ref_ptr[m]) || (own_ptr[m + 1] == own_ptr[m]) ||
                        ref_sp[ref_ptr[m + 1] - 1] < own_sp[own_ptr[m]];
         canon[m] = c;
         all_canon = all_canon && c;
@@ -213,15 +217,12 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             const auto it = std::lower_bound(halo.begin(), halo.end(), g);
             return (uint16_t)(kTile + (it - halo.begin()));
         };
-        // fp32 builds: one 256-wide slice (slot = q*256 + l), fp64: 32-wide slices
-        const uint32_t sl = in.f32 ? 8u : 5u;
+        const uint32_t sl = 5u;                // 32-wide slices
         const int slices = (n + (1 << sl) - 1) >> sl;
         const uint32_t own_n = ((uint32_t)slices * W) << sl, ref_n = ((uint32_t)slices * Wr) << sl;
         // foreign references (owner outside the tile)
         std::vector<int32_t> foreign;          // spring ids
-        std::vector<uint8_t> foreign_l;        // their tile-local partner
         std::vector<uint16_t> refs(ref_n, 0xffff);
-        std::vector<uint8_t> nfr(kTile, 0);    // leading foreign refs per mass (fp32)
         int64_t n_refs = 0;
         for (int l = 0; l < n; ++l) {
             const int64_t m = base + l;
@@ -235,23 +236,12 @@ int build_tiles(const TileInput &in, TileLayout &L) {
                 } else {
                     v = (uint16_t)(0x8000 | foreign.size());
                     foreign.push_back(s);
-                    foreign_l.push_back((uint8_t)l);
                 }
                 refs[ell_slot(l, q, Wr, sl)] = v;
                 ++q;
                 ++n_refs;
             };
-            auto in_tile = [&](int32_t s) {
-                const int32_t o = owner_new[s];
-                return o >= base && o < base + n;
-            };
-            if (in.f32) {                      // foreign first, then in-tile
-                for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r)
-                    if (!in_tile(ref_sp[r])) emit(ref_sp[r]);
-                nfr[l] = (uint8_t)q;
-                for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r)
-                    if (in_tile(ref_sp[r])) emit(ref_sp[r]);
-            } else if (canon[m]) {
+            if (canon[m]) {
                 for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r) emit(ref_sp[r]);
             } else {
                 int64_t a = ref_ptr[m], b = own_ptr[m];
@@ -276,7 +266,6 @@ int build_tiles(const TileInput &in, TileLayout &L) {
         uint32_t off = align16(sizeof(TileHdr));
         h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
         h.off_cnt = off; off = align16(off + kTile * 2);
-        h.off_nf = off;  off = align16(off + kTile);
         h.off_oo = off;  off = align16(off + own_n * 2);
         h.off_okl = off; off = align16(off + own_n * 2 * rs);
         h.off_og = 0;
@@ -286,17 +275,10 @@ int build_tiles(const TileInput &in, TileLayout &L) {
         h.off_fkl = off; off = align16(off + nf * 2 * rs);
         h.off_fg = 0;
         if (has_g) { h.off_fg = off; off = align16(off + nf); }
-        h.off_fl = off;  off = align16(off + nf);
         h.bytes = off;
         std::vector<uint8_t> &blob = parts[t];
         blob.assign(off, 0);
         std::memcpy(blob.data(), &h, sizeof h);
-        if (in.f32) {
-            // padding slots point at their own row's mass: d = 0, c = 0, never counted
-            for (uint32_t l = 0; l < ((uint32_t)slices << sl); ++l)
-                for (int q = 0; q < W; ++q)
-                    put<uint16_t>(blob, h.off_oo + 2 * ell_slot(l, q, W, sl), (uint16_t)l);
-        }
         for (int l = 0; l < n; ++l) {
             const int64_t m = base + l;
             const int no = canon[m] ? (int)(own_ptr[m + 1] - own_ptr[m]) : 0;
@@ -308,7 +290,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
                 put<uint16_t>(blob, h.off_oo + 2 * slot, local_of(other_new[s]));
                 if (in.f32) {
                     put<float>(blob, h.off_okl + 8 * slot, (float)in.k[s]);
-                    put<float>(blob, h.off_okl + 8 * slot + 4, (float)in.l0[s]);
+                    put<float>(blob, h.off_okl + 8 * slot + 4, (float)(in.k[s] * in.l0[s]));
                 } else {
                     put<double>(blob, h.off_okl + 16 * slot, in.k[s]);
                     put<double>(blob, h.off_okl + 16 * slot + 8, in.l0[s]);
@@ -317,19 +299,17 @@ int build_tiles(const TileInput &in, TileLayout &L) {
             }
         }
         std::memcpy(blob.data() + h.off_ref, refs.data(), refs.size() * 2);
-        std::memcpy(blob.data() + h.off_nf, nfr.data(), kTile);
         for (uint32_t f = 0; f < nf; ++f) {
             const int32_t s = foreign[f];
             put<uint16_t>(blob, h.off_fo + 2 * f, local_of(owner_new[s]));
             if (in.f32) {
                 put<float>(blob, h.off_fkl + 8 * f, (float)in.k[s]);
-                put<float>(blob, h.off_fkl + 8 * f + 4, (float)in.l0[s]);
+                put<float>(blob, h.off_fkl + 8 * f + 4, (float)(in.k[s] * in.l0[s]));
             } else {
                 put<double>(blob, h.off_fkl + 16 * f, in.k[s]);
                 put<double>(blob, h.off_fkl + 16 * f + 8, in.l0[s]);
             }
             if (has_g) put<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
-            put<uint8_t>(blob, h.off_fl + f, foreign_l[f]);
         }
         std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
         tW[t] = W; tWr[t] = Wr; tH[t] = (uint32_t)halo.size(); tF[t] = nf; tRefs[t] = n_refs;

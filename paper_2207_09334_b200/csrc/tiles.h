@@ -9,23 +9,35 @@ namespace ss {
 constexpr int kTile = 256;            // masses per tile == threads per CTA
 
 // Per-tile blob header (all offsets in bytes from the tile start, 16-B aligned).
-// Section order: header | halo ids | counts | own other | own (k,l0) | own grp |
-// refs | foreign owner | foreign (k,l0) | foreign grp.  [0, off_cnt) is copied
-// first so the halo gather overlaps the record stream.
-// fp32 builds (any summation order is within the production tolerance)
-// treat every mass as canonical and list a mass's foreign references before
-// its in-tile ones; off_nf holds the per-mass count of the leading foreign
-// references, so the spring-once kernel can split its two reference passes.
+// [0, off_cnt) (header + halo ids) is copied first so the halo gather
+// overlaps the record stream.
+//
+// fp64 builds (bit parity, tiles.cpp build_tiles): 32-wide ELL slices.
+//   Section order: header | halo ids | counts | own other | own (k,l0) |
+//   own grp | refs | foreign owner | foreign (k,l0) | foreign grp.
+//   counts: n_own | n_ref << 8.  A mass sums references then own records,
+//   both in ascending spring id (the reference's serial order).
 //   ref value: bit 15 set  -> foreign record index (bits 0-14)
 //              bit 15 clear-> in-tile record: owner local id (bits 0-7), slot q (bits 8-14)
+//
+// fp32 builds (production, tiles_f32.cpp build_tiles_f32): one 256-wide ELL
+// slice, slot = q*256 + l, records (other local u16, k f32, k*l0 f32
+// [, grp i8]) as planar arrays (the okl section is k[W*256] then
+// k*l0[W*256]; fkl likewise over the n_foreign copies); padding slots
+// point at their own mass with k = 0.  A
+// spring whose owner lies in another tile is copied into the partner's
+// tile (foreign owner, foreign local partner off_fl, (k, k*l0), grp).  A
+// mass's reference list holds its foreign references first (0x8000 | copy;
+// their count per mass in off_nf) and then its in-tile ones, whose value
+// is the owner's slot.  counts: n_own | n_ref << 8.
 struct TileHdr {
     uint32_t n, W, Wr, n_halo;
     uint32_t n_foreign, bytes, off_cnt, off_oo;
     uint32_t off_okl, off_og, off_ref, off_fo;
     uint32_t off_fkl, off_fg, off_halo, canonical;
-    uint32_t off_nf;       // u8 per mass: leading foreign refs (fp32 builds)
+    uint32_t off_nf;       // fp32 builds: u8 per mass, leading foreign references
     uint32_t slice_log2;   // sliced-ELL slice of 2^slice_log2 masses (fp64 builds 5, fp32 builds 8)
-    uint32_t off_fl;       // u8 per foreign record: its tile-local partner
+    uint32_t off_fl;       // fp32 builds: u8 per foreign copy, its local partner
     uint32_t pad3;
 };
 static_assert(sizeof(TileHdr) == 80, "TileHdr must stay 80 bytes");
@@ -69,6 +81,9 @@ struct TileLayout {
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };
 
-int build_tiles(const TileInput &in, TileLayout &out);
+int build_tiles(const TileInput &in, TileLayout &out);      // fp64; dispatches fp32 builds to:
+int build_tiles_f32(const TileInput &in, TileLayout &out);
+// Device slot order (brick renumbering, tiles padded to kTile slots).
+void tile_order(const TileInput &in, std::vector<int32_t> &orig_of);
 
 }  // namespace ss
