@@ -103,9 +103,7 @@ struct ss_engine {
     unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
-    size_t ws_smem = 0;            // persistent warp-specialized tile kernel (fp32 Euler/Verlet), 0 = off
-    int ws_grid = 0;
-    size_t lean_smem = 0;          // one-tile-per-CTA spring-once kernel (fp32 Euler/Verlet), 0 = off
+    size_t lean_smem = 0;          // fp32 Euler/Verlet tile kernel (tile_f32.cuh), 0 = off
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -393,6 +391,16 @@ int halo_exchange_nccl(ss_engine *h) {
     return SS_OK;
 }
 
+// fp32 Euler/Verlet step on tiles: tile_lean_kernel in the compact or the
+// explicit record format (tile_f32.cuh).
+template <bool GROUPS>
+void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
+    const bool euler = h->integrator == SS_EULER, compact = h->tl.compact;
+    auto *k = euler ? (compact ? tile_lean_kernel<0, GROUPS, 1> : tile_lean_kernel<0, GROUPS, 0>)
+                    : (compact ? tile_lean_kernel<1, GROUPS, 1> : tile_lean_kernel<1, GROUPS, 0>);
+    k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
@@ -425,20 +433,9 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.Xprev = Xo;
             p.bootstrap = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
             if constexpr (F32 && LAYOUT >= 3) {
-                if (h->ws_smem) {
-                    constexpr bool GROUPS = LAYOUT == 3;
-                    if (h->integrator == SS_EULER)
-                        tile_ws_kernel<0, GROUPS><<<h->ws_grid, kWsThreads, h->ws_smem, h->stream>>>(p);
-                    else
-                        tile_ws_kernel<1, GROUPS><<<h->ws_grid, kWsThreads, h->ws_smem, h->stream>>>(p);
-                    goto launched;
-                }
                 if (h->lean_smem) {
                     constexpr bool GROUPS = LAYOUT == 3;
-                    if (h->integrator == SS_EULER)
-                        tile_lean_kernel<0, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
-                    else
-                        tile_lean_kernel<1, GROUPS><<<grid, kTile, h->lean_smem, h->stream>>>(p);
+                    launch_tile_f32<GROUPS>(h, p, grid);
                     goto launched;
                 }
             }
@@ -634,7 +631,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         h->d_toff = reinterpret_cast<unsigned long long *>(p);
         if ((rc = up_vec(h, &p, L.split))) return rc;
         h->d_tsplit = reinterpret_cast<unsigned int *>(p);
-        h->blob_smem = (L.max_tile_bytes + 127u) & ~127u;
+        h->blob_smem = (L.max_tile_smem + 127u) & ~127u;
         h->max_halo = L.max_halo;
         h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4);   // one staged vector per mass
         int dev_max = 0;
@@ -645,33 +642,19 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         // the process: grant the device maximum, never a per-engine size
         if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
         if constexpr (F32) {
-            // kernel choice for fp32 Euler/Verlet on tiles:
-            // SS_KERNEL=ws (default: persistent warp-specialized, one CTA per
-            // SM), lean (one tile per CTA; also the fallback when the 3-stage
-            // ring does not fit), step1 (kernels.cuh step_kernel).  The tile
-            // kernels need an fp32 build without self-springs.
-            int sms = 0;
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+            // fp32 Euler/Verlet on tiles: tile_lean_kernel (tile_f32.cuh) unless
+            // SS_KERNEL=step1 asks for kernels.cuh's step_kernel; the tile
+            // kernels need a build without self-springs.
             const char *kenv = getenv("SS_KERNEL");
-            const std::string kname = kenv ? kenv : "ws";
-            const bool tile_ok = h->integrator != SS_RK4 && !L.has_self;
-            const size_t ws = 128 + kWsStages * ws_stage_bytes(h->blob_smem, L.max_halo);
-            const int b = dev_max;
-            if (kname == "ws" && tile_ok && (int64_t)ws <= dev_max && L.n_tiles >= 2 * (int64_t)sms) {
-                h->ws_smem = ws;
-                h->ws_grid = sms;
-                CK(cudaFuncSetAttribute(tile_ws_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_ws_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_ws_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_ws_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-            }
-            if ((kname == "lean" || (kname == "ws" && !h->ws_smem)) && tile_ok &&
-                (int64_t)h->smem_bytes <= dev_max) {
+            const std::string kname = kenv ? kenv : "lean";
+            if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
-                CK(cudaFuncSetAttribute(tile_lean_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_lean_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_lean_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                CK(cudaFuncSetAttribute(tile_lean_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+                const int b = dev_max;
+                for (auto *kk : {tile_lean_kernel<0, false, 0>, tile_lean_kernel<1, false, 0>,
+                                 tile_lean_kernel<0, true, 0>, tile_lean_kernel<1, true, 0>,
+                                 tile_lean_kernel<0, false, 1>, tile_lean_kernel<1, false, 1>,
+                                 tile_lean_kernel<0, true, 1>, tile_lean_kernel<1, true, 1>})
+                    CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
         h->lay.canonical = L.canonical;
@@ -1082,8 +1065,8 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
-        info->tile_kernel = h->ws_smem ? 2 : (h->lean_smem ? 1 : 0);
-        info->kernel_smem = (int32_t)(h->ws_smem ? h->ws_smem : (h->lean_smem ? h->lean_smem : h->smem_bytes));
+        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1) : 0;
+        info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->smem_bytes);
     } else {
         info->ell_width_own = h->lay.W;
         info->ell_width_ref = h->lay.Wr;
@@ -1132,11 +1115,11 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     info->tile_foreign_frac = tl.foreign_frac;
     const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
     info->smem_per_block =
-        (int32_t)(128 + ((tl.max_tile_bytes + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec);
+        (int32_t)(128 + ((tl.max_tile_smem + 127u) & ~127u) + (size_t)(kTile + tl.max_halo) * vec);
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
-    info->kernel_smem = (int32_t)(128 + kWsStages * ws_stage_bytes((tl.max_tile_bytes + 127u) & ~127u, tl.max_halo));
-    info->tile_kernel = f32 && info->kernel_smem <= 232448 ? 2 : 1;   // B200 opt-in maximum per CTA
+    info->kernel_smem = info->smem_per_block;
+    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : 0;
     return SS_OK;
 }
 

@@ -1,38 +1,25 @@
 // fp32 production-mode tile kernels (Euler / Verlet).  DESIGN.md §4.
 //
-// Both kernels evaluate every spring ONCE per tile it touches (spring-once),
-// on the fp32 tile layout of tiles_f32.cpp:
+// tile_lean_kernel: one tile (256 masses) per CTA of 256 threads; the tile
+// blob is TMA-bulk-copied into shared memory while the own states load and
+// the halo positions are gathered once as tile-local y = (P - A) + r; then
 //
-//   owner pass      one thread per tile mass walks its own records (slot =
-//                   q*256 + l): c = k - (k l0)/L, the term c*d is
-//                   accumulated in registers and c is written back over the
-//                   record's k in the tile's shared-memory copy;
-//   foreign pass    springs whose owner lies in another tile are evaluated
-//                   from the tile's copies, thread per record;
-//   barrier
-//   reference pass  each mass adds c * (y_owner - y_me): foreign references
-//                   first, then in-tile ones, whose value IS the owner's
-//                   slot -- one LDS c, one LDS.128 y, 3 FADD, 3 FFMA, no
-//                   square root;
-//   epilogue        external forces, Verlet / Euler, restore fixed,
-//                   finiteness (integrate_store).
+//   compact format (tiles.h, the default): each thread walks its mass's
+//     incidence list (partner slot, dictionary index) and sums
+//     c*d, c = k - (k l0)/L, evaluating each spring from both endpoints --
+//     no barrier, no written state, 2 B per incidence streamed;
+//   explicit format (fallback when a tile has > 64 distinct records):
+//     spring-once passes -- owner pass (c written over the record's k),
+//     foreign pass over the copies of cross-tile springs, barrier, reference
+//     pass adding c * (y_owner - y_me);
 //
-// The masses of a tile are ordered by their (foreign, own, in-tile) counts,
-// so the lanes of a warp walk lists of (nearly) equal length.
+// then the fused epilogue: external forces, Verlet / Euler, restore fixed,
+// finiteness (integrate_store).
 //
 // Positions are staged as tile-local y = (P - A) + r (kernels.cuh
 // stage_tile): both endpoints of a spring see the same c and exactly
 // opposite d, so Newton's third law holds bitwise; the summation order is
-// fixed by the layout, so results are deterministic and identical between
-// the two kernels.
-//
-//   tile_lean_kernel  one tile per CTA (256 threads, 3 CTAs per SM).
-//   tile_ws_kernel    persistent, one CTA per SM, warp-specialized: producer
-//                     warps stream tiles into a 3-stage shared-memory ring
-//                     (TMA bulk copy of the records + cp.async gathers of the
-//                     own and halo states), two consumer groups of 8 warps
-//                     compute alternate tiles, so the record stream overlaps
-//                     the arithmetic.
+// fixed by the layout, so results are deterministic.
 //
 // Record format of fp32 tile builds (tiles_f32.cpp): k and k*l0 in fp32
 // (planar), so c = k (L - l0)/L = fma(-(k l0), 1/L, k): one FFMA after the
@@ -160,6 +147,8 @@ __device__ __forceinline__ void acc3(V3<float> &s, float c, float dx, float dy, 
     s.z = __fmaf_rn(c, dz, s.z);
 }
 
+// ------------------------------------------------- explicit format passes
+
 // Owner pass of tile mass l: its own records (slot q*256 + l).
 // Accumulates c*d, writes c over k (the in-tile partners read it in
 // ref_pass), and returns the number of degenerate own springs (counted once
@@ -278,6 +267,59 @@ __device__ __forceinline__ void ref_pass(const TileView &v, int l, const float4 
     for (; q < n_ref; ++q) ibody(q);
 }
 
+// -------------------------------------------------- compact format pass
+
+// Spring sum of tile mass l over its incidence list (tiles.h compact
+// format: u16 = partner slot | dictionary index << 10, own springs first).
+// Each spring is evaluated from both of its endpoints; the two evaluations
+// see exactly opposite d and the same c, so Newton's third law holds
+// bitwise.  Returns the number of degenerate own springs.
+template <bool GROUPS>
+__device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const TileView &v, int l, const float4 &y,
+                                                  int n_own, int n_inc, V3<float> &s) {
+    const uint16_t *inc = reinterpret_cast<const uint16_t *>(v.bl + v.h->off_oo) + l;
+    const float2 *dict = reinterpret_cast<const float2 *>(v.bl + v.h->off_okl);
+    const int8_t *dg = GROUPS && v.h->off_og ? reinterpret_cast<const int8_t *>(v.bl + v.h->off_og) : nullptr;
+    float dmin = INFINITY;
+    auto body = [&](int q) {
+        const uint32_t e = inc[q << 8];
+        const uint32_t mi = e >> 10;
+        float2 kl = dict[mi];
+        if constexpr (GROUPS) {
+            if (dg) {
+                const int g = dg[mi];
+                if (g >= 0) kl.y = kl.y * p.scale[g];
+            }
+        }
+        const float4 yo = v.sY[e & 0x3ffu];
+        const float dx = yo.x - y.x, dy = yo.y - y.y, dz = yo.z - y.z;
+        float d2;
+        const float c = spring_c(dx, dy, dz, kl.x, kl.y, d2);
+        if (q < n_own) dmin = fminf(dmin, d2);
+        acc3(s, c, dx, dy, dz);
+    };
+    int q = 0;
+#pragma unroll 1
+    for (; q + 3 < n_inc; q += 4) {
+        body(q);
+        body(q + 1);
+        body(q + 2);
+        body(q + 3);
+    }
+#pragma unroll 1
+    for (; q < n_inc; ++q) body(q);
+    unsigned deg = 0;
+    if (dmin < 1e-24f) {                                    // rare: count the degenerate own springs
+        for (int r = 0; r < n_own; ++r) {
+            const float4 yo = v.sY[inc[r << 8] & 0x3ffu];
+            const float dx = yo.x - y.x, dy = yo.y - y.y, dz = yo.z - y.z;
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+            deg += d2 < 1e-24f ? 1u : 0u;
+        }
+    }
+    return deg;
+}
+
 // Epilogue of tile mass l (device id m): the history vector the integrator
 // needs (x_prev for Verlet, v otherwise) was prefetched; v is read only to
 // bootstrap, for friction, or to restore a fixed mass; P only for contact.
@@ -298,8 +340,8 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
     __syncthreads();
 }
 
-template <int INTEG, bool GROUPS>
-__global__ void __launch_bounds__(kTile, 3) tile_lean_kernel(Params<float> p) {
+template <int INTEG, bool GROUPS, int FMT>
+__global__ void __launch_bounds__(kTile, FMT == 1 ? 5 : 3) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (*p.div_step < p.step) return;                       // grid-uniform
     const Topology<float> &t = p.topo;
@@ -341,196 +383,34 @@ __global__ void __launch_bounds__(kTile, 3) tile_lean_kernel(Params<float> p) {
 #pragma unroll 1
         for (int i = l; i < nh; i += kTile) {
             const int gm = halo[i];
+            if (gm < 0) continue;                           // hole of the bank-aware halo layout
             const float4 r = ldg4(p.X + gm), pp = ldg4(p.P + gm);
             sY[kTile + i] = make_float4((pp.x - A.x) + r.x, (pp.y - A.y) + r.y, (pp.z - A.z) + r.z, 0.f);
         }
     }
     mbar_wait_warp0(bar + 1, 0);                            // records (+ the staged states)
     V3<float> s = {0.f, 0.f, 0.f};
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    int n_ref = 0;
-    if (active && p.debug != 1) {
-        y = sY[l];
-        const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
-        n_ref = cnt >> 8;
-        flush_degenerate(p.degenerate, owner_pass<GROUPS>(p, v, l, y, cnt & 0xff, s));
-    }
-    if (p.debug != 1) foreign_pass<GROUPS>(p, v, l, kTile);
-    __syncthreads();                                        // every c written
-    if (!active) return;
-    if (p.debug != 1) ref_pass(v, l, y, n_ref, s);
-    tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
-}
-
-// ------------------------------------------------------------- persistent
-
-constexpr int kWsProducers = 128;
-constexpr int kWsStages = 3;
-constexpr int kWsThreads = kWsProducers + 2 * kTile;
-
-// Stage s of the ring: [blob (blob_smem) | X raw (256 + max_halo) | P raw
-// (256 + max_halo)].  The producers' cp.async gathers land raw X and P; the
-// consumers convert them in place into y (over the P slots) before use.
-struct WsGeom {
-    uint32_t stage_bytes, blob_smem, slots;
-    __device__ __forceinline__ unsigned char *blob(unsigned char *smem, int s) const {
-        return smem + 128 + (size_t)s * stage_bytes;
-    }
-    __device__ __forceinline__ float4 *xraw(unsigned char *smem, int s) const {
-        return reinterpret_cast<float4 *>(blob(smem, s) + blob_smem);
-    }
-    __device__ __forceinline__ float4 *praw(unsigned char *smem, int s) const {
-        return xraw(smem, s) + slots;
-    }
-};
-
-__host__ __device__ inline size_t ws_stage_bytes(size_t blob_smem, size_t max_halo) {
-    return (blob_smem + 2 * (kTile + max_halo) * sizeof(float4) + 127u) & ~(size_t)127u;
-}
-
-// Barriers:
-//   mbarrier [3s]   header + halo ids of stage s (TMA)
-//   mbarrier [3s+1] records of stage s (TMA)
-//   mbarrier [3s+2] cp.async gathers of stage s: one arrival per producer thread
-//   named FULL[s] = 1+s is not needed: consumers wait on the mbarriers directly
-//   named EMPTY[s] = 4+s: 256 consumer arrivals + 128 producer syncs
-//   named GROUP[g] = 7+g: the 256 threads of a consumer group
-//   named PROD = 9: the 128 producer threads
-template <int INTEG, bool GROUPS>
-__global__ void __launch_bounds__(kWsThreads, 1) tile_ws_kernel(Params<float> p) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    if (*p.div_step < p.step) return;                       // grid-uniform
-    const Topology<float> &t = p.topo;
-    const int tid = threadIdx.x;
-    const int G = (int)gridDim.x;
-    const int b = (int)blockIdx.x;
-    const int n_mine = (t.n_tiles - b + G - 1) / G;
-    const WsGeom geo{(uint32_t)ws_stage_bytes(t.blob_smem, t.max_halo), t.blob_smem, kTile + t.max_halo};
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-    if (tid == 0) {
-        for (int i = 0; i < kWsStages; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 3 * i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 3 * i + 1)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar + 3 * i + 2)),
-                         "r"(kWsProducers));
+    if constexpr (FMT == 1) {                               // compact: one pass, no further barrier
+        if (!active) return;
+        if (p.debug != 1) {
+            const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
+            flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, sY[l], cnt & 0xff, cnt >> 8, s));
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (tid < kWsProducers) {
-        // ------------------------------------------------------------ producers
-        // Tile k: TMA its blob, cp.async its own states, then (header landed)
-        // cp.async its halo states.  Nothing here waits for data except the
-        // 1.3 KB header; the consumers wait on the three mbarriers.
-        long long t0 = prof_clock();
-        const bool pw = tid == 0;
-        for (int k = 0; k < n_mine; ++k) {
-            const int s = k % kWsStages;
-            const uint32_t phase = (uint32_t)(k / kWsStages) & 1u;
-            const int T = b + k * G;
-            if (k >= kWsStages) named_sync(4 + s, kWsProducers + kTile);   // stage released
-            prof_add(p, pw, 0, t0);                         // [0] producer: waiting for a free stage
-            unsigned char *bl = geo.blob(smem, s);
-            if (tid == 0) {
-                const int tb = p.debug == 2 ? 0 : T;
-                const unsigned long long g0 = t.toff[tb];
-                const uint32_t bytes = (uint32_t)(t.toff[tb + 1] - g0);
-                const uint32_t split = t.tsplit[tb] & 0xffffffu;
-                bulk_copy(bl, t.blob + g0, split, bar + 3 * s);
-                bulk_copy(bl + split, t.blob + g0 + split, bytes - split, bar + 3 * s + 1);
-            }
-            float4 *xr = geo.xraw(smem, s), *pr = geo.praw(smem, s);
-            const int n = (int)(__ldg(t.tsplit + T) >> 24) + 1;
-            for (int i = tid; i < n; i += kWsProducers) {   // own states: no dependency
-                cp_async16(xr + i, p.X + T * kTile + i);
-                cp_async16(pr + i, p.P + T * kTile + i);
-            }
-            prof_add(p, pw, 1, t0);                         // [1] producer: TMA + own gathers issued
-            if (tid < 32) mbar_wait(bar + 3 * s, phase);   // header + halo ids
-            named_sync(9, kWsProducers);
-            prof_add(p, pw, 2, t0);                         // [2] producer: waiting for the header
-            const TileHdr *h = reinterpret_cast<const TileHdr *>(bl);
-            const int *halo = reinterpret_cast<const int *>(bl + h->off_halo);
-            const int nh = (int)h->n_halo;
-            for (int i = tid; i < nh; i += kWsProducers) {
-                const int gm = halo[i];
-                cp_async16(xr + kTile + i, p.X + gm);
-                cp_async16(pr + kTile + i, p.P + gm);
-            }
-            cp_async_mbar_arrive(bar + 3 * s + 2);          // fires when this thread's copies land
-            prof_add(p, pw, 3, t0);                         // [3] producer: halo gathers issued
-        }
-        // drain the releases of the last stages so no named barrier is left
-        // with pending arrivals when the CTA exits
-        for (int k = n_mine > kWsStages ? n_mine - kWsStages : 0; k < n_mine; ++k)
-            named_sync(4 + k % kWsStages, kWsProducers + kTile);
-        return;
-    }
-
-    // ---------------------------------------------------------------- consumers
-    const int c = tid - kWsProducers;
-    const int g = c >> 8;                                   // consumer group
-    const int l = c & (kTile - 1);
-    const bool need_prev = INTEG == 1 && !p.bootstrap;
-    unsigned deg = 0;
-    long long t0 = prof_clock();
-    const bool cw = l == 0;
-    for (int k = g; k < n_mine; k += 2) {
-        const int s = k % kWsStages;
-        const uint32_t phase = (uint32_t)(k / kWsStages) & 1u;
-        const int T = b + k * G;
-        const int m = T * kTile + l;
-        const int n = (int)(__ldg(t.tsplit + T) >> 24) + 1;
-        const bool active = l < n;
-        float4 hist = make_float4(0.f, 0.f, 0.f, 0.f);     // epilogue history, prefetched
-        if (active) hist = need_prev ? ldg4(p.Xprev + m) : ldg4(p.V + m);
-        unsigned char *bl = geo.blob(smem, s);
-        float4 *xr = geo.xraw(smem, s), *pr = geo.praw(smem, s);
-        mbar_wait(bar + 3 * s + 2, phase);                  // own + halo states landed
-        mbar_wait(bar + 3 * s, phase);                      // header (halo count)
-        prof_add(p, cw, 4, t0);                             // [4] consumer: waiting for the states
-        const TileView v0 = tile_view(bl, pr);
-        {                                                   // y = (P - A) + r, in place over P
-            const float4 A = pr[(n - 1) / 2];
-            const int ns = kTile + (int)v0.h->n_halo;
-            named_sync(7 + g, kTile);                       // A read before anyone overwrites it
-            for (int i = l; i < ns; i += kTile) {
-                if (i >= n && i < kTile) continue;
-                const float4 r = xr[i], pp = pr[i];
-                pr[i] = make_float4((pp.x - A.x) + r.x, (pp.y - A.y) + r.y, (pp.z - A.z) + r.z, r.w);
-            }
-        }
-        const float4 x4 = active ? xr[l] : make_float4(0.f, 0.f, 0.f, 0.f);
-        prof_add(p, cw, 5, t0);                             // [5] consumer: y conversion
-        mbar_wait(bar + 3 * s + 1, phase);                  // records
-        named_sync(7 + g, kTile);                           // every y converted
-        prof_add(p, cw, 6, t0);                             // [6] consumer: waiting for records + group
-        const TileView v = v0;
-        V3<float> sum = {0.f, 0.f, 0.f};
+    } else {                                                // explicit: spring-once passes
         float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
         int n_ref = 0;
         if (active && p.debug != 1) {
-            y = v.sY[l];
+            y = sY[l];
             const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
             n_ref = cnt >> 8;
-            deg += owner_pass<GROUPS>(p, v, l, y, cnt & 0xff, sum);
+            flush_degenerate(p.degenerate, owner_pass<GROUPS>(p, v, l, y, cnt & 0xff, s));
         }
-        prof_add(p, cw, 7, t0);                             // [7] consumer: owner pass
         if (p.debug != 1) foreign_pass<GROUPS>(p, v, l, kTile);
-        prof_add(p, cw, 8, t0);                             // [8] consumer: foreign pass
-        named_sync(7 + g, kTile);                           // every c of the tile written
-        prof_add(p, cw, 9, t0);                             // [9] consumer: group barrier
-        if (active && p.debug != 1) ref_pass(v, l, y, n_ref, sum);
-        prof_add(p, cw, 10, t0);                            // [10] consumer: reference pass
-        // generic-proxy writes (c over k, y over P) must be ordered before the
-        // next async-proxy (TMA / cp.async) writes into this stage
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_arrive(4 + s, kWsProducers + kTile);          // stage free for tile k + 3
-        if (active) tile_epilogue<INTEG>(p, m, sum, x4, hist, need_prev);
-        prof_add(p, cw, 11, t0);                            // [11] consumer: epilogue
+        __syncthreads();                                    // every c written
+        if (!active) return;
+        if (p.debug != 1) ref_pass(v, l, y, n_ref, s);
     }
-    flush_degenerate(p.degenerate, deg);
+    tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
 }
 
 }  // namespace ss

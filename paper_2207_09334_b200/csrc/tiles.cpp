@@ -40,7 +40,7 @@ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
 // tile's first n slots, the rest are padding (-1).  With order == 1 the
 // masses are sorted into 4x8x8 bricks of quantised coordinates and whole
 // bricks are packed into tiles, so tiles never straddle brick boundaries.
-void tile_order(const TileInput &in, std::vector<int32_t> &orig_of) {
+void tile_order(const TileInput &in, std::vector<int32_t> &orig_of, std::vector<int32_t> *zcell) {
     const int64_t N = in.N;
     std::vector<int32_t> sorted(N);
     std::iota(sorted.begin(), sorted.end(), 0);
@@ -60,12 +60,14 @@ void tile_order(const TileInput &in, std::vector<int32_t> &orig_of) {
             for (int64_t i = 0; i < N; ++i)
                 for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], in.x[3 * i + c]);
             std::vector<int64_t> cell((size_t)N * 3);
+            if (zcell) zcell->assign(N, 0);
             int64_t mx[3] = {0, 0, 0};
             for (int64_t i = 0; i < N; ++i)
                 for (int c = 0; c < 3; ++c) {
                     const double q = std::floor((in.x[3 * i + c] - lo[c]) / h + 0.5);
                     const int64_t v = q < 0 ? 0 : (int64_t)q;
                     cell[3 * i + c] = v;
+                    if (zcell && c == 2) (*zcell)[i] = (int32_t)(v & 0x7fffffff);
                     mx[c] = std::max(mx[c], v);
                 }
             const int64_t B[3] = {4, 8, 8};
@@ -333,6 +335,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     double hsum = 0, fsum = 0, rsum = 0;
     for (int64_t t = 0; t < n_tiles; ++t) {
         L.max_tile_bytes = std::max<uint32_t>(L.max_tile_bytes, (uint32_t)parts[t].size());
+        L.max_tile_smem = std::max<uint32_t>(L.max_tile_smem, (uint32_t)parts[t].size());
         const uint32_t head = tSplit[t] & 0xffffffu;
         L.max_head_bytes = std::max<uint32_t>(L.max_head_bytes, head);
         L.max_rest_bytes = std::max<uint32_t>(L.max_rest_bytes, (uint32_t)parts[t].size() - head);

@@ -7,6 +7,7 @@
 namespace ss {
 
 constexpr int kTile = 256;            // masses per tile == threads per CTA
+constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compact format
 
 // Per-tile blob header (all offsets in bytes from the tile start, 16-B aligned).
 // [0, off_cnt) (header + halo ids) is copied first so the halo gather
@@ -21,15 +22,23 @@ constexpr int kTile = 256;            // masses per tile == threads per CTA
 //              bit 15 clear-> in-tile record: owner local id (bits 0-7), slot q (bits 8-14)
 //
 // fp32 builds (production, tiles_f32.cpp build_tiles_f32): one 256-wide ELL
-// slice, slot = q*256 + l, records (other local u16, k f32, k*l0 f32
-// [, grp i8]) as planar arrays (the okl section is k[W*256] then
-// k*l0[W*256]; fkl likewise over the n_foreign copies); padding slots
-// point at their own mass with k = 0.  A
-// spring whose owner lies in another tile is copied into the partner's
-// tile (foreign owner, foreign local partner off_fl, (k, k*l0), grp).  A
-// mass's reference list holds its foreign references first (0x8000 | copy;
-// their count per mass in off_nf) and then its in-tile ones, whose value
-// is the owner's slot.  counts: n_own | n_ref << 8.
+// slice, slot = q*256 + l, in one of two record formats:
+//  * compact (canonical bit 1 set, the default when every tile has <= 64
+//    distinct (k, k*l0, group) records and <= 768 halo slots): every mass
+//    has ONE incidence list -- its own springs first, then the springs it
+//    references -- of u16 = partner slot (10 bits) | dictionary index << 10;
+//    counts = n_own | n_inc << 8 (off_cnt), incidences at off_oo (W = max
+//    n_inc), dictionary float2 (k, k*l0) at off_okl, int8 groups at off_og.
+//    2 B per incidence, 4 B per spring, no foreign copies.
+//  * explicit (canonical bit 1 clear): counts = n_own | n_ref << 8; own
+//    records (other u16 off_oo, then planar k[W*256] and k*l0[W*256] at
+//    off_okl, grp i8 off_og); a spring whose owner lies in another tile is
+//    copied into the partner's tile (owner u16 off_fo, partner u8 off_fl,
+//    planar k, k*l0 off_fkl, grp off_fg); a mass's reference list holds its
+//    foreign references first (0x8000 | copy; their count per mass in
+//    off_nf) and then its in-tile ones, whose value is the owner's slot.
+// Padding slots point at their own mass.  Halo slots are bank-aware
+// (tiles_f32.cpp): slot == z (mod 8), holes carry id -1.
 struct TileHdr {
     uint32_t n, W, Wr, n_halo;
     uint32_t n_foreign, bytes, off_cnt, off_oo;
@@ -38,7 +47,7 @@ struct TileHdr {
     uint32_t off_nf;       // fp32 builds: u8 per mass, leading foreign references
     uint32_t slice_log2;   // sliced-ELL slice of 2^slice_log2 masses (fp64 builds 5, fp32 builds 8)
     uint32_t off_fl;       // fp32 builds: u8 per foreign copy, its local partner
-    uint32_t pad3;
+    uint32_t n_dict;       // fp32 compact format: entries of the tile's (k, k*l0) dictionary
 };
 static_assert(sizeof(TileHdr) == 80, "TileHdr must stay 80 bytes");
 
@@ -71,19 +80,22 @@ struct TileLayout {
     std::vector<uint32_t> split;    // per tile: bytes of the first copy (header + halo ids)
     int64_t n_tiles = 0;
     uint32_t max_tile_bytes = 0;
+    uint32_t max_tile_smem = 0;     // shared memory a tile blob needs
     uint32_t max_head_bytes = 0;    // [0, split): header + halo ids
     uint32_t max_rest_bytes = 0;    // [split, bytes): counts + records + refs
     uint32_t max_halo = 0;
     int max_W = 0, max_Wr = 0;
     bool canonical = true;
     bool has_self = false;          // a spring joins a mass to itself
+    bool compact = false;           // fp32 compact format (tiles_f32.cpp)
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };
 
 int build_tiles(const TileInput &in, TileLayout &out);      // fp64; dispatches fp32 builds to:
 int build_tiles_f32(const TileInput &in, TileLayout &out);
-// Device slot order (brick renumbering, tiles padded to kTile slots).
-void tile_order(const TileInput &in, std::vector<int32_t> &orig_of);
+// Device slot order (brick renumbering, tiles padded to kTile slots);
+// optionally the quantised z cell of every mass (empty: no positions).
+void tile_order(const TileInput &in, std::vector<int32_t> &orig_of, std::vector<int32_t> *zcell = nullptr);
 
 }  // namespace ss

@@ -19,7 +19,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
+#include <tuple>
 
 #include "common.h"
 #include "springsim_b200.h"
@@ -38,11 +40,35 @@ void put_at(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 
 }  // namespace
 
+int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict);
+
+namespace {
+size_t own_total(const std::vector<std::vector<int32_t>> &own) {
+    size_t n = 0;
+    for (const auto &o : own) n += o.size();
+    return n;
+}
+}  // namespace
+
+// Compact format when every tile has at most 64 distinct (k, k*l0, group)
+// records and at most 768 halo slots, the explicit format otherwise
+// (SS_TILE_DICT=0 forces it).
 int build_tiles_f32(const TileInput &in, TileLayout &L) {
+    const char *env = getenv("SS_TILE_DICT");
+    if (!env || atoi(env) != 0) {
+        const int rc = build_tiles_f32_fmt(in, L, true);
+        if (rc != SS_EAGAIN_DICT) return rc;
+    }
+    return build_tiles_f32_fmt(in, L, false);
+}
+
+int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
-    tile_order(in, L.orig_of);
+    std::vector<int32_t> zcell;
+    tile_order(in, L.orig_of, &zcell);
+    const bool bank_aware = !zcell.empty();
     const int64_t D = (int64_t)L.orig_of.size();
     const int64_t n_tiles = D / kTile;
     // per caller mass: own springs and springs referencing it, ascending id
@@ -110,7 +136,7 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
     // 2) per-tile blobs
     L.n_tiles = n_tiles;
     std::vector<std::vector<uint8_t>> parts(n_tiles);
-    std::vector<uint32_t> tH(n_tiles), tSplit(n_tiles), tN(n_tiles), tW(n_tiles), tWr(n_tiles);
+    std::vector<uint32_t> tH(n_tiles), tHr(n_tiles), tSplit(n_tiles), tN(n_tiles), tW(n_tiles), tWr(n_tiles);
     std::vector<int64_t> tFor(n_tiles), tRefs(n_tiles);
     const bool has_g = in.group != nullptr;
     int err = 0;
@@ -153,12 +179,37 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
         }
         std::sort(halo.begin(), halo.end());
         halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+        // Bank-aware halo slots: slot = 256 + 8j + (z mod 8), so every staged
+        // mass (own ones sit at l == z mod 8 in a brick) has slot == z (mod 8)
+        // and the 8 lanes of a 128-bit shared-memory phase (8 consecutive z
+        // of one brick row) gather 8 distinct bank groups, in-tile or halo.
+        std::vector<uint16_t> halo_slot(halo.size());
+        std::vector<int32_t> halo_ids;            // per slot, -1 = hole
+        if (bank_aware) {
+            uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            std::vector<uint32_t> cls(halo.size());
+            for (size_t i = 0; i < halo.size(); ++i) {
+                const uint32_t r = (uint32_t)zcell[L.orig_of[halo[i]]] & 7u;
+                cls[i] = cnt[r]++;
+            }
+            uint32_t maxc = 0;
+            for (int r = 0; r < 8; ++r) maxc = std::max(maxc, cnt[r]);
+            halo_ids.assign((size_t)8 * maxc, -1);
+            for (size_t i = 0; i < halo.size(); ++i) {
+                const uint32_t slot = 8 * cls[i] + ((uint32_t)zcell[L.orig_of[halo[i]]] & 7u);
+                halo_ids[slot] = halo[i];
+                halo_slot[i] = (uint16_t)(kTile + slot);
+            }
+        } else {
+            halo_ids = halo;
+            for (size_t i = 0; i < halo.size(); ++i) halo_slot[i] = (uint16_t)(kTile + i);
+        }
         int W = 1, Wr = 1;
         for (int l = 0; l < n; ++l) {
             W = std::max(W, (int)own[l].size());
             Wr = std::max(Wr, (int)refs[l].size());
         }
-        if (W > 255 || Wr > 255 || halo.size() + kTile > 65535 || foreign.size() >= 0x8000) {
+        if (W > 255 || Wr > 255 || halo_ids.size() + kTile > 65535 || foreign.size() >= 0x8000) {
 #pragma omp atomic write
             err = 1;
             continue;
@@ -167,15 +218,82 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
             const int64_t ol = dev - base;
             if (ol >= 0 && ol < n) return (uint16_t)ol;
             const auto it = std::lower_bound(halo.begin(), halo.end(), (int32_t)dev);
-            return (uint16_t)(kTile + (it - halo.begin()));
+            return halo_slot[it - halo.begin()];
         };
         const uint32_t own_n = (uint32_t)W << 8, ref_n = (uint32_t)Wr << 8, nf = (uint32_t)foreign.size();
+        if (use_dict) {
+            // compact format: per mass one incidence list (own springs, then
+            // the springs it references), u16 = partner slot | dict index << 10
+            std::map<std::tuple<float, float, int>, uint32_t> dict;
+            auto key_of = [&](int32_t s) {
+                return std::make_tuple((float)in.k[s], (float)(in.k[s] * in.l0[s]), has_g ? (int)in.group[s] : -1);
+            };
+            std::vector<std::vector<int32_t>> inc(n);
+            int Wi = 1;
+            for (int l = 0; l < n; ++l) {
+                const int64_t m = L.orig_of[base + l];
+                for (const int32_t s : own[l]) inc[l].push_back(s);
+                for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r) inc[l].push_back(ref_sp[r]);
+                for (const int32_t s : inc[l]) dict.emplace(key_of(s), 0u);
+                Wi = std::max(Wi, (int)inc[l].size());
+            }
+            if (dict.size() > 64 || kTile + halo_ids.size() > 1024 || Wi > 255) {
+#pragma omp atomic write
+                err = 3;
+                continue;
+            }
+            uint32_t di = 0;
+            for (auto &kv : dict) kv.second = di++;
+            const uint32_t D = (uint32_t)dict.size(), inc_n = (uint32_t)Wi << 8;
+            TileHdr h{};
+            h.n = n; h.W = Wi; h.Wr = 0; h.n_halo = (uint32_t)halo_ids.size(); h.n_foreign = 0;
+            h.canonical = 1 | 2;                               // bit 1: compact format
+            h.slice_log2 = 8;
+            h.n_dict = D;
+            uint32_t off = al16(sizeof(TileHdr));
+            h.off_halo = off; off = al16(off + (uint32_t)halo_ids.size() * 4);
+            h.off_cnt = off;  off = al16(off + kTile * 2);       // n_own | n_inc << 8
+            h.off_oo = off;   off = al16(off + inc_n * 2);       // incidences
+            h.off_okl = off;  off = al16(off + D * 8);           // dictionary (k, k*l0)
+            h.off_og = 0;
+            if (has_g) { h.off_og = off; off = al16(off + D); } // dictionary groups
+            h.off_nf = h.off_ref = h.off_fo = h.off_fkl = h.off_fl = h.off_fg = 0;
+            h.bytes = off;
+            std::vector<uint8_t> &blob = parts[t];
+            blob.assign(off, 0);
+            std::memcpy(blob.data(), &h, sizeof h);
+            std::memcpy(blob.data() + h.off_halo, halo_ids.data(), halo_ids.size() * 4);
+            for (const auto &kv : dict) {
+                put_at<float>(blob, h.off_okl + 8 * kv.second, std::get<0>(kv.first));
+                put_at<float>(blob, h.off_okl + 8 * kv.second + 4, std::get<1>(kv.first));
+                if (has_g) put_at<int8_t>(blob, h.off_og + kv.second, (int8_t)std::get<2>(kv.first));
+            }
+            int64_t n_inc = 0;
+            for (int l = 0; l < n; ++l) {
+                const int64_t m = L.orig_of[base + l];
+                put_at<uint16_t>(blob, h.off_cnt + 2 * l, (uint16_t)(own[l].size() | (inc[l].size() << 8)));
+                for (size_t q = 0; q < inc[l].size(); ++q) {
+                    const int32_t s = inc[l][q];
+                    const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;   // the other endpoint
+                    const uint32_t v = (uint32_t)slot_of_local(L.new_of[o]) | (dict.at(key_of(s)) << 10);
+                    put_at<uint16_t>(blob, h.off_oo + 2 * (((uint32_t)q << 8) | (uint32_t)l), (uint16_t)v);
+                }
+                n_inc += (int64_t)inc[l].size();
+            }
+            tH[t] = (uint32_t)halo_ids.size();
+            tHr[t] = (uint32_t)halo.size();
+            tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);
+            tN[t] = n; tW[t] = Wi; tWr[t] = 0;
+            tFor[t] = nf;
+            tRefs[t] = n_inc - (int64_t)own_total(own);
+            continue;
+        }
         TileHdr h{};
-        h.n = n; h.W = W; h.Wr = Wr; h.n_halo = (uint32_t)halo.size(); h.n_foreign = nf;
+        h.n = n; h.W = W; h.Wr = Wr; h.n_halo = (uint32_t)halo_ids.size(); h.n_foreign = nf;
         h.canonical = 1;
         h.slice_log2 = 8;
         uint32_t off = al16(sizeof(TileHdr));
-        h.off_halo = off; off = al16(off + (uint32_t)halo.size() * 4);
+        h.off_halo = off; off = al16(off + (uint32_t)halo_ids.size() * 4);
         h.off_cnt = off;  off = al16(off + kTile * 2);
         h.off_nf = off;   off = al16(off + kTile);
         h.off_oo = off;   off = al16(off + own_n * 2);
@@ -192,7 +310,7 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
         std::vector<uint8_t> &blob = parts[t];
         blob.assign(off, 0);
         std::memcpy(blob.data(), &h, sizeof h);
-        std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
+        std::memcpy(blob.data() + h.off_halo, halo_ids.data(), halo_ids.size() * 4);
         for (uint32_t l = 0; l < (uint32_t)kTile; ++l)          // padding: self, k = 0
             for (int q = 0; q < W; ++q) put_at<uint16_t>(blob, h.off_oo + 2 * (((uint32_t)q << 8) | l), (uint16_t)l);
         if (has_g) std::memset(blob.data() + h.off_og, 0xff, own_n);
@@ -224,13 +342,16 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
             if (has_g) put_at<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
         }
         const int64_t n_for_t = nf;
-        tH[t] = (uint32_t)halo.size();
+        tH[t] = (uint32_t)halo_ids.size();
+            tHr[t] = (uint32_t)halo.size();
         tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);
         tN[t] = n; tW[t] = W; tWr[t] = Wr;
         tFor[t] = n_for_t;
         tRefs[t] = n_refs;
     }
     if (err == 1) return fail(SS_EINVAL, "tile exceeds layout limits (degree or halo too large)");
+    if (err == 3) return SS_EAGAIN_DICT;
+    L.compact = use_dict;
     if (in.group) {
         for (int64_t s = 0; s < S; ++s)
             if (in.group[s] > 127) return fail(SS_EINVAL, "at most 128 actuation groups in the tiled layout");
@@ -245,13 +366,18 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
     double hsum = 0, fsum = 0, rsum = 0;
     for (int64_t t = 0; t < n_tiles; ++t) {
         L.max_tile_bytes = std::max<uint32_t>(L.max_tile_bytes, (uint32_t)parts[t].size());
+        {
+            TileHdr th;
+            std::memcpy(&th, parts[t].data(), sizeof th);
+            L.max_tile_smem = std::max<uint32_t>(L.max_tile_smem, (uint32_t)parts[t].size());
+        }
         const uint32_t head = tSplit[t] & 0xffffffu;
         L.max_head_bytes = std::max<uint32_t>(L.max_head_bytes, head);
         L.max_rest_bytes = std::max<uint32_t>(L.max_rest_bytes, (uint32_t)parts[t].size() - head);
         L.max_halo = std::max(L.max_halo, tH[t]);
         L.max_W = std::max<int>(L.max_W, (int)tW[t]);
         L.max_Wr = std::max<int>(L.max_Wr, (int)tWr[t]);
-        hsum += (double)(tN[t] + tH[t]) / tN[t];
+        hsum += (double)(tN[t] + tHr[t]) / tN[t];
         fsum += (double)tFor[t];
         rsum += (double)tRefs[t];
     }
