@@ -273,7 +273,12 @@ def run_single(args):
                      "traffic": profiled_traffic(workload, args.precision, layout_name),
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo,
-                     "avg_launch_us": per_launch_s * 1e6},
+                     "avg_launch_us": per_launch_s * 1e6,
+                     "note": ("compact tile records: %d record bytes/substep (%.1f B/spring) stream instead of "
+                              "the 16 B/spring of the SURVEY 8d model, so measured DRAM traffic is below the "
+                              "algorithmic bytes; see DESIGN.md 4" % (info["tile_blob_bytes"],
+                                                                      info["tile_blob_bytes"] / S))
+                             if info.get("tile_kernel") == 2 else None},
         "cpu_baseline": cpu,
         "e2e": {"value": S * sub * e2e_steps / e2e_wall, "unit": "spring-updates/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

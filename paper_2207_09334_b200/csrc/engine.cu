@@ -104,6 +104,7 @@ struct ss_engine {
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet tile kernel (tile_f32.cuh), 0 = off
+    int lean_minb = 0;             // SS_LEAN_MINB: register budget experiments (resident CTAs per SM)
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -398,6 +399,8 @@ void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     const bool euler = h->integrator == SS_EULER, compact = h->tl.compact;
     auto *k = euler ? (compact ? tile_lean_kernel<0, GROUPS, 1> : tile_lean_kernel<0, GROUPS, 0>)
                     : (compact ? tile_lean_kernel<1, GROUPS, 1> : tile_lean_kernel<1, GROUPS, 0>);
+    if (compact && !euler && h->lean_minb == 6) k = tile_lean_kernel<1, GROUPS, 1, 6>;   // SS_LEAN_MINB experiments
+    if (compact && !euler && h->lean_minb == 8) k = tile_lean_kernel<1, GROUPS, 1, 8>;
     k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
 }
 
@@ -649,7 +652,11 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             const std::string kname = kenv ? kenv : "lean";
             if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
+                if (const char *mb = getenv("SS_LEAN_MINB")) h->lean_minb = atoi(mb);
                 const int b = dev_max;
+                for (auto *kk : {tile_lean_kernel<1, false, 1, 6>, tile_lean_kernel<1, false, 1, 8>,
+                                 tile_lean_kernel<1, true, 1, 6>, tile_lean_kernel<1, true, 1, 8>})
+                    CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
                 for (auto *kk : {tile_lean_kernel<0, false, 0>, tile_lean_kernel<1, false, 0>,
                                  tile_lean_kernel<0, true, 0>, tile_lean_kernel<1, true, 0>,
                                  tile_lean_kernel<0, false, 1>, tile_lean_kernel<1, false, 1>,

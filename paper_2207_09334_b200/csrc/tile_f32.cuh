@@ -295,7 +295,7 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
         const float dx = yo.x - y.x, dy = yo.y - y.y, dz = yo.z - y.z;
         float d2;
         const float c = spring_c(dx, dy, dz, kl.x, kl.y, d2);
-        if (q < n_own) dmin = fminf(dmin, d2);
+        dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
         acc3(s, c, dx, dy, dz);
     };
     int q = 0;
@@ -340,8 +340,8 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
     __syncthreads();
 }
 
-template <int INTEG, bool GROUPS, int FMT>
-__global__ void __launch_bounds__(kTile, FMT == 1 ? 5 : 3) tile_lean_kernel(Params<float> p) {
+template <int INTEG, bool GROUPS, int FMT, int MINB = (FMT == 1 ? 5 : 3)>
+__global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (*p.div_step < p.step) return;                       // grid-uniform
     const Topology<float> &t = p.topo;

@@ -1,5 +1,7 @@
 #!/bin/bash
-# Full measurement round: GPU tests, smoke, bench line, ncu launch list + full capture.
+# Full measurement round (1 GPU): GPU tests, smoke, bench line, reference arm,
+# ncu launch list + one full capture of the dominant kernel.
+#   KREGEX (default tile_lean) selects the kernel for the full capture.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
 nproc > gpurun_out/host.txt; grep -m1 "model name" /proc/cpuinfo >> gpurun_out/host.txt
@@ -9,7 +11,7 @@ timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "ben
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 30 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-tile_lean} -s 30 -c 1 \
    -o gpurun_out/prof python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log
 cat gpurun_out/bench.log gpurun_out/bench_ref.log
