@@ -183,6 +183,24 @@ int ss_get_info(ss_engine *h, ss_info *info);
  * needed) and report its statistics in `info`. */
 int ss_plan(const ss_scene_desc *desc, ss_info *info);
 
+/* On-device sampling for simulate()/RunResult (engine.py:476-565) and the
+ * energy breakdown (engine.py:148-170, Engine.energies engine.py:390-398).
+ * ss_energy_setup hands the engine the caller-order spring list (k, l0,
+ * actuation group, -1 passive) and the GPE datum once.  ss_step_sampled runs
+ * `count` steps; after every step whose index d (Verlet: n-1, sampled at
+ * x_prev with the lagged central-difference v, exactly like the reference's
+ * simulate; Euler/RK4: n) is a multiple of sample_every it records t = d*dt,
+ * the positions of the n_ids traced masses (caller ids) and (epe, gpe, ke,
+ * total) in device buffers, and copies the rows out once at the end (one
+ * host synchronisation per call).  *rows_out = rows written (<= max_rows);
+ * divergence: SS_EDIVERGED with `res` filled and no rows. */
+int ss_energy_setup(ss_engine *h, int64_t n_springs, const int64_t *si, const int64_t *sj,
+                    const double *k, const double *l0, const int32_t *group, double gpe_datum);
+int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every,
+                    const int64_t *ids, int64_t n_ids, int64_t max_rows,
+                    double *times_out, double *pos_out, double *energy_out,
+                    int64_t *rows_out, ss_step_result *res);
+
 /* Kernel launches issued so far (for the bench's gpu_launches claim). */
 int64_t ss_launch_count(ss_engine *h);
 

@@ -22,6 +22,7 @@
 #include "common.h"
 #include "kernels.cuh"
 #include "tile_f32.cuh"
+#include "sampling.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
 #include "tiles.h"
@@ -62,15 +63,19 @@ struct ss_engine {
 
     // host-side scalars (engine.py:190-194, 222-224)
     double dt = 1e-4, damping = 0.0, gravity[3] = {0, 0, 0};
+    double gpe_datum = 0.0;        // GPE reference height (engine.py:240-242), sampling only
     std::vector<Group> groups;
     std::vector<double> planes;    // 6 per plane
     std::vector<double> m;         // masses (caller order)
     std::vector<uint8_t> fixed;    // caller order
     std::vector<int32_t> orig_of;  // device id -> caller id (empty: identity)
     std::vector<float> base;       // fp32 base positions, device order, 4 per mass
+    std::vector<double> x0;        // fp32 TILE: rest positions X0 (device order, 3 per slot); state r = x - X0
+    bool rx0 = false;              // fp32 TILE engines keep r = x - X0 (tiles.h), others r = x - P
     double t = 0.0;
     int64_t n = 0;
     bool has_prev = false;
+    void *U = nullptr;             // fp32 Verlet: u = x - x_prev (increment form, kernels.cuh verlet_u)
     bool has_fext = false;
 
     // device state (device order)
@@ -85,6 +90,13 @@ struct ss_engine {
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
     unsigned long long *d_prof = nullptr;      // 16 phase-cycle counters (SS_PROF)
+    void *pinned = nullptr;                    // page-locked staging for state transfers
+    size_t pinned_bytes = 0;
+    // on-device sampling (ss_energy_setup / ss_step_sampled)
+    int *d_ssi = nullptr, *d_ssj = nullptr, *d_sgrp = nullptr;
+    double *d_sk = nullptr, *d_sl0 = nullptr, *d_smass = nullptr, *d_sx0 = nullptr;
+    int64_t energy_springs = -1;               // -1: ss_energy_setup not called
+    DevBuf d_sids, d_srows, d_serows, d_sscale, d_spartial;
     long long *d_div_step = nullptr;
     int *d_div_mass = nullptr;
     int *d_orig_of = nullptr;
@@ -103,8 +115,7 @@ struct ss_engine {
     unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
-    size_t lean_smem = 0;          // fp32 Euler/Verlet tile kernel (tile_f32.cuh), 0 = off
-    int lean_minb = 0;             // SS_LEAN_MINB: register budget experiments (resident CTAs per SM)
+    size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -126,6 +137,7 @@ struct ss_engine {
             if (const NcclApi *api = nccl_api()) api->commDestroy(nccl);
         }
         for (auto &b : bufs) cudaFree(b.p);
+        if (pinned) cudaFreeHost(pinned);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -164,10 +176,17 @@ void pack_positions(const ss_engine *h, const double *x, T4 *out) {
         }
         const double w = h->fixed[s] ? -h->m[s] : h->m[s];
         if constexpr (std::is_same<T, float>::value) {
-            const float *b = h->base.data() + 4 * i;
-            o.x = (float)(x[3 * s + 0] - (double)b[0]);
-            o.y = (float)(x[3 * s + 1] - (double)b[1]);
-            o.z = (float)(x[3 * s + 2] - (double)b[2]);
+            if (h->rx0) {
+                const double *b = h->x0.data() + 3 * i;
+                o.x = (float)(x[3 * s + 0] - b[0]);
+                o.y = (float)(x[3 * s + 1] - b[1]);
+                o.z = (float)(x[3 * s + 2] - b[2]);
+            } else {
+                const float *b = h->base.data() + 4 * i;
+                o.x = (float)(x[3 * s + 0] - (double)b[0]);
+                o.y = (float)(x[3 * s + 1] - (double)b[1]);
+                o.z = (float)(x[3 * s + 2] - (double)b[2]);
+            }
             o.w = (float)w;
         } else {
             o.x = x[3 * s + 0];
@@ -204,10 +223,17 @@ void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
         const int64_t s = h->src_of(i);
         if (s < 0) continue;
         if constexpr (std::is_same<T, float>::value) {
-            const float *b = h->base.data() + 4 * i;
-            x[3 * s + 0] = (double)b[0] + (double)in[i].x;
-            x[3 * s + 1] = (double)b[1] + (double)in[i].y;
-            x[3 * s + 2] = (double)b[2] + (double)in[i].z;
+            if (h->rx0) {
+                const double *b = h->x0.data() + 3 * i;
+                x[3 * s + 0] = b[0] + (double)in[i].x;
+                x[3 * s + 1] = b[1] + (double)in[i].y;
+                x[3 * s + 2] = b[2] + (double)in[i].z;
+            } else {
+                const float *b = h->base.data() + 4 * i;
+                x[3 * s + 0] = (double)b[0] + (double)in[i].x;
+                x[3 * s + 1] = (double)b[1] + (double)in[i].y;
+                x[3 * s + 2] = (double)b[2] + (double)in[i].z;
+            }
         } else {
             x[3 * s + 0] = in[i].x;
             x[3 * s + 1] = in[i].y;
@@ -396,11 +422,7 @@ int halo_exchange_nccl(ss_engine *h) {
 // explicit record format (tile_f32.cuh).
 template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
-    const bool euler = h->integrator == SS_EULER, compact = h->tl.compact;
-    auto *k = euler ? (compact ? tile_lean_kernel<0, GROUPS, 1> : tile_lean_kernel<0, GROUPS, 0>)
-                    : (compact ? tile_lean_kernel<1, GROUPS, 1> : tile_lean_kernel<1, GROUPS, 0>);
-    if (compact && !euler && h->lean_minb == 6) k = tile_lean_kernel<1, GROUPS, 1, 6>;   // SS_LEAN_MINB experiments
-    if (compact && !euler && h->lean_minb == 8) k = tile_lean_kernel<1, GROUPS, 1, 8>;
+    auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
     k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
 }
 
@@ -434,6 +456,10 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.Xout = Xo;
             p.Vout = V;
             p.Xprev = Xo;
+            if (F32 && h->U) {                       // increment-form Verlet: u read and written in place
+                p.Xprev = reinterpret_cast<const T4 *>(h->U);
+                p.U = reinterpret_cast<T4 *>(h->U);
+            }
             p.bootstrap = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
             if constexpr (F32 && LAYOUT >= 3) {
                 if (h->lean_smem) {
@@ -599,11 +625,24 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         }
         if ((rc = h->alloc(&h->P, (size_t)ND * sizeof(T4)))) return rc;
         if ((rc = upload(h, h->P, h->base.data(), (size_t)ND * sizeof(T4)))) return rc;
+        if (layout == SS_LAYOUT_TILE) {             // r = x - X0 with the records' rest vectors
+            h->rx0 = true;
+            h->x0.assign((size_t)ND * 3, 0.0);
+            for (int64_t i = 0; i < ND; ++i) {
+                const int64_t s = h->src_of(i);
+                if (s < 0) continue;
+                for (int c = 0; c < 3; ++c) h->x0[3 * i + c] = d->x[3 * s + c];
+            }
+        }
     }
     for (int b = 0; b < 2; ++b)
         if ((rc = h->alloc(&h->X[b], (size_t)ND * sizeof(T4)))) return rc;
     if ((rc = h->alloc(&h->V, (size_t)ND * sizeof(T4)))) return rc;
     if ((rc = h->alloc(&h->F, (size_t)ND * sizeof(T4)))) return rc;
+    if (F32 && h->integrator == SS_VERLET) {
+        if ((rc = h->alloc(&h->U, (size_t)ND * sizeof(T4)))) return rc;
+        CK(cudaMemsetAsync(h->U, 0, (size_t)ND * sizeof(T4), h->stream));
+    }
     if (h->integrator == SS_RK4) {
         for (void **b : {&h->XA, &h->XB, &h->VS, &h->SV, &h->SA})
             if ((rc = h->alloc(b, (size_t)ND * sizeof(T4)))) return rc;
@@ -645,22 +684,17 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         // the process: grant the device maximum, never a per-engine size
         if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
         if constexpr (F32) {
-            // fp32 Euler/Verlet on tiles: tile_lean_kernel (tile_f32.cuh) unless
-            // SS_KERNEL=step1 asks for kernels.cuh's step_kernel; the tile
-            // kernels need a build without self-springs.
+            // fp32 Euler/Verlet on compact tiles: tile_lean_kernel (tile_f32.cuh)
+            // unless SS_KERNEL=step1 asks for kernels.cuh's step_kernel; the
+            // explicit format and RK4 use the kernels.cuh kernels.
             const char *kenv = getenv("SS_KERNEL");
             const std::string kname = kenv ? kenv : "lean";
-            if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && (int64_t)h->smem_bytes <= dev_max) {
+            if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && L.compact &&
+                (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
-                if (const char *mb = getenv("SS_LEAN_MINB")) h->lean_minb = atoi(mb);
                 const int b = dev_max;
-                for (auto *kk : {tile_lean_kernel<1, false, 1, 6>, tile_lean_kernel<1, false, 1, 8>,
-                                 tile_lean_kernel<1, true, 1, 6>, tile_lean_kernel<1, true, 1, 8>})
-                    CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-                for (auto *kk : {tile_lean_kernel<0, false, 0>, tile_lean_kernel<1, false, 0>,
-                                 tile_lean_kernel<0, true, 0>, tile_lean_kernel<1, true, 0>,
-                                 tile_lean_kernel<0, false, 1>, tile_lean_kernel<1, false, 1>,
-                                 tile_lean_kernel<0, true, 1>, tile_lean_kernel<1, true, 1>})
+                for (auto *kk : {tile_lean_kernel<0, false>, tile_lean_kernel<1, false>, tile_lean_kernel<0, true>,
+                                 tile_lean_kernel<1, true>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
@@ -756,24 +790,59 @@ int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
     });
 }
 
+// Page-locked staging buffer for one (ND) state vector, kept for the
+// engine's lifetime: transfers run at full PCIe/C2C speed and the packing
+// loop never page-faults a fresh allocation.
+template <typename T4>
+int staging(ss_engine *h, T4 **out) {
+    const size_t bytes = (size_t)h->ND * sizeof(T4);
+    if (h->pinned_bytes < bytes) {
+        if (h->pinned) cudaFreeHost(h->pinned);
+        h->pinned = nullptr;
+        h->pinned_bytes = 0;
+        CK(cudaHostAlloc(&h->pinned, bytes, cudaHostAllocDefault));
+        h->pinned_bytes = bytes;
+    }
+    *out = reinterpret_cast<T4 *>(h->pinned);
+    return SS_OK;
+}
+
 template <bool F32>
 int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
-    std::vector<T4> tmp((size_t)h->ND);
+    T4 *tmp;
+    int rc = staging<T4>(h, &tmp);
+    if (rc) return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);
-    int rc;
     if (x) {
-        if ((rc = download(h, tmp.data(), h->X[h->cur], bytes))) return rc;
-        unpack_positions<T, T4>(h, tmp.data(), x);
+        if ((rc = download(h, tmp, h->X[h->cur], bytes))) return rc;
+        unpack_positions<T, T4>(h, tmp, x);
     }
     if (v) {
-        if ((rc = download(h, tmp.data(), h->V, bytes))) return rc;
-        unpack_vec<T, T4>(h, tmp.data(), v);
+        if ((rc = download(h, tmp, h->V, bytes))) return rc;
+        unpack_vec<T, T4>(h, tmp, v);
     }
     if (x_prev && h->has_prev) {
-        if ((rc = download(h, tmp.data(), h->X[h->cur ^ 1], bytes))) return rc;
-        unpack_positions<T, T4>(h, tmp.data(), x_prev);
+        if (F32 && h->U) {                        // x_prev = x - u, in fp64
+            std::vector<T4> xr((size_t)h->ND);
+            if ((rc = download(h, xr.data(), h->X[h->cur], bytes))) return rc;
+            if ((rc = download(h, tmp, h->U, bytes))) return rc;
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < h->ND; ++i) {
+                const int64_t s = h->src_of(i);
+                if (s < 0) continue;
+                const double r[3] = {(double)xr[i].x, (double)xr[i].y, (double)xr[i].z};
+                const double u[3] = {(double)tmp[i].x, (double)tmp[i].y, (double)tmp[i].z};
+                for (int c = 0; c < 3; ++c) {
+                    const double b = h->rx0 ? h->x0[3 * i + c] : (double)h->base[4 * i + c];
+                    x_prev[3 * s + c] = b + (r[c] - u[c]);
+                }
+            }
+        } else {
+            if ((rc = download(h, tmp, h->X[h->cur ^ 1], bytes))) return rc;
+            unpack_positions<T, T4>(h, tmp, x_prev);
+        }
     }
     return SS_OK;
 }
@@ -782,20 +851,51 @@ template <bool F32>
 int set_state_impl(ss_engine *h, const double *x, const double *v, const double *x_prev) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
-    std::vector<T4> tmp((size_t)h->ND);
+    // increment-form Verlet: a new x with the old x_prev means a new u
+    std::vector<double> keep_prev;
+    if (F32 && h->U && x && !x_prev && h->has_prev) {
+        keep_prev.resize((size_t)h->N * 3);
+        int r0 = get_state_impl<F32>(h, nullptr, nullptr, keep_prev.data());
+        if (r0) return r0;
+        x_prev = keep_prev.data();
+    }
+    T4 *tmp;
+    int rc = staging<T4>(h, &tmp);
+    if (rc) return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);
-    int rc;
     if (x) {
-        pack_positions<T, T4>(h, x, tmp.data());
-        if ((rc = upload(h, h->X[h->cur], tmp.data(), bytes))) return rc;
+        pack_positions<T, T4>(h, x, tmp);
+        if ((rc = upload(h, h->X[h->cur], tmp, bytes))) return rc;
     }
     if (v) {
-        pack_vec<T, T4>(h, v, tmp.data());
-        if ((rc = upload(h, h->V, tmp.data(), bytes))) return rc;
+        pack_vec<T, T4>(h, v, tmp);
+        if ((rc = upload(h, h->V, tmp, bytes))) return rc;
     }
     if (x_prev) {
-        pack_positions<T, T4>(h, x_prev, tmp.data());
-        if ((rc = upload(h, h->X[h->cur ^ 1], tmp.data(), bytes))) return rc;
+        if (F32 && h->U) {                        // u = x - x_prev, in fp64 then rounded once
+            std::vector<double> xc;
+            const double *xs = x;
+            if (!xs) {
+                xc.resize((size_t)h->N * 3);
+                if ((rc = get_state_impl<F32>(h, xc.data(), nullptr, nullptr))) return rc;
+                xs = xc.data();
+            }
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < h->ND; ++i) {
+                const int64_t s = h->src_of(i);
+                T4 o{};
+                if (s >= 0) {
+                    o.x = (float)(xs[3 * s + 0] - x_prev[3 * s + 0]);
+                    o.y = (float)(xs[3 * s + 1] - x_prev[3 * s + 1]);
+                    o.z = (float)(xs[3 * s + 2] - x_prev[3 * s + 2]);
+                }
+                tmp[i] = o;
+            }
+            if ((rc = upload(h, h->U, tmp, bytes))) return rc;
+        } else {
+            pack_positions<T, T4>(h, x_prev, tmp);
+            if ((rc = upload(h, h->X[h->cur ^ 1], tmp, bytes))) return rc;
+        }
         h->has_prev = true;
     }
     return SS_OK;
@@ -916,6 +1016,194 @@ int ss_step_async(ss_engine *h, int64_t count) {
     h->n += count;                   // provisional; ss_sync settles it
     h->t = (double)h->n * h->dt;
     return SS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int64_t dev_of(const ss_engine *h, int64_t caller) {
+    return h->tl.new_of.empty() || h->orig_of.empty() ? caller : (int64_t)h->tl.new_of[caller];
+}
+
+int ensure(ss_engine *h, DevBuf &b, size_t bytes) {
+    if (b.bytes >= bytes) return SS_OK;
+    void *p;
+    const int rc = h->alloc(&p, std::max<size_t>(bytes, 256));   // old buffer freed with the engine
+    if (rc) return rc;
+    b.p = p;
+    b.bytes = std::max<size_t>(bytes, 256);
+    return SS_OK;
+}
+
+// Launch the sample kernels for one row at the current device state
+// (Verlet: x_prev buffer, others: x), scales row `scale_row`.
+int launch_sample(ss_engine *h, int64_t row, int n_ids, int use_prev, int grid) {
+    SampleArgs a{};
+    a.X = h->X[use_prev && !h->U ? (h->cur ^ 1) : h->cur];
+    a.Usub = use_prev && h->U ? h->U : nullptr;          // fp32 Verlet: x_prev = x - u
+    a.V = h->V;
+    a.P = h->precision == SS_F32 ? reinterpret_cast<const float4 *>(h->P) : nullptr;
+    a.mass = h->d_smass;
+    a.x0 = h->rx0 ? h->d_sx0 : nullptr;
+    a.nd = (int)h->ND;
+    a.ssi = h->d_ssi;
+    a.ssj = h->d_ssj;
+    a.sk = h->d_sk;
+    a.sl0 = h->d_sl0;
+    a.sgrp = h->groups.empty() ? nullptr : h->d_sgrp;
+    a.scale = reinterpret_cast<const double *>(h->d_sscale.p) + (size_t)row * std::max<size_t>(h->groups.size(), 1);
+    a.n_springs = h->energy_springs;
+    const double g2 = h->gravity[0] * h->gravity[0] + h->gravity[1] * h->gravity[1] + h->gravity[2] * h->gravity[2];
+    a.g_mag = std::sqrt(g2);
+    for (int c = 0; c < 3; ++c) a.up[c] = a.g_mag > 0.0 ? -h->gravity[c] / a.g_mag : 0.0;
+    a.datum = h->gpe_datum;
+    a.ids = reinterpret_cast<const int *>(h->d_sids.p);
+    a.n_ids = n_ids;
+    a.pos_row = reinterpret_cast<double *>(h->d_srows.p) + (size_t)row * n_ids * 3;
+    a.partial = reinterpret_cast<double *>(h->d_spartial.p);
+    a.energy_row = reinterpret_cast<double *>(h->d_serows.p) + (size_t)row * 4;
+    if (h->precision == SS_F32) sample_partial_kernel<true><<<grid, kSampleThreads, 0, h->stream>>>(a);
+    else sample_partial_kernel<false><<<grid, kSampleThreads, 0, h->stream>>>(a);
+    sample_final_kernel<<<1, kSampleThreads, 0, h->stream>>>(a.partial, grid, a.energy_row);
+    CK(cudaGetLastError());
+    h->launches += 2;
+    return SS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ss_energy_setup(ss_engine *h, int64_t n_springs, const int64_t *si, const int64_t *sj, const double *k,
+                    const double *l0, const int32_t *group, double gpe_datum) {
+    if (!h || n_springs < 0 || (n_springs && (!si || !sj || !k || !l0)))
+        return ss::fail(SS_EINVAL, "ss_energy_setup: bad arguments");
+    CK(cudaSetDevice(h->device));
+    int rc = sync_pending(h);
+    if (rc) return rc;
+    h->gpe_datum = gpe_datum;
+    if (h->energy_springs < 0) {
+        const size_t S = (size_t)std::max<int64_t>(n_springs, 1);
+        if ((rc = h->alloc(&h->d_ssi, S * sizeof(int))) || (rc = h->alloc(&h->d_ssj, S * sizeof(int))) ||
+            (rc = h->alloc(&h->d_sgrp, S * sizeof(int))) || (rc = h->alloc(&h->d_sk, S * sizeof(double))) ||
+            (rc = h->alloc(&h->d_sl0, S * sizeof(double))) ||
+            (rc = h->alloc(&h->d_smass, (size_t)h->ND * sizeof(double))))
+            return rc;
+        std::vector<double> md((size_t)h->ND, 0.0);
+        for (int64_t i = 0; i < h->ND; ++i) {
+            const int64_t src = h->src_of(i);
+            if (src >= 0) md[i] = h->m[src];
+        }
+        if ((rc = upload(h, h->d_smass, md.data(), md.size() * sizeof(double)))) return rc;
+        if (h->rx0) {
+            if ((rc = h->alloc(&h->d_sx0, h->x0.size() * sizeof(double)))) return rc;
+            if ((rc = upload(h, h->d_sx0, h->x0.data(), h->x0.size() * sizeof(double)))) return rc;
+        }
+    } else if (n_springs != h->energy_springs) {
+        return ss::fail(SS_EINVAL, "ss_energy_setup: spring count changed");
+    }
+    std::vector<int> a((size_t)n_springs), b((size_t)n_springs), g((size_t)n_springs, -1);
+    for (int64_t s = 0; s < n_springs; ++s) {
+        a[s] = (int)dev_of(h, si[s]);
+        b[s] = (int)dev_of(h, sj[s]);
+        if (group) g[s] = group[s];
+    }
+    if (n_springs) {
+        if ((rc = upload(h, h->d_ssi, a.data(), a.size() * sizeof(int))) ||
+            (rc = upload(h, h->d_ssj, b.data(), b.size() * sizeof(int))) ||
+            (rc = upload(h, h->d_sgrp, g.data(), g.size() * sizeof(int))) ||
+            (rc = upload(h, h->d_sk, k, (size_t)n_springs * sizeof(double))) ||
+            (rc = upload(h, h->d_sl0, l0, (size_t)n_springs * sizeof(double))))
+            return rc;
+    }
+    h->energy_springs = n_springs;
+    return SS_OK;
+}
+
+int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every, const int64_t *ids, int64_t n_ids,
+                    int64_t max_rows, double *times_out, double *pos_out, double *energy_out,
+                    int64_t *rows_out, ss_step_result *res) {
+    if (!h || count < 0 || sample_every < 1 || n_ids < 0 || (n_ids && !ids) || max_rows < 0 || !rows_out)
+        return ss::fail(SS_EINVAL, "ss_step_sampled: bad arguments");
+    if (h->energy_springs < 0) return ss::fail(SS_EINVAL, "ss_step_sampled: call ss_energy_setup first");
+    if (h->integrator == SS_RK4 && h->nccl) return ss::fail(SS_EINVAL, "ss_step_sampled: not for sharded RK4");
+    CK(cudaSetDevice(h->device));
+    int rc = sync_pending(h);
+    if (rc) return rc;
+    const bool verlet = h->integrator == SS_VERLET;
+    // plan the chunks exactly like simulate() (engine.py:546-559 with the
+    // reference's sampling points): samples after steps whose index d
+    // (Verlet: n-1, paired with x_prev) is a multiple of sample_every
+    std::vector<int64_t> chunks, sample_d;
+    {
+        int64_t n = h->n, done = 0;
+        while (done < count) {
+            const int64_t target = verlet ? n - 1 : n;
+            int64_t chunk = sample_every - (((target % sample_every) + sample_every) % sample_every);
+            if (chunk <= 0) chunk = sample_every;
+            chunk = std::min(chunk, count - done);
+            n += chunk;
+            done += chunk;
+            chunks.push_back(chunk);
+            const int64_t d = verlet ? n - 1 : n;
+            sample_d.push_back(d % sample_every == 0 ? d : -1);
+        }
+    }
+    int64_t rows = 0;
+    for (int64_t d : sample_d) rows += d >= 0 ? 1 : 0;
+    if (rows > max_rows) return ss::fail(SS_EINVAL, "ss_step_sampled: %lld rows > max_rows %lld",
+                                         (long long)rows, (long long)max_rows);
+    const size_t G = std::max<size_t>(h->groups.size(), 1);
+    std::vector<double> sc((size_t)std::max<int64_t>(rows, 1) * G, 1.0);
+    std::vector<int> dids((size_t)std::max<int64_t>(n_ids, 1), 0);
+    for (int64_t i = 0; i < n_ids; ++i) dids[i] = (int)dev_of(h, ids[i]);
+    {
+        int64_t r = 0;
+        for (int64_t d : sample_d)
+            if (d >= 0) {
+                if (!h->groups.empty()) scales_at(h, (double)d * h->dt, &sc[(size_t)r * G]);
+                ++r;
+            }
+    }
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = std::max(1, std::min(4 * sms, (int)((std::max<int64_t>(h->energy_springs, h->ND) + 255) / 256)));
+    if ((rc = ensure(h, h->d_sids, dids.size() * sizeof(int))) ||
+        (rc = ensure(h, h->d_srows, (size_t)std::max<int64_t>(rows, 1) * std::max<int64_t>(n_ids, 1) * 3 * sizeof(double))) ||
+        (rc = ensure(h, h->d_serows, (size_t)std::max<int64_t>(rows, 1) * 4 * sizeof(double))) ||
+        (rc = ensure(h, h->d_sscale, sc.size() * sizeof(double))) ||
+        (rc = ensure(h, h->d_spartial, (size_t)grid * 3 * sizeof(double))))
+        return rc;
+    if ((rc = upload(h, h->d_sids.p, dids.data(), dids.size() * sizeof(int))) ||
+        (rc = upload(h, h->d_sscale.p, sc.data(), sc.size() * sizeof(double))))
+        return rc;
+    // enqueue: chunk of steps, then the sample kernels (stream order), one
+    // host synchronisation at the end
+    const int64_t n0 = h->n;
+    const int cur0 = h->cur;
+    int64_t r = 0, total = 0;
+    for (size_t c = 0; c < chunks.size(); ++c) {
+        if ((rc = dispatch_steps(h, chunks[c]))) return rc;
+        h->n += chunks[c];                    // provisional (dispatch reads h->n for scales)
+        h->t = (double)h->n * h->dt;
+        total += chunks[c];
+        if (sample_d[c] >= 0) {
+            if (times_out) times_out[r] = (double)sample_d[c] * h->dt;
+            if ((rc = launch_sample(h, r, (int)n_ids, verlet ? 1 : 0, grid))) return rc;
+            ++r;
+        }
+    }
+    h->n = n0;
+    rc = finish_batch(h, total, n0, cur0, res);
+    const int64_t valid = rc == SS_OK ? rows : 0;       // simulate() raises on divergence
+    if (valid > 0) {
+        if (pos_out && n_ids)
+            CK(cudaMemcpy(pos_out, h->d_srows.p, (size_t)valid * n_ids * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+        if (energy_out) CK(cudaMemcpy(energy_out, h->d_serows.p, (size_t)valid * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    *rows_out = valid;
+    return rc;
 }
 
 int ss_sync(ss_engine *h, ss_step_result *res) {

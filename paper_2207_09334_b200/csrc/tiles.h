@@ -22,21 +22,28 @@ constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compa
 //              bit 15 clear-> in-tile record: owner local id (bits 0-7), slot q (bits 8-14)
 //
 // fp32 builds (production, tiles_f32.cpp build_tiles_f32): one 256-wide ELL
-// slice, slot = q*256 + l, in one of two record formats:
+// slice, slot = q*256 + l.  fp32 tile engines keep the state as the
+// displacement r = x - X0 from the caller's fp64 rest positions, and every
+// record carries the fp32 rest vector D = X0_partner - X0_me, so a spring
+// vector is d = D + (r_partner - r_me): the small r differences keep the
+// strain resolution.  Two record formats:
 //  * compact (canonical bit 1 set, the default when every tile has <= 64
-//    distinct (k, k*l0, group) records and <= 768 halo slots): every mass
-//    has ONE incidence list -- its own springs first, then the springs it
+//    distinct (k, k*l0, group, D) records and <= 768 halo slots -- a voxel
+//    lattice has one per material and stencil direction): every mass has
+//    ONE incidence list -- its own springs first, then the springs it
 //    references -- of u16 = partner slot (10 bits) | dictionary index << 10;
 //    counts = n_own | n_inc << 8 (off_cnt), incidences at off_oo (W = max
-//    n_inc), dictionary float2 (k, k*l0) at off_okl, int8 groups at off_og.
-//    2 B per incidence, 4 B per spring, no foreign copies.
+//    n_inc); dictionary float4 (k, k*l0, Dx, Dy)[n_dict] then float Dz at
+//    off_okl, int8 groups at off_og.  2 B per incidence, 4 B per spring.
 //  * explicit (canonical bit 1 clear): counts = n_own | n_ref << 8; own
-//    records (other u16 off_oo, then planar k[W*256] and k*l0[W*256] at
-//    off_okl, grp i8 off_og); a spring whose owner lies in another tile is
+//    records (other u16 off_oo, then planar k, k*l0, Dx, Dy, Dz [W*256 each]
+//    at off_okl, grp i8 off_og); a spring whose owner lies in another tile is
 //    copied into the partner's tile (owner u16 off_fo, partner u8 off_fl,
-//    planar k, k*l0 off_fkl, grp off_fg); a mass's reference list holds its
-//    foreign references first (0x8000 | copy; their count per mass in
-//    off_nf) and then its in-tile ones, whose value is the owner's slot.
+//    planar k, k*l0, D = X0_owner - X0_partner [n_foreign each] off_fkl, grp
+//    off_fg); a mass's reference list holds its foreign references first
+//    (0x8000 | copy; their count per mass in off_nf) and then its in-tile
+//    ones, whose value is the owner's slot (the vector to the owner is -D of
+//    that record).
 // Padding slots point at their own mass.  Halo slots are bank-aware
 // (tiles_f32.cpp): slot == z (mod 8), holes carry id -1.
 struct TileHdr {

@@ -224,9 +224,14 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
         if (use_dict) {
             // compact format: per mass one incidence list (own springs, then
             // the springs it references), u16 = partner slot | dict index << 10
-            std::map<std::tuple<float, float, int>, uint32_t> dict;
-            auto key_of = [&](int32_t s) {
-                return std::make_tuple((float)in.k[s], (float)(in.k[s] * in.l0[s]), has_g ? (int)in.group[s] : -1);
+            // dictionary key: (k, k*l0, group, rest vector D = fp32(X0_other - X0_me))
+            using Key = std::tuple<float, float, int, float, float, float>;
+            std::map<Key, uint32_t> dict;
+            auto key_of = [&](int32_t s, int64_t m) {
+                const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;
+                return std::make_tuple((float)in.k[s], (float)(in.k[s] * in.l0[s]), has_g ? (int)in.group[s] : -1,
+                                       (float)(in.x[3 * o] - in.x[3 * m]), (float)(in.x[3 * o + 1] - in.x[3 * m + 1]),
+                                       (float)(in.x[3 * o + 2] - in.x[3 * m + 2]));
             };
             std::vector<std::vector<int32_t>> inc(n);
             int Wi = 1;
@@ -234,7 +239,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 const int64_t m = L.orig_of[base + l];
                 for (const int32_t s : own[l]) inc[l].push_back(s);
                 for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r) inc[l].push_back(ref_sp[r]);
-                for (const int32_t s : inc[l]) dict.emplace(key_of(s), 0u);
+                for (const int32_t s : inc[l]) dict.emplace(key_of(s, m), 0u);
                 Wi = std::max(Wi, (int)inc[l].size());
             }
             if (dict.size() > 64 || kTile + halo_ids.size() > 1024 || Wi > 255) {
@@ -254,7 +259,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             h.off_halo = off; off = al16(off + (uint32_t)halo_ids.size() * 4);
             h.off_cnt = off;  off = al16(off + kTile * 2);       // n_own | n_inc << 8
             h.off_oo = off;   off = al16(off + inc_n * 2);       // incidences
-            h.off_okl = off;  off = al16(off + D * 8);           // dictionary (k, k*l0)
+            h.off_okl = off;  off = al16(off + D * 16 + D * 4);  // dictionary float4 (k, k*l0, Dx, Dy), then Dz
             h.off_og = 0;
             if (has_g) { h.off_og = off; off = al16(off + D); } // dictionary groups
             h.off_nf = h.off_ref = h.off_fo = h.off_fkl = h.off_fl = h.off_fg = 0;
@@ -264,9 +269,13 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             std::memcpy(blob.data(), &h, sizeof h);
             std::memcpy(blob.data() + h.off_halo, halo_ids.data(), halo_ids.size() * 4);
             for (const auto &kv : dict) {
-                put_at<float>(blob, h.off_okl + 8 * kv.second, std::get<0>(kv.first));
-                put_at<float>(blob, h.off_okl + 8 * kv.second + 4, std::get<1>(kv.first));
-                if (has_g) put_at<int8_t>(blob, h.off_og + kv.second, (int8_t)std::get<2>(kv.first));
+                const uint32_t e = kv.second;
+                put_at<float>(blob, h.off_okl + 16 * e, std::get<0>(kv.first));
+                put_at<float>(blob, h.off_okl + 16 * e + 4, std::get<1>(kv.first));
+                put_at<float>(blob, h.off_okl + 16 * e + 8, std::get<3>(kv.first));
+                put_at<float>(blob, h.off_okl + 16 * e + 12, std::get<4>(kv.first));
+                put_at<float>(blob, h.off_okl + 16 * D + 4 * e, std::get<5>(kv.first));
+                if (has_g) put_at<int8_t>(blob, h.off_og + e, (int8_t)std::get<2>(kv.first));
             }
             int64_t n_inc = 0;
             for (int l = 0; l < n; ++l) {
@@ -275,7 +284,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 for (size_t q = 0; q < inc[l].size(); ++q) {
                     const int32_t s = inc[l][q];
                     const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;   // the other endpoint
-                    const uint32_t v = (uint32_t)slot_of_local(L.new_of[o]) | (dict.at(key_of(s)) << 10);
+                    const uint32_t v = (uint32_t)slot_of_local(L.new_of[o]) | (dict.at(key_of(s, m)) << 10);
                     put_at<uint16_t>(blob, h.off_oo + 2 * (((uint32_t)q << 8) | (uint32_t)l), (uint16_t)v);
                 }
                 n_inc += (int64_t)inc[l].size();
@@ -297,13 +306,13 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
         h.off_cnt = off;  off = al16(off + kTile * 2);
         h.off_nf = off;   off = al16(off + kTile);
         h.off_oo = off;   off = al16(off + own_n * 2);
-        h.off_okl = off;  off = al16(off + own_n * 8);
+        h.off_okl = off;  off = al16(off + own_n * 20);         // planar k, k*l0, Dx, Dy, Dz
         h.off_og = 0;
         if (has_g) { h.off_og = off; off = al16(off + own_n); }
         h.off_ref = off;  off = al16(off + ref_n * 2);
         h.off_fo = off;   off = al16(off + nf * 2);
         h.off_fl = off;   off = al16(off + nf);
-        h.off_fkl = off;  off = al16(off + nf * 8);
+        h.off_fkl = off;  off = al16(off + nf * 20);            // planar k, k*l0, Dx, Dy, Dz
         h.off_fg = 0;
         if (has_g) { h.off_fg = off; off = al16(off + nf); }
         h.bytes = off;
@@ -324,14 +333,16 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 const int32_t s = own[l][q];
                 const uint32_t slot = ((uint32_t)q << 8) | (uint32_t)l;
                 put_at<uint16_t>(blob, h.off_oo + 2 * slot, slot_of_local(L.new_of[other_of(s)]));
+                const int64_t o = other_of(s);                  // D = X0_other - X0_owner
                 put_at<float>(blob, h.off_okl + 4 * slot, (float)in.k[s]);
                 put_at<float>(blob, h.off_okl + 4 * (own_n + slot), (float)(in.k[s] * in.l0[s]));
+                for (int c = 0; c < 3; ++c)
+                    put_at<float>(blob, h.off_okl + 4 * ((2 + c) * own_n + slot), (float)(in.x[3 * o + c] - in.x[3 * m + c]));
                 if (has_g) put_at<int8_t>(blob, h.off_og + slot, (int8_t)in.group[s]);
             }
             for (size_t q = 0; q < refs[l].size(); ++q)
                 put_at<uint16_t>(blob, h.off_ref + 2 * (((uint32_t)q << 8) | (uint32_t)l), (uint16_t)refs[l][q]);
             n_refs += (int64_t)refs[l].size();
-            (void)m;
         }
         for (uint32_t f = 0; f < nf; ++f) {
             const int32_t s = foreign[f];
@@ -339,6 +350,11 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             put_at<uint8_t>(blob, h.off_fl + f, foreign_l[f]);
             put_at<float>(blob, h.off_fkl + 4 * f, (float)in.k[s]);
             put_at<float>(blob, h.off_fkl + 4 * (nf + f), (float)(in.k[s] * in.l0[s]));
+            {                                                   // D = X0_owner - X0_partner
+                const int64_t ow = owner_of(s), pa = other_of(s);
+                for (int c = 0; c < 3; ++c)
+                    put_at<float>(blob, h.off_fkl + 4 * ((2 + c) * nf + f), (float)(in.x[3 * ow + c] - in.x[3 * pa + c]));
+            }
             if (has_g) put_at<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
         }
         const int64_t n_for_t = nf;

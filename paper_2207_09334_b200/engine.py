@@ -495,6 +495,46 @@ class Engine:
             raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
         _lib.check(rc, "ss_step")
 
+    def step_sampled(self, count: int, sample_every: int, traces=()):
+        """Advance ``count`` steps recording, on the device, the samples
+        ``simulate`` takes (engine.py:546-559): after every step whose index
+        d (Verlet: n-1, at x_prev with the lagged v; otherwise n) is a
+        multiple of ``sample_every``, the traced positions and the energy
+        breakdown at t = d*dt.  Returns (times (R,), positions (R, n, 3),
+        energies (R, 4)).  One host synchronisation per call."""
+        count = int(count)
+        sample_every = max(1, int(sample_every))
+        ids = np.ascontiguousarray(list(traces), dtype=np.int64)
+        if count <= 0:
+            return np.zeros(0), np.zeros((0, ids.size, 3)), np.zeros((0, 4))
+        self.drain_commands()
+        self._upload_lent()
+        self._push_params()
+        lib = _lib.lib()
+        if not getattr(self, "_energy_ready", False):
+            grp = np.ascontiguousarray(self._group_of, dtype=np.int32)
+            _lib.check(lib.ss_energy_setup(self._h, self.spring_count, _lib.i64ptr(self._si),
+                                           _lib.i64ptr(self._sj), _lib.dptr(self._sk),
+                                           _lib.dptr(self._l0),
+                                           grp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                           float(self.gpe_datum)), "ss_energy_setup")
+            self._energy_ready = True
+        max_rows = count // sample_every + 2
+        times = np.empty(max_rows)
+        pos = np.empty((max_rows, max(ids.size, 1), 3))
+        en = np.empty((max_rows, 4))
+        rows = C.c_int64()
+        res = _lib.StepResult()
+        rc = lib.ss_step_sampled(self._h, count, sample_every, _lib.i64ptr(ids) if ids.size else None,
+                                 int(ids.size), max_rows, _lib.dptr(times), _lib.dptr(pos), _lib.dptr(en),
+                                 C.byref(rows), C.byref(res))
+        self._mark_stepped()
+        if rc == _lib.SS_EDIVERGED:
+            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+        _lib.check(rc, "ss_step_sampled")
+        r = int(rows.value)
+        return times[:r], pos[:r, :ids.size], en[:r]
+
     def step_async(self, count: int) -> None:
         """Enqueue ``count`` steps without synchronising (benchmarks)."""
         self._upload_lent()
@@ -671,6 +711,10 @@ class RunResult:
             fh.write("\n".join(lines) + "\n")
 
 
+SAMPLE_SEGMENT_ROWS = 4096          # samples per device segment of simulate()
+DEVICE_SAMPLING = True              # False: sample on the host after every chunk (reference-style)
+
+
 def simulate(scene, duration: float, traces=(), integrator: str = VERLET,
              mode: str = SERIAL, threads: int | None = None, sample_every: int = 1,
              engine: Engine | None = None, **engine_kwargs) -> RunResult:
@@ -698,11 +742,24 @@ def simulate(scene, duration: float, traces=(), integrator: str = VERLET,
         emit(0, engine.x, engine.v)
 
     done = 0
+    device_sampling = DEVICE_SAMPLING
     while done < steps:
         while engine.paused and not engine.stopped:
             engine.drain_commands(wait=0.02)
         if engine.stopped:
             break
+        if device_sampling and engine._commands.empty():
+            # steps and samples enqueued on the device in segments; commands
+            # and pause/stop are honoured between segments
+            seg = min(steps - done, SAMPLE_SEGMENT_ROWS * sample_every)
+            t_s, p_s, e_s = engine.step_sampled(seg, sample_every, list(rows))
+            done += seg
+            for r in range(len(t_s)):
+                times.append(float(t_s[r]))
+                for q, mass_id in enumerate(rows):
+                    rows[mass_id].append(p_s[r, q].copy())
+                erows.append(tuple(e_s[r]))
+            continue
         n = engine.n
         if not engine._commands.empty():
             chunk = 1                       # reference: drain + one step

@@ -286,3 +286,33 @@ def test_host_inplace_edits_reach_the_device():
     eng.step()
     assert eng.x[0, 0] == pytest.approx(0.2)
     assert eng.v[0, 1] == pytest.approx(1.0)
+
+
+@pytest.mark.parametrize("integrator", ["verlet", "euler", "rk4"])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_device_sampling_matches_host_sampling(integrator, precision):
+    """simulate() with on-device sampling (ss_step_sampled) against the
+    reference-style host path (step per sampling chunk, download, numpy
+    energy_breakdown): identical sample times and positions, energies equal
+    to 1e-12 relative (only the summation order differs)."""
+    import paper_2207_09334_b200.engine as E
+    from paper_2207_09334_b200 import crawler_scene
+    out = {}
+    for device in (True, False):
+        E.DEVICE_SAMPLING = device
+        try:
+            sc = crawler_scene()
+            res = simulate(sc, 0.02, traces=[0, 7, 19], integrator=integrator, sample_every=7,
+                           precision=precision)
+        finally:
+            E.DEVICE_SAMPLING = True
+        out[device] = res
+    a, b = out[True], out[False]
+    np.testing.assert_array_equal(a.times, b.times)
+    for i in (0, 7, 19):
+        if precision == "f64":
+            assert a.positions[i].tobytes() == b.positions[i].tobytes()
+        else:   # fp32 Verlet samples x_prev = X0 + (r - u): same value, fp64 rounding path may differ
+            np.testing.assert_allclose(a.positions[i], b.positions[i], rtol=1e-14, atol=1e-16)
+    np.testing.assert_allclose(a.energies, b.energies, rtol=1e-12, atol=1e-15)
+    assert a.engine.n == b.engine.n
