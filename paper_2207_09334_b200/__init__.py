@@ -53,5 +53,6 @@ from .model import (
     validate_scene,
 )
 from .traces import TraceSeries
+from .batch import per_instance, replicate
 
 __version__ = "0.1.0"

@@ -9,6 +9,9 @@ reference (springsim) on this container's CPU:
   for the 20x4x4 and 40x4x4 beams: the calibrated tip load, the probe and
   tip masses, the step counts, the damped-relaxed tip deflection and the
   FFT / zero-cross frequency of the released ring-down;
+* config 3, an ensemble of actuated crawlers (demos/crawler.py) with
+  1e-9 m position jitter: net travel per instance after 8 s (the walker is
+  chaotic, SURVEY §7 d', so fp32 is judged on the ensemble mean);
 * config 2, the multi-material natural-frequency cube (SURVEY §8d recipe:
   block_scene(n), k x10 where both endpoints have x < side/2, released from
   a 0.1% x-stretch about the centroid at rest): FFT dominant frequency of the
@@ -91,6 +94,33 @@ def cube_case(cells, seconds=2.0, stiff=10.0, stretch=1e-3, threads=8):
             "cpu_seconds": round(time.time() - t0, 1)}
 
 
+def crawler_ensemble(copies=16, jitter=1e-9, seed=5, seconds=8.0):
+    """Config 3: the actuated crawler (demos/crawler.py:27-71, damping 2e-4),
+    `copies` instances whose initial positions carry N(0, jitter) noise
+    (instance 0 exact; numpy default_rng(seed).normal(0, jitter, (copies, N, 3))),
+    each run by the reference for `seconds`; net x-centre travel per instance."""
+    sys.path.insert(0, "/root/reference/pkg/demos")
+    from crawler import build_crawler
+    t0 = time.time()
+    base = build_crawler()
+    n = base.mass_count
+    noise = np.random.default_rng(seed).normal(0.0, jitter, (copies, n, 3))
+    noise[0] = 0.0
+    travel = []
+    for c in range(copies):
+        scene = build_crawler()
+        for i, m in enumerate(scene.masses):
+            m.x = tuple(np.asarray(m.x, dtype=np.float64) + noise[c, i])
+        eng = Engine(scene)
+        eng.set_damping(2e-4)
+        start = float(np.mean(eng.x[:, 0]))
+        eng.step(int(round(seconds / scene.dt)))
+        travel.append(float(np.mean(eng.x[:, 0])) - start)
+    return {"copies": copies, "jitter": jitter, "seed": seed, "seconds": seconds, "damping": 2e-4,
+            "travel": travel, "mean_travel": float(np.mean(travel)), "std_travel": float(np.std(travel)),
+            "cpu_seconds": round(time.time() - t0, 1)}
+
+
 if __name__ == "__main__":
     out = json.load(open(OUT)) if os.path.exists(OUT) else {}
     which = sys.argv[1:] or ["beam20", "beam40", "cube12", "cube42"]
@@ -103,6 +133,9 @@ if __name__ == "__main__":
             out["cube_mm_12"] = cube_case(12)
         elif w == "cube42":
             out["cube_mm_42"] = cube_case(42)
+        elif w == "crawler":
+            out["crawler_ensemble"] = crawler_ensemble()
         json.dump(out, open(OUT, "w"), indent=1)
         print(w, json.dumps(out.get({"beam20": "beam_20x4x4", "beam40": "beam_40x4x4",
-                                     "cube12": "cube_mm_12", "cube42": "cube_mm_42"}[w])), flush=True)
+                                     "cube12": "cube_mm_12", "cube42": "cube_mm_42",
+                                     "crawler": "crawler_ensemble"}[w])), flush=True)

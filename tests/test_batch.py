@@ -1,0 +1,77 @@
+"""Batches of independent instances (paper_2207_09334_b200.batch).
+
+CPU: the block-diagonal structure.  GPU: an instance of the batch steps
+bitwise like the scene alone (fp64), and the fp32 crawler ensemble's mean
+travel agrees with the reference's ensemble (tests/golden/observables.json).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2207_09334_b200 import Engine, crawler_scene, per_instance, replicate
+from paper_2207_09334_b200.batch import jitter_noise, shard
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "observables.json")
+
+
+def test_replicate_is_block_diagonal():
+    sc = crawler_scene()
+    b = replicate(sc, 5, jitter=1e-9, seed=3)
+    n, s = sc.mass_count, sc.spring_count
+    assert b.mass_count == 5 * n and b.spring_count == 5 * s
+    for c in range(5):
+        seg = slice(c * s, (c + 1) * s)
+        assert (b.si[seg] == sc.si + c * n).all() and (b.sj[seg] == sc.sj + c * n).all()
+        assert (b.group[seg] == sc.group).all()
+    x = per_instance(b.x, 5)
+    assert x[0].tobytes() == sc.x.tobytes()
+    np.testing.assert_allclose(x - sc.x[None], jitter_noise(n, 5, 1e-9, 3), atol=1e-15)
+    assert b.planes == sc.planes and b.group_labels == sc.group_labels
+
+
+def test_shard_by_instance_covers_once():
+    for copies in (1, 7, 16, 33):
+        for ranks in (1, 2, 3, 8):
+            spans = [shard(copies, ranks, r) for r in range(ranks)]
+            assert spans[0][0] == 0 and spans[-1][1] == copies
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("integrator", ["verlet", "euler"])
+def test_batch_instance_bitwise_equals_single(integrator):
+    sc = crawler_scene()
+    one = Engine(sc, integrator=integrator, precision="f64")
+    one.set_damping(2e-4)
+    one.step(3000)
+    b = replicate(sc, 8)
+    eng = Engine(b, integrator=integrator, precision="f64")
+    eng.set_damping(2e-4)
+    eng.step(3000)
+    x = per_instance(eng.x, 8)
+    for c in range(8):
+        assert x[c].tobytes() == one.x.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_crawler_ensemble_travel(precision):
+    """Config 3 (walker): 16 jittered crawlers for 8 s in one batch.  fp64:
+    every instance's travel equals the reference's bitwise; fp32 (chaotic
+    trajectories): the ensemble mean within 5% of the reference's."""
+    if not os.path.exists(GOLD) or "crawler_ensemble" not in json.load(open(GOLD)):
+        pytest.skip("crawler_ensemble golden not generated")
+    g = json.load(open(GOLD))["crawler_ensemble"]
+    sc = crawler_scene()
+    b = replicate(sc, g["copies"], jitter=g["jitter"], seed=g["seed"])
+    eng = Engine(b, integrator="verlet", precision=precision)
+    eng.set_damping(g["damping"])
+    start = per_instance(eng.x, g["copies"])[:, :, 0].mean(axis=1)
+    eng.step(int(round(g["seconds"] / sc.dt)))
+    travel = per_instance(eng.x, g["copies"])[:, :, 0].mean(axis=1) - start
+    if precision == "f64":
+        np.testing.assert_array_equal(travel, np.asarray(g["travel"]))
+    else:
+        assert abs(travel.mean() - g["mean_travel"]) <= 0.05 * abs(g["mean_travel"])

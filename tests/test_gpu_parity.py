@@ -45,6 +45,10 @@ def test_fp64_bitwise_vs_reference(case, layout):
 @pytest.mark.parametrize("layout", ["csr", "ell", "tile"])
 @pytest.mark.parametrize("case", [c for c in golden_cases() if "degenerate" not in c])
 def test_fp32_within_tolerance(case, layout):
+    run_case_fp32(case, layout)
+
+
+def run_case_fp32(case, layout):
     d, eng = run_engine(case, layout, precision="f32")
     done = 0
     for c in d["checkpoints"]:
@@ -120,3 +124,18 @@ def test_momentum_conserved_free_block():
     eng.step(1000)
     p1 = (eng.m[:, None] * eng.v).sum(axis=0)
     assert np.linalg.norm(p1 - p0) / np.linalg.norm(p0) <= 1e-9
+
+
+@pytest.mark.parametrize("case", ["crawler_verlet", "block9_excited_verlet", "cantilever_10x2x2_verlet",
+                                  "random_order_verlet", "block3_excited_rk4"])
+def test_fp32_explicit_tile_format(case, monkeypatch):
+    """The fp32 explicit tile format (the fallback for tiles with more than 64
+    distinct spring records, SS_TILE_DICT=0 forces it) within the fp32
+    tolerance of the reference."""
+    monkeypatch.setenv("SS_TILE_DICT", "0")
+    if "degenerate" in case:
+        pytest.skip("degenerate golden is fp64-only")
+    run_case_fp32(case, "tile")
+    from paper_2207_09334_b200.engine import plan  # noqa: F401  (format check below)
+    d, eng = run_engine(case, "tile", precision="f32")
+    assert eng.info()["tile_kernel"] in (0, 1)      # explicit records, kernels.cuh step_kernel
