@@ -92,6 +92,8 @@ struct ss_engine {
     unsigned long long *d_prof = nullptr;      // 16 phase-cycle counters (SS_PROF)
     void *pinned = nullptr;                    // page-locked staging for state transfers
     size_t pinned_bytes = 0;
+    void *pinned2 = nullptr;                   // second staging buffer (x_prev = x - u)
+    size_t pinned2_bytes = 0;
     // on-device sampling (ss_energy_setup / ss_step_sampled)
     int *d_ssi = nullptr, *d_ssj = nullptr, *d_sgrp = nullptr;
     double *d_sk = nullptr, *d_sl0 = nullptr, *d_smass = nullptr, *d_sx0 = nullptr;
@@ -138,6 +140,7 @@ struct ss_engine {
         }
         for (auto &b : bufs) cudaFree(b.p);
         if (pinned) cudaFreeHost(pinned);
+        if (pinned2) cudaFreeHost(pinned2);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -794,16 +797,18 @@ int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
 // engine's lifetime: transfers run at full PCIe/C2C speed and the packing
 // loop never page-faults a fresh allocation.
 template <typename T4>
-int staging(ss_engine *h, T4 **out) {
+int staging(ss_engine *h, T4 **out, int which = 0) {
     const size_t bytes = (size_t)h->ND * sizeof(T4);
-    if (h->pinned_bytes < bytes) {
-        if (h->pinned) cudaFreeHost(h->pinned);
-        h->pinned = nullptr;
-        h->pinned_bytes = 0;
-        CK(cudaHostAlloc(&h->pinned, bytes, cudaHostAllocDefault));
-        h->pinned_bytes = bytes;
+    void *&buf = which ? h->pinned2 : h->pinned;
+    size_t &have = which ? h->pinned2_bytes : h->pinned_bytes;
+    if (have < bytes) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        have = 0;
+        CK(cudaHostAlloc(&buf, bytes, cudaHostAllocDefault));
+        have = bytes;
     }
-    *out = reinterpret_cast<T4 *>(h->pinned);
+    *out = reinterpret_cast<T4 *>(buf);
     return SS_OK;
 }
 
@@ -825,8 +830,9 @@ int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     }
     if (x_prev && h->has_prev) {
         if (F32 && h->U) {                        // x_prev = x - u, in fp64
-            std::vector<T4> xr((size_t)h->ND);
-            if ((rc = download(h, xr.data(), h->X[h->cur], bytes))) return rc;
+            T4 *xr;
+            if ((rc = staging<T4>(h, &xr, 1))) return rc;
+            if ((rc = download(h, xr, h->X[h->cur], bytes))) return rc;
             if ((rc = download(h, tmp, h->U, bytes))) return rc;
 #pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < h->ND; ++i) {

@@ -363,8 +363,9 @@ class Engine:
 
     @x.setter
     def x(self, value) -> None:
-        self._download()
-        self._x.arr = np.array(value, dtype=np.float64).reshape(-1, 3)
+        # like the reference's plain attribute: keep the caller's array (no
+        # copy when it is already (N,3) float64); uploaded before the next step
+        self._x.arr = np.asarray(value, dtype=np.float64).reshape(-1, 3)
         self._x.stale, self._x.lent = False, True
 
     @property
@@ -375,8 +376,7 @@ class Engine:
 
     @v.setter
     def v(self, value) -> None:
-        self._download()
-        self._v.arr = np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._v.arr = np.asarray(value, dtype=np.float64).reshape(-1, 3)
         self._v.stale, self._v.lent = False, True
 
     @property
@@ -392,8 +392,7 @@ class Engine:
         if self.integrator != VERLET:
             self._host_prev_nonverlet = None if value is None else np.array(value, dtype=np.float64)
             return
-        self._download()
-        self._xp.arr = None if value is None else np.array(value, dtype=np.float64).reshape(-1, 3)
+        self._xp.arr = None if value is None else np.asarray(value, dtype=np.float64).reshape(-1, 3)
         self._xp.stale, self._xp.lent = False, True
 
     @property
