@@ -118,6 +118,7 @@ struct ss_engine {
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
+    bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
     int64_t device_bytes = 0;
     int64_t launches = 0;
     int64_t pending = 0;
@@ -426,7 +427,23 @@ int halo_exchange_nccl(ss_engine *h) {
 template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
-    k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+    if (!h->pdl) {
+        k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+        return;
+    }
+    // programmatic dependent launch: the next substep's CTAs may start (and
+    // prefetch their records) while this one drains (tile_f32.cuh)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTile);
+    cfg.dynamicSmemBytes = h->lean_smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, p);
 }
 
 template <bool F32, int LAYOUT>
@@ -695,6 +712,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
+                if (const char *e = getenv("SS_PDL")) h->pdl = atoi(e) != 0;
                 const int b = dev_max;
                 for (auto *kk : {tile_lean_kernel<0, false>, tile_lean_kernel<1, false>, tile_lean_kernel<0, true>,
                                  tile_lean_kernel<1, true>})

@@ -204,10 +204,15 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
     __syncthreads();
 }
 
+// Launched with programmatic dependent launch (engine.cu launch_tile_f32):
+// every CTA lets the next substep's grid launch as soon as it has started,
+// so the next grid's CTAs fill the SM slots freed during this grid's tail and
+// stream their (step-independent) record blobs by TMA before they wait for
+// this grid's positions (griddepcontrol.wait).
 template <int INTEG, bool GROUPS, int MINB = 5>
 __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    if (*p.div_step < p.step) return;                       // grid-uniform
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const Topology<float> &t = p.topo;
     const int l = threadIdx.x;
     const int m = blockIdx.x * kTile + l;
@@ -231,6 +236,9 @@ __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p)
         bulk_copy(bl, t.blob + g0, split, bar);
         bulk_copy(bl + split, t.blob + g0 + split, bytes - split, bar + 1);
     }
+    // everything below reads the previous substep's state
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (*p.div_step < p.step) return;                       // grid-uniform (an earlier step diverged)
     float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), hist = x4;
     if (active) {
         x4 = ldg4(p.X + m);                                 // r = x - X0, w = +-m
