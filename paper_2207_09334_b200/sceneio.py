@@ -1,0 +1,229 @@
+"""Scene documents: the reference's strict, versioned JSON format
+(reference sceneio.py:1-251), read and written array-natively.
+
+``render_scene`` produces byte-identical text to the reference's
+``render_scene`` for the same scene (same key order, same shortest
+round-trip float repr, 2-space indent), straight from the SoA arrays -- no
+Mass/Spring objects are built, which is what makes 10^6-spring scenes
+practical.  ``parse_scene`` applies the reference's schema checks (unknown
+and missing fields, types, contiguous ids, mass indices, duplicate springs
+via ``validate_scene``) and returns an :class:`ArrayScene` ready for
+``Engine``; errors are :class:`SceneFormatError` with the offending path.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+from .model import ActuationGroup, ArrayScene, ContactPlane, Material, scene_arrays, validate_scene
+
+SCHEMA_VERSION = 1
+
+__all__ = ["SCHEMA_VERSION", "SceneFormatError", "render_scene", "parse_scene", "save_scene", "load_scene"]
+
+
+class SceneFormatError(ValueError):
+    """A scene document that cannot be accepted, with the offending path (sceneio.py:23-28)."""
+
+    def __init__(self, path: str, message: str):
+        self.path = path
+        super().__init__(f"{path}: {message}")
+
+
+def _vec(a) -> list:
+    return [float(c) for c in a]
+
+
+def render_scene(scene) -> str:
+    """Serialize ``scene`` (Scene, ArrayScene or a reference Scene) to the
+    versioned document text (sceneio.py:57-75)."""
+    a = scene_arrays(scene)
+    labels = [g[0] for g in a.group_params]
+    x, v, f = a.x.tolist(), a.v.tolist(), a.f_ext.tolist()
+    m, fixed = a.m.tolist(), a.fixed.tolist()
+    masses = [{"id": i, "m": m[i], "x": x[i], "v": v[i], "f_ext": f[i], "fixed": bool(fixed[i])}
+              for i in range(len(m))]
+    si, sj, k, l0 = a.si.tolist(), a.sj.tolist(), a.k.tolist(), a.l0.tolist()
+    grp = a.group.tolist() if a.group is not None else None
+    springs = [{"id": s, "i": si[s], "j": sj[s], "k": k[s], "l0": l0[s],
+                "group": (labels[grp[s]] if grp is not None and grp[s] >= 0 else None)}
+               for s in range(len(si))]
+    mats = [{"name": mt.name, "k0": mt.k0, "l_ref": mt.l_ref, "density": mt.density,
+             "total_mass": mt.total_mass, "mass_per_node": mt.mass_per_node}
+            for mt in getattr(scene, "materials", [])]
+    groups = [{"label": lab, "mode": mode, "amplitude": amp, "frequency": freq, "phase": ph}
+              for lab, mode, amp, freq, ph in a.group_params]
+    planes = [{"normal": _vec(nrm), "offset": off, "penalty": pen, "friction": fr}
+              for nrm, off, pen, fr in a.planes]
+    doc = {"schema_version": SCHEMA_VERSION, "gravity": _vec(a.gravity), "dt": a.dt, "damping": a.damping,
+           "masses": masses, "springs": springs, "materials": mats, "groups": groups, "planes": planes}
+    try:
+        return json.dumps(doc, indent=2, allow_nan=False) + "\n"
+    except ValueError as exc:
+        raise SceneFormatError("$", f"non-finite value in scene: {exc}") from exc
+
+
+# ------------------------------------------------------------ parsing
+
+_NUM = (int, float)
+
+
+def _coerce(value, path: str, kind):
+    """Type checks of sceneio.py:98-136."""
+    if kind == "number":
+        if isinstance(value, bool) or not isinstance(value, _NUM):
+            raise SceneFormatError(path, f"expected a number, got {type(value).__name__}")
+        return float(value)
+    if kind == "int":
+        if isinstance(value, bool) or not isinstance(value, int):
+            raise SceneFormatError(path, f"expected an integer, got {type(value).__name__}")
+        return value
+    if kind == "bool":
+        if not isinstance(value, bool):
+            raise SceneFormatError(path, f"expected a boolean, got {type(value).__name__}")
+        return value
+    if kind == "string":
+        if not isinstance(value, str):
+            raise SceneFormatError(path, f"expected a string, got {type(value).__name__}")
+        return value
+    if kind == "string?":
+        if value is not None and not isinstance(value, str):
+            raise SceneFormatError(path, f"expected a string or null, got {type(value).__name__}")
+        return value
+    if kind == "number?":
+        return None if value is None else _coerce(value, path, "number")
+    if kind == "vec3":
+        if (not isinstance(value, list) or len(value) != 3
+                or any(isinstance(c, bool) or not isinstance(c, _NUM) for c in value)):
+            raise SceneFormatError(path, "expected a list of three numbers")
+        return tuple(float(c) for c in value)
+    if kind == "list":
+        if not isinstance(value, list):
+            raise SceneFormatError(path, f"expected a list, got {type(value).__name__}")
+        return value
+    raise AssertionError(kind)
+
+
+def _expect(obj, path: str, required: dict, optional: dict) -> dict:
+    if not isinstance(obj, dict):
+        raise SceneFormatError(path, f"expected an object, got {type(obj).__name__}")
+    known = set(required) | set(optional)
+    for key in obj:
+        if key not in known:
+            raise SceneFormatError(f"{path}.{key}", "unknown field")
+    out = {}
+    for key, kind in required.items():
+        if key not in obj:
+            raise SceneFormatError(path, f"missing required field {key!r}")
+        out[key] = _coerce(obj[key], f"{path}.{key}", kind)
+    for key, (kind, default) in optional.items():
+        out[key] = _coerce(obj[key], f"{path}.{key}", kind) if key in obj else default
+    return out
+
+
+_TOP = dict(required={"schema_version": "int", "gravity": "vec3", "dt": "number", "masses": "list",
+                      "springs": "list"},
+            optional={"damping": ("number", 0.0), "materials": ("list", []), "groups": ("list", []),
+                      "planes": ("list", [])})
+_MASS = dict(required={"m": "number", "x": "vec3"},
+             optional={"id": ("int", None), "v": ("vec3", (0.0, 0.0, 0.0)), "f_ext": ("vec3", (0.0, 0.0, 0.0)),
+                       "fixed": ("bool", False)})
+_SPRING = dict(required={"i": "int", "j": "int", "k": "number", "l0": "number"},
+               optional={"id": ("int", None), "group": ("string?", None)})
+_MATERIAL = dict(required={"name": "string"},
+                 optional={"k0": ("number", 10000.0), "l_ref": ("number?", None), "density": ("number?", None),
+                           "total_mass": ("number?", None), "mass_per_node": ("number?", None)})
+_GROUP = dict(required={"label": "string", "mode": "string"},
+              optional={"amplitude": ("number", 0.0), "frequency": ("number", 1.0), "phase": ("number", 0.0)})
+_PLANE = dict(required={"normal": "vec3"},
+              optional={"offset": ("number", 0.0), "penalty": ("number", 1e5), "friction": ("number", 0.0)})
+
+
+def parse_scene(text: str) -> ArrayScene:
+    """Parse and validate a scene document (sceneio.py:173-239) into arrays."""
+    try:
+        raw = json.loads(text)
+    except json.JSONDecodeError as exc:
+        raise SceneFormatError("$", f"malformed document: {exc}") from exc
+    top = _expect(raw, "$", **_TOP)
+    if top["schema_version"] != SCHEMA_VERSION:
+        raise SceneFormatError("$.schema_version",
+                               f"unsupported version {top['schema_version']} (this reader handles {SCHEMA_VERSION})")
+    n = len(top["masses"])
+    x = np.empty((n, 3))
+    v = np.empty((n, 3))
+    f = np.empty((n, 3))
+    m = np.empty(n)
+    fixed = np.zeros(n, dtype=bool)
+    for idx, entry in enumerate(top["masses"]):
+        path = f"$.masses[{idx}]"
+        fl = _expect(entry, path, **_MASS)
+        if fl["id"] is not None and fl["id"] != idx:
+            raise SceneFormatError(f"{path}.id", f"ids must be contiguous; expected {idx}")
+        x[idx], v[idx], f[idx], m[idx], fixed[idx] = fl["x"], fl["v"], fl["f_ext"], fl["m"], fl["fixed"]
+    s_count = len(top["springs"])
+    si = np.empty(s_count, dtype=np.int64)
+    sj = np.empty(s_count, dtype=np.int64)
+    k = np.empty(s_count)
+    l0 = np.empty(s_count)
+    labels: list = []
+    glist = []
+    for idx, entry in enumerate(top["springs"]):
+        path = f"$.springs[{idx}]"
+        fl = _expect(entry, path, **_SPRING)
+        if fl["id"] is not None and fl["id"] != idx:
+            raise SceneFormatError(f"{path}.id", f"ids must be contiguous; expected {idx}")
+        for end in ("i", "j"):
+            if not 0 <= fl[end] < n:
+                raise SceneFormatError(f"{path}.{end}", f"no such mass {fl[end]}")
+        si[idx], sj[idx], k[idx], l0[idx] = fl["i"], fl["j"], fl["k"], fl["l0"]
+        glist.append(fl["group"])
+    mats = [Material(**_expect(e, f"$.materials[{i}]", **_MATERIAL)) for i, e in enumerate(top["materials"])]
+    groups = {}
+    for i, e in enumerate(top["groups"]):
+        fl = _expect(e, f"$.groups[{i}]", **_GROUP)
+        try:
+            g = ActuationGroup(**fl)
+        except ValueError as exc:
+            raise SceneFormatError(f"$.groups[{i}]", str(exc)) from exc
+        if g.label in groups:
+            raise SceneFormatError(f"$.groups[{i}]", f"duplicate actuation group {g.label!r}")
+        groups[g.label] = g
+    labels = list(groups)
+    group = None
+    if any(g is not None for g in glist):
+        group = np.full(s_count, -1, dtype=np.int32)
+        for idx, g in enumerate(glist):
+            if g is not None:
+                group[idx] = labels.index(g) if g in groups else -2      # -2: unknown, reported below
+    planes = [ContactPlane(**_expect(e, f"$.planes[{i}]", **_PLANE)) for i, e in enumerate(top["planes"])]
+    scene = ArrayScene(x=x, m=m, si=si, sj=sj, k=k, l0=l0, v=v, f_ext=f, fixed=fixed, gravity=top["gravity"],
+                       dt=top["dt"], damping=top["damping"], groups=groups, group=None, planes=planes,
+                       materials=mats)
+    if group is not None:
+        if (group == -2).any():
+            bad = int(np.flatnonzero(group == -2)[0])
+            raise SceneFormatError(f"$.springs[{bad}]", f"unknown actuation group {glist[bad]!r}")
+        scene.group = group
+    pair = np.sort(np.stack([si, sj], axis=1), axis=1)
+    if s_count and np.unique(pair, axis=0).shape[0] != s_count:
+        _, first = np.unique(pair, axis=0, return_index=True)
+        dup = sorted(set(range(s_count)) - set(first.tolist()))[0]
+        raise SceneFormatError(f"$.springs[{dup}]", f"duplicate spring between masses {si[dup]} and {sj[dup]}")
+    violations = validate_scene(scene)
+    if violations:
+        first = violations[0]
+        raise SceneFormatError(f"$.{first.where}", first.message)
+    return scene
+
+
+def save_scene(scene, path) -> None:
+    with open(path, "w") as fh:
+        fh.write(render_scene(scene))
+
+
+def load_scene(path) -> ArrayScene:
+    with open(path) as fh:
+        return parse_scene(fh.read())
