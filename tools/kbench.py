@@ -24,7 +24,7 @@ first = None
 for var in os.environ.get("VARIANTS", "once:3,once:2,step2").split(","):
     head, *extra = var.split("+")
     name, _, minb = head.partition(":")
-    for k in ("SS_DEBUG", "SS_ONCE_MINB", "SS_LEAN_MINB", "SS_TILE_DICT", "SS_TILE_SORT", "SS_PROF"):
+    for k in ("SS_DEBUG", "SS_ONCE_MINB", "SS_LEAN_MINB", "SS_TILE_DICT", "SS_TILE_SORT", "SS_PROF", "SS_PDL", "SS_KERNEL"):
         os.environ.pop(k, None)
     os.environ["SS_KERNEL"] = name
     if minb:
