@@ -137,23 +137,20 @@ template <bool GROUPS>
 __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const TileView &v, int l, const float4 &rm,
                                                   int n_own, int n_inc, V3<float> &s) {
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(v.bl + v.h->off_oo) + l;
-    const float4 *dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);
-    const float *dz = reinterpret_cast<const float *>(dict + v.h->n_dict);
-    const int8_t *dg = GROUPS && v.h->off_og ? reinterpret_cast<const int8_t *>(v.bl + v.h->off_og) : nullptr;
+    const float4 *dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);   // 2 float4 per entry
     float dmin = INFINITY;
     auto body = [&](int q) {
         const uint32_t e = inc[q << 8];
-        const uint32_t mi = e >> 10;
-        const float4 kd = dict[mi];                         // (k, k*l0, Dx, Dy)
+        const float4 *ent = dict + 2 * (e >> 10);
+        const float4 kd = ent[0];                           // (k, k*l0, Dx, Dy)
+        const float4 ez = ent[1];                           // (Dz, group bits, -, -)
         float kl0 = kd.y;
         if constexpr (GROUPS) {
-            if (dg) {
-                const int g = dg[mi];
-                if (g >= 0) kl0 = kl0 * p.scale[g];
-            }
+            const int g = __float_as_int(ez.y);
+            if (g >= 0) kl0 = kl0 * p.scale[g];
         }
         const float4 ro = v.sY[e & 0x3ffu];
-        const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = dz[mi] + (ro.z - rm.z);
+        const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = ez.x + (ro.z - rm.z);
         float d2;
         const float c = spring_c(dx, dy, dz_, kd.x, kl0, d2);
         dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
@@ -173,10 +170,10 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
     if (dmin < 1e-24f) {                                    // rare: count the degenerate own springs
         for (int r = 0; r < n_own; ++r) {
             const uint32_t e = inc[r << 8];
-            const uint32_t mi = e >> 10;
-            const float4 kd = dict[mi];
+            const float4 *ent = dict + 2 * (e >> 10);
+            const float4 kd = ent[0], ez = ent[1];
             const float4 ro = v.sY[e & 0x3ffu];
-            const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = dz[mi] + (ro.z - rm.z);
+            const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = ez.x + (ro.z - rm.z);
             const float d2 = __fmaf_rn(dz_, dz_, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
             deg += d2 < 1e-24f ? 1u : 0u;
         }

@@ -33,8 +33,9 @@ constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compa
 //    ONE incidence list -- its own springs first, then the springs it
 //    references -- of u16 = partner slot (10 bits) | dictionary index << 10;
 //    counts = n_own | n_inc << 8 (off_cnt), incidences at off_oo (W = max
-//    n_inc); dictionary float4 (k, k*l0, Dx, Dy)[n_dict] then float Dz at
-//    off_okl, int8 groups at off_og.  2 B per incidence, 4 B per spring.
+//    n_inc); dictionary of 32-byte entries at off_okl: float4 (k, k*l0, Dx,
+//    Dy), float4 (Dz, group as int32 bits (-1 passive), 0, 0); int8 groups
+//    also at off_og.  2 B per incidence, 4 B per spring.
 //  * explicit (canonical bit 1 clear): counts = n_own | n_ref << 8; own
 //    records (other u16 off_oo, then planar k, k*l0, Dx, Dy, Dz [W*256 each]
 //    at off_okl, grp i8 off_og); a spring whose owner lies in another tile is

@@ -259,7 +259,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             h.off_halo = off; off = al16(off + (uint32_t)halo_ids.size() * 4);
             h.off_cnt = off;  off = al16(off + kTile * 2);       // n_own | n_inc << 8
             h.off_oo = off;   off = al16(off + inc_n * 2);       // incidences
-            h.off_okl = off;  off = al16(off + D * 16 + D * 4);  // dictionary float4 (k, k*l0, Dx, Dy), then Dz
+            h.off_okl = off;  off = al16(off + D * 32);          // dictionary: float4 (k, k*l0, Dx, Dy), float4 (Dz, grp bits, 0, 0)
             h.off_og = 0;
             if (has_g) { h.off_og = off; off = al16(off + D); } // dictionary groups
             h.off_nf = h.off_ref = h.off_fo = h.off_fkl = h.off_fl = h.off_fg = 0;
@@ -270,11 +270,12 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             std::memcpy(blob.data() + h.off_halo, halo_ids.data(), halo_ids.size() * 4);
             for (const auto &kv : dict) {
                 const uint32_t e = kv.second;
-                put_at<float>(blob, h.off_okl + 16 * e, std::get<0>(kv.first));
-                put_at<float>(blob, h.off_okl + 16 * e + 4, std::get<1>(kv.first));
-                put_at<float>(blob, h.off_okl + 16 * e + 8, std::get<3>(kv.first));
-                put_at<float>(blob, h.off_okl + 16 * e + 12, std::get<4>(kv.first));
-                put_at<float>(blob, h.off_okl + 16 * D + 4 * e, std::get<5>(kv.first));
+                put_at<float>(blob, h.off_okl + 32 * e, std::get<0>(kv.first));
+                put_at<float>(blob, h.off_okl + 32 * e + 4, std::get<1>(kv.first));
+                put_at<float>(blob, h.off_okl + 32 * e + 8, std::get<3>(kv.first));
+                put_at<float>(blob, h.off_okl + 32 * e + 12, std::get<4>(kv.first));
+                put_at<float>(blob, h.off_okl + 32 * e + 16, std::get<5>(kv.first));
+                put_at<int32_t>(blob, h.off_okl + 32 * e + 20, (int32_t)std::get<2>(kv.first));
                 if (has_g) put_at<int8_t>(blob, h.off_og + e, (int8_t)std::get<2>(kv.first));
             }
             int64_t n_inc = 0;
