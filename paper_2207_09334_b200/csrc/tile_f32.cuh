@@ -206,10 +206,8 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
 // so the next grid's CTAs fill the SM slots freed during this grid's tail and
 // stream their (step-independent) record blobs by TMA before they wait for
 // this grid's positions (griddepcontrol.wait).
-template <int INTEG, bool GROUPS, int MINB = 5>
-__global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+template <int INTEG, bool GROUPS>
+__device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char *smem) {
     const Topology<float> &t = p.topo;
     const int l = threadIdx.x;
     const int m = blockIdx.x * kTile + l;
@@ -220,6 +218,10 @@ __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p)
     unsigned char *bl = smem + 128;
     float4 *sR = reinterpret_cast<float4 *>(bl + t.blob_smem);
     if (l == 0) {
+        if (p.reinit) {                                     // persistent kernel: re-arm completed barriers
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)));
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar + 1)));
+        }
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + 1)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -262,6 +264,27 @@ __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p)
         flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt >> 8, s));
     }
     tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
+}
+
+template <int INTEG, bool GROUPS, int MINB = 5>
+__global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    lean_body<INTEG, GROUPS>(p, smem);
+}
+
+// Persistent cooperative variant for small scenes (kernels.cuh persist_step_kernel).
+template <int INTEG, bool GROUPS>
+__global__ void __launch_bounds__(kTile) persist_lean_kernel(Params<float> p, PersistArgs<float> a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ Params<float> q;                             // this step's parameters, one copy per CTA
+    for (long long s = 0; s < a.count; ++s) {
+        if (threadIdx.x == 0) q = persist_params(p, a, s);
+        __syncthreads();
+        lean_body<INTEG, GROUPS>(q, smem);
+        grid_barrier();
+        if (*p.div_step <= a.step0 + s + 1) return;         // this or an earlier step diverged
+    }
 }
 
 }  // namespace ss
