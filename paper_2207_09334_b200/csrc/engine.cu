@@ -89,7 +89,6 @@ struct ss_engine {
     void *scale = nullptr;
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
-    unsigned long long *d_prof = nullptr;      // 16 phase-cycle counters (SS_PROF)
     void *pinned = nullptr;                    // page-locked staging for state transfers
     size_t pinned_bytes = 0;
     void *pinned2 = nullptr;                   // second staging buffer (x_prev = x - u)
@@ -367,7 +366,6 @@ Params<T> base_params(const ss_engine *h) {
         p.pfric[q] = (T)h->planes[6 * q + 5];
     }
     p.degenerate = h->d_degenerate;
-    p.prof = getenv("SS_PROF") ? h->d_prof : nullptr;
     p.div_step = h->d_div_step;
     p.div_mass = h->d_div_mass;
     if (const char *dbg = getenv("SS_DEBUG")) p.debug = atoi(dbg);   // timing experiments only
@@ -1038,8 +1036,6 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     int rc;
     if ((rc = h->alloc(&h->d_degenerate, sizeof(unsigned long long)))) return rc;
-    if ((rc = h->alloc(&h->d_prof, 16 * sizeof(unsigned long long)))) return rc;
-    CK(cudaMemsetAsync(h->d_prof, 0, 16 * sizeof(unsigned long long), h->stream));
     if ((rc = h->alloc(&h->d_div_step, sizeof(long long)))) return rc;
     if ((rc = h->alloc(&h->d_div_mass, sizeof(int)))) return rc;
     CK(cudaMemsetAsync(h->d_degenerate, 0, sizeof(unsigned long long), h->stream));
@@ -1494,14 +1490,6 @@ int ss_get_info(ss_engine *h, ss_info *info) {
 
 int64_t ss_launch_count(ss_engine *h) { return h ? h->launches : 0; }
 
-// Development aid (not part of the public header): the SS_PROF phase-cycle
-// counters of the tile kernels.
-int ss_debug_prof(ss_engine *h, unsigned long long *out16) {
-    if (!h || !out16) return ss::fail(SS_EINVAL, "ss_debug_prof: null argument");
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy(out16, h->d_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    return SS_OK;
-}
 
 }  // extern "C"
 

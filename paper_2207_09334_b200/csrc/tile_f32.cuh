@@ -29,34 +29,6 @@ namespace ss {
 
 // --------------------------------------------------------------- primitives
 
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-// arrive on an mbarrier when all of this thread's prior cp.async have landed
-// (counts as one of the barrier's expected arrivals)
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void named_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// SS_PROF phase timing: thread `who` adds the cycles since `t0` to slot i.
-__device__ __forceinline__ long long prof_clock() { return clock64(); }
-__device__ __forceinline__ void prof_add(const Params<float> &p, bool who, int i, long long &t0) {
-    if (p.prof && who) {
-        const long long t1 = clock64();
-        atomicAdd(p.prof + i, (unsigned long long)(t1 - t0));
-        t0 = t1;
-    }
-}
-
 __device__ __forceinline__ float rsqrt_ftz(float x) {
     float r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

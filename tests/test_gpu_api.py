@@ -316,3 +316,21 @@ def test_device_sampling_matches_host_sampling(integrator, precision):
             np.testing.assert_allclose(a.positions[i], b.positions[i], rtol=1e-14, atol=1e-16)
     np.testing.assert_allclose(a.energies, b.energies, rtol=1e-12, atol=1e-15)
     assert a.engine.n == b.engine.n
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("integrator", ["verlet", "euler"])
+def test_persistent_small_scene_stepping_is_bitwise_identical(precision, integrator, monkeypatch):
+    """The opt-in cooperative persistent stepping (SS_PERSIST=1) gives the
+    same bits as back-to-back launches, actuation and contact included."""
+    from paper_2207_09334_b200 import crawler_scene
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SS_PERSIST", flag)
+        eng = Engine(crawler_scene(), integrator=integrator, precision=precision)
+        eng.set_damping(2e-4)
+        eng.step(777)
+        out.append((eng.x.copy(), eng.v.copy(), eng.n))
+    assert out[0][0].tobytes() == out[1][0].tobytes()
+    assert out[0][1].tobytes() == out[1][1].tobytes()
+    assert out[0][2] == out[1][2] == 777

@@ -24,7 +24,7 @@ first = None
 for var in os.environ.get("VARIANTS", "once:3,once:2,step2").split(","):
     head, *extra = var.split("+")
     name, _, minb = head.partition(":")
-    for k in ("SS_DEBUG", "SS_ONCE_MINB", "SS_LEAN_MINB", "SS_TILE_DICT", "SS_TILE_SORT", "SS_PROF", "SS_PDL", "SS_KERNEL"):
+    for k in ("SS_DEBUG", "SS_ONCE_MINB", "SS_LEAN_MINB", "SS_TILE_DICT", "SS_TILE_SORT", "SS_PDL", "SS_KERNEL"):
         os.environ.pop(k, None)
     os.environ["SS_KERNEL"] = name
     if minb:
@@ -53,19 +53,5 @@ for var in os.environ.get("VARIANTS", "once:3,once:2,step2").split(","):
              springs_per_s=scene.spring_count / (us * 1e-6),
              algo_GBs=round(info["algorithmic_bytes_per_step"] / (us * 1e-6) / 1e9, 1),
              smem=info["smem_per_block"], rel_dev_vs_first=dev, launches=eng.launch_count)
-    if os.environ.get("SS_PROF"):
-        import ctypes
-        from paper_2207_09334_b200 import _lib
-        buf = (ctypes.c_ulonglong * 16)()
-        fn = _lib.lib().ss_debug_prof
-        fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
-        fn(eng._h, buf)
-        launches = eng.launch_count
-        names = ["p_wait_free", "p_issue_own", "p_wait_hdr", "p_issue_halo", "c_wait_states", "c_convert",
-                 "c_wait_records", "c_owner", "c_foreign", "c_barrier", "c_refs", "c_epilogue"]
-        # per launch, per CTA (148), consumers per group (2): microseconds at 1.965 GHz
-        prof = {nm: round(buf[i] / launches / 148 / (2 if nm.startswith("c_") else 1) / 1965.0, 2)
-                for i, nm in enumerate(names)}
-        r["prof_us_per_cta"] = prof
     print(json.dumps(r), flush=True)
     eng.close()
