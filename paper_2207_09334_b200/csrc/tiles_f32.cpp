@@ -185,7 +185,15 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
         // of one brick row) gather 8 distinct bank groups, in-tile or halo.
         std::vector<uint16_t> halo_slot(halo.size());
         std::vector<int32_t> halo_ids;            // per slot, -1 = hole
-        if (bank_aware) {
+        bool pad_ok = bank_aware;
+        if (pad_ok && use_dict) {                 // the compact format addresses <= 768 halo slots
+            uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (size_t i = 0; i < halo.size(); ++i) cnt[(uint32_t)zcell[L.orig_of[halo[i]]] & 7u]++;
+            uint32_t maxc = 0;
+            for (int r = 0; r < 8; ++r) maxc = std::max(maxc, cnt[r]);
+            pad_ok = kTile + 8 * maxc <= 1024;    // else: plain sorted halo for this tile
+        }
+        if (pad_ok) {
             uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             std::vector<uint32_t> cls(halo.size());
             for (size_t i = 0; i < halo.size(); ++i) {
