@@ -243,6 +243,32 @@ def run_single(args):
     h2d = 3 * N * vec
     d2h = N * vec
 
+    # configs[3] is a sweep "fp32 vs fp64 validation mode": the fp64 engine
+    # (bitwise equal to the reference) on the same cube, same timing rules
+    fp64 = None
+    if args.precision == "f32" and not args.no_fp64:
+        e64 = Engine(scene, integrator="verlet", precision="f64", layout=args.layout)
+        st64 = torch.cuda.ExternalStream(e64.stream_ptr, device=torch.device("cuda", 0))
+        for _ in range(3):
+            e64.step_async(sub)
+        e64.synchronize()
+        k64 = max(3, min(args.steps, 10))
+        a64 = torch.cuda.Event(enable_timing=True)
+        b64 = torch.cuda.Event(enable_timing=True)
+        a64.record(st64)
+        for _ in range(k64):
+            e64.step_async(sub)
+        b64.record(st64)
+        b64.synchronize()
+        e64.synchronize()
+        ms64 = a64.elapsed_time(b64)
+        inf64 = e64.info()
+        fp64 = {"value": S * sub * k64 / (ms64 / 1e3), "unit": "spring-updates/s", "steps": k64,
+                "ms_per_step": ms64 / k64, "dtype": "f64",
+                "roofline_frac": inf64["algorithmic_bytes_per_step"] / (ms64 / 1e3 / (k64 * sub)) / 1e9 / peak,
+                "note": "fp64 validation mode, bitwise equal to the reference's serial engine"}
+        e64.close()
+
     cpu = None
     if not args.no_cpu:
         cv, csteps, cwall, cthreads = cpu_sample(scene)
@@ -279,6 +305,7 @@ def run_single(args):
                               "algorithmic bytes; see DESIGN.md 4" % (info["tile_blob_bytes"],
                                                                       info["tile_blob_bytes"] / S))
                              if info.get("tile_kernel") == 2 else None},
+        "fp64_validation": fp64,
         "cpu_baseline": cpu,
         "e2e": {"value": S * sub * e2e_steps / e2e_wall, "unit": "spring-updates/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -299,6 +326,7 @@ def main():
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--layout", default="auto", choices=["auto", "csr", "ell"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 validation-mode measurement")
     ap.add_argument("--sharded", action="store_true",
                     help="run the x-slab sharded path even on one rank (400M cube by default)")
     args = ap.parse_args()

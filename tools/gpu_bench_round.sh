@@ -10,8 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_launch_bench.log 2>&1
+   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-fp64 > gpurun_out/ncu_launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-tile_lean} -s 30 -c 1 \
-   -o gpurun_out/prof python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
+   -o gpurun_out/prof python bench.py --steps 1 --warmup 3 --no-cpu --no-fp64 > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log
 cat gpurun_out/bench.log gpurun_out/bench_ref.log
