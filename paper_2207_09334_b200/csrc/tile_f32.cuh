@@ -251,7 +251,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
 }
 
-template <int INTEG, bool GROUPS, int MINB = 5>
+template <int INTEG, bool GROUPS, int MINB = 6>
 __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
