@@ -1,4 +1,5 @@
-// Host builder of the tiled incidence layout.
+// Host builder of the fp64 (bit-parity) tiled incidence layout;
+// fp32 builds are dispatched to tiles_f32.cpp.
 //
 // Masses are renumbered into 4x8x8 bricks of the lattice (generic scenes:
 // bricks of quantised coordinates), and consecutive runs of kTile=256 new
@@ -181,7 +182,7 @@ int build_tiles(const TileInput &in, TileLayout &L) {
     std::vector<uint32_t> tW(n_tiles), tWr(n_tiles), tH(n_tiles), tF(n_tiles), tSplit(n_tiles), tN(n_tiles);
     std::vector<int64_t> tRefs(n_tiles);
     const bool has_g = in.group != nullptr;
-    const size_t rs = in.f32 ? 4 : 8;
+    const size_t rs = 8;                   // fp64 records (fp32 builds: tiles_f32.cpp)
     int err = 0;
 
 #pragma omp parallel for schedule(dynamic, 16)
@@ -290,13 +291,8 @@ int build_tiles(const TileInput &in, TileLayout &L) {
                 const int32_t s = own_sp[q];
                 const uint32_t slot = ell_slot(l, (uint32_t)(q - own_ptr[m]), W, sl);
                 put<uint16_t>(blob, h.off_oo + 2 * slot, local_of(other_new[s]));
-                if (in.f32) {
-                    put<float>(blob, h.off_okl + 8 * slot, (float)in.k[s]);
-                    put<float>(blob, h.off_okl + 8 * slot + 4, (float)(in.k[s] * in.l0[s]));
-                } else {
-                    put<double>(blob, h.off_okl + 16 * slot, in.k[s]);
-                    put<double>(blob, h.off_okl + 16 * slot + 8, in.l0[s]);
-                }
+                put<double>(blob, h.off_okl + 16 * slot, in.k[s]);
+                put<double>(blob, h.off_okl + 16 * slot + 8, in.l0[s]);
                 if (has_g) put<int8_t>(blob, h.off_og + slot, (int8_t)in.group[s]);
             }
         }
@@ -304,13 +300,8 @@ int build_tiles(const TileInput &in, TileLayout &L) {
         for (uint32_t f = 0; f < nf; ++f) {
             const int32_t s = foreign[f];
             put<uint16_t>(blob, h.off_fo + 2 * f, local_of(owner_new[s]));
-            if (in.f32) {
-                put<float>(blob, h.off_fkl + 8 * f, (float)in.k[s]);
-                put<float>(blob, h.off_fkl + 8 * f + 4, (float)(in.k[s] * in.l0[s]));
-            } else {
-                put<double>(blob, h.off_fkl + 16 * f, in.k[s]);
-                put<double>(blob, h.off_fkl + 16 * f + 8, in.l0[s]);
-            }
+            put<double>(blob, h.off_fkl + 16 * f, in.k[s]);
+            put<double>(blob, h.off_fkl + 16 * f + 8, in.l0[s]);
             if (has_g) put<int8_t>(blob, h.off_fg + f, (int8_t)in.group[s]);
         }
         std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
