@@ -423,26 +423,29 @@ int halo_exchange_nccl(ss_engine *h) {
 
 // fp32 Euler/Verlet step on tiles: tile_lean_kernel in the compact or the
 // explicit record format (tile_f32.cuh).
-template <bool GROUPS>
-void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
-    auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
-    if (!h->pdl) {
-        k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
-        return;
-    }
-    // programmatic dependent launch: the next substep's CTAs may start (and
-    // prefetch their records) while this one drains (tile_f32.cuh)
+// Programmatic dependent launch: the kernel's CTAs may start (and prefetch
+// their tile records) while the previous kernel on the stream drains; the
+// kernel orders its state reads with griddepcontrol.wait.
+template <typename P>
+void launch_pdl(void (*k)(P), int grid, int block, size_t smem, cudaStream_t stream, const P &p) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTile);
-    cfg.dynamicSmemBytes = h->lean_smem;
-    cfg.stream = h->stream;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k, p);
+}
+
+template <bool GROUPS>
+void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
+    auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
+    if (h->pdl) launch_pdl(k, grid, kTile, h->lean_smem, h->stream, p);      // tile_f32.cuh
+    else k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
 }
 
 template <bool F32, int LAYOUT>
@@ -526,8 +529,11 @@ int launch_steps(ss_engine *h, int64_t count) {
                     goto launched;
                 }
             }
-            if (h->integrator == SS_EULER) step_kernel<F32, 0, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
-            else step_kernel<F32, 1, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            {
+                auto *k = h->integrator == SS_EULER ? step_kernel<F32, 0, LAYOUT> : step_kernel<F32, 1, LAYOUT>;
+                if (LAYOUT >= 3 && h->pdl) launch_pdl(k, grid, kBlock, smem, h->stream, p);
+                else k<<<grid, kBlock, smem, h->stream>>>(p);
+            }
         launched:
             h->launches += 1;
             h->cur ^= 1;
@@ -741,6 +747,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         // the attribute is a per-function permission shared by every engine in
         // the process: grant the device maximum, never a per-engine size
         if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
+        if (const char *e = getenv("SS_PDL")) h->pdl = atoi(e) != 0;
         if constexpr (F32) {
             // fp32 Euler/Verlet on compact tiles: tile_lean_kernel (tile_f32.cuh)
             // unless SS_KERNEL=step1 asks for kernels.cuh's step_kernel; the
@@ -750,7 +757,6 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
-                if (const char *e = getenv("SS_PDL")) h->pdl = atoi(e) != 0;
                 const int b = dev_max;
                 for (auto *kk : {tile_lean_kernel<0, false>, tile_lean_kernel<1, false>, tile_lean_kernel<0, true>,
                                  tile_lean_kernel<1, true>})

@@ -23,8 +23,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <tuple>
 
 #include "common.h"
 #include "springsim_b200.h"
@@ -127,8 +129,172 @@ void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 
 }  // namespace
 
+// fp64 compact format (tiles.h): one incidence list per mass in ascending
+// spring id -- the reference's serial summation order for every mass, no
+// canonical-order condition -- of u16 = partner slot | dictionary index << 10
+// over a per-tile dictionary of distinct (k, l0, group).  SS_EAGAIN_DICT when
+// a tile does not fit (more than 64 dictionary entries, more than 768 halo
+// slots, a mass of degree > 255, a self spring).
+int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
+    const int64_t N = in.N, S = in.S;
+    if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
+    for (int64_t s = 0; s < S; ++s)
+        if (in.si[s] == in.sj[s]) return SS_EAGAIN_DICT;
+    L = TileLayout{};
+    tile_order(in, L.orig_of);
+    const int64_t D = (int64_t)L.orig_of.size();
+    L.new_of.assign(N, -1);
+    for (int64_t i = 0; i < D; ++i)
+        if (L.orig_of[i] >= 0) L.new_of[L.orig_of[i]] = (int32_t)i;
+    // incidences per device slot, ascending spring id
+    std::vector<int64_t> ptr(D + 1, 0);
+    for (int64_t s = 0; s < S; ++s) {
+        ptr[L.new_of[in.si[s]] + 1]++;
+        ptr[L.new_of[in.sj[s]] + 1]++;
+    }
+    for (int64_t m = 0; m < D; ++m) ptr[m + 1] += ptr[m];
+    std::vector<int32_t> inc_s((size_t)2 * S), inc_o((size_t)2 * S);
+    {
+        std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+        for (int64_t s = 0; s < S; ++s) {
+            const int32_t a = L.new_of[in.si[s]], b = L.new_of[in.sj[s]];
+            inc_s[fill[a]] = (int32_t)s;
+            inc_o[fill[a]++] = b;
+            inc_s[fill[b]] = (int32_t)s;
+            inc_o[fill[b]++] = a;
+        }
+    }
+    const int64_t n_tiles = D / kTile;
+    L.n_tiles = n_tiles;
+    std::vector<std::vector<uint8_t>> parts(n_tiles);
+    std::vector<uint32_t> tW(n_tiles), tH(n_tiles), tSplit(n_tiles), tN(n_tiles);
+    std::vector<double> tRatio(n_tiles);
+    const bool has_g = in.group != nullptr;
+    int err = 0;
+
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        if (err) continue;
+        const int64_t base = t * kTile;
+        int n = 0;
+        while (n < kTile && L.orig_of[base + n] >= 0) ++n;
+        uint32_t W = 1;
+        std::vector<int32_t> halo;
+        for (int l = 0; l < n; ++l) {
+            const int64_t m = base + l;
+            W = std::max<uint32_t>(W, (uint32_t)(ptr[m + 1] - ptr[m]));
+            for (int64_t q = ptr[m]; q < ptr[m + 1]; ++q)
+                if (inc_o[q] < base || inc_o[q] >= base + n) halo.push_back(inc_o[q]);
+        }
+        std::sort(halo.begin(), halo.end());
+        halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+        if (W > 255 || halo.size() > 768) {
+#pragma omp atomic write
+            err = 3;
+            continue;
+        }
+        // dictionary of distinct (k, l0, group), in first-use order
+        std::vector<std::tuple<uint64_t, uint64_t, int32_t>> keys;
+        std::vector<uint16_t> incs((size_t)W * kTile, 0);
+        bool fits = true;
+        for (int l = 0; l < n && fits; ++l) {
+            const int64_t m = base + l;
+            for (int64_t q = ptr[m]; q < ptr[m + 1]; ++q) {
+                const int32_t s = inc_s[q], o = inc_o[q];
+                uint64_t kb, lb;
+                std::memcpy(&kb, &in.k[s], 8);
+                std::memcpy(&lb, &in.l0[s], 8);
+                const auto key = std::make_tuple(kb, lb, has_g ? in.group[s] : -1);
+                size_t di = 0;
+                while (di < keys.size() && keys[di] != key) ++di;
+                if (di == keys.size()) {
+                    if (keys.size() == 64) { fits = false; break; }
+                    keys.push_back(key);
+                }
+                const uint32_t slot = (o >= base && o < base + n)
+                                          ? (uint32_t)(o - base)
+                                          : (uint32_t)(kTile + (std::lower_bound(halo.begin(), halo.end(), o) -
+                                                                halo.begin()));
+                incs[(size_t)(q - ptr[m]) * kTile + l] = (uint16_t)(slot | (di << 10));
+            }
+        }
+        if (!fits) {
+#pragma omp atomic write
+            err = 3;
+            continue;
+        }
+        const uint32_t nd = (uint32_t)keys.size();
+        TileHdr h{};
+        h.n = n; h.W = W; h.Wr = W; h.n_halo = (uint32_t)halo.size();
+        h.canonical = 1u | 2u;                 // bit 1: compact format
+        h.slice_log2 = 8;
+        h.n_dict = nd;
+        uint32_t off = align16(sizeof(TileHdr));
+        h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
+        h.off_cnt = off;  off = align16(off + kTile * 2);
+        h.off_oo = off;   off = align16(off + W * kTile * 2);
+        h.off_okl = off;  off = align16(off + nd * 16);
+        h.off_og = 0;
+        if (has_g) { h.off_og = off; off = align16(off + nd); }
+        h.off_ref = h.off_fo = h.off_fkl = h.off_fg = 0;
+        h.bytes = off;
+        std::vector<uint8_t> &blob = parts[t];
+        blob.assign(off, 0);
+        std::memcpy(blob.data(), &h, sizeof h);
+        std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
+        for (int l = 0; l < n; ++l)
+            put<uint16_t>(blob, h.off_cnt + 2 * l, (uint16_t)((ptr[base + l + 1] - ptr[base + l]) << 8));
+        std::memcpy(blob.data() + h.off_oo, incs.data(), incs.size() * 2);
+        for (uint32_t d = 0; d < nd; ++d) {
+            uint64_t kb = std::get<0>(keys[d]), lb = std::get<1>(keys[d]);
+            std::memcpy(blob.data() + h.off_okl + 16 * d, &kb, 8);
+            std::memcpy(blob.data() + h.off_okl + 16 * d + 8, &lb, 8);
+            if (has_g) put<int8_t>(blob, h.off_og + d, (int8_t)std::get<2>(keys[d]));
+        }
+        tW[t] = W; tH[t] = (uint32_t)halo.size(); tN[t] = n;
+        tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);
+        tRatio[t] = (double)(n + halo.size()) / n;
+    }
+    if (err) return SS_EAGAIN_DICT;
+    if (in.group) {
+        for (int64_t s = 0; s < S; ++s)
+            if (in.group[s] > 127) return fail(SS_EINVAL, "at most 128 actuation groups in the tiled layout");
+    }
+    L.canonical = true;
+    L.compact = true;
+    L.split = tSplit;
+    L.off.assign(n_tiles + 1, 0);
+    for (int64_t t = 0; t < n_tiles; ++t) L.off[t + 1] = L.off[t] + parts[t].size();
+    L.blob.resize(L.off[n_tiles]);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n_tiles; ++t)
+        std::memcpy(L.blob.data() + L.off[t], parts[t].data(), parts[t].size());
+    double hsum = 0;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        L.max_tile_bytes = std::max<uint32_t>(L.max_tile_bytes, (uint32_t)parts[t].size());
+        L.max_tile_smem = L.max_tile_bytes;
+        const uint32_t head = tSplit[t] & 0xffffffu;
+        L.max_head_bytes = std::max<uint32_t>(L.max_head_bytes, head);
+        L.max_rest_bytes = std::max<uint32_t>(L.max_rest_bytes, (uint32_t)parts[t].size() - head);
+        L.max_halo = std::max(L.max_halo, tH[t]);
+        L.max_W = std::max<int>(L.max_W, (int)tW[t]);
+        L.max_Wr = L.max_W;
+        hsum += tRatio[t];
+    }
+    L.halo_ratio = hsum / (double)n_tiles;
+    L.foreign_frac = 0.0;
+    return SS_OK;
+}
+
 int build_tiles(const TileInput &in, TileLayout &L) {
     if (in.f32) return build_tiles_f32(in, L);
+    {
+        const char *env = getenv("SS_TILE_DICT");     // 0: the explicit fp64 format
+        if (!env || atoi(env) != 0) {
+            const int rc = build_tiles_f64_compact(in, L);
+            if (rc != SS_EAGAIN_DICT) return rc;
+        }
+    }
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
