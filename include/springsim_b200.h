@@ -174,7 +174,7 @@ typedef struct ss_info {
     int64_t tile_blob_bytes;   /* TILE: bytes of records streamed per step */
     double  tile_halo_ratio;   /* TILE: mean (tile + halo masses) / tile masses */
     double  tile_foreign_frac; /* TILE: fraction of references whose owner is in another tile */
-    int32_t tile_kernel;       /* fp32 Euler/Verlet tile kernel: 0 step_kernel, 1 explicit records, 2 compact records */
+    int32_t tile_kernel;       /* tile record format: fp32 1 explicit, 2 compact (0: step_kernel); fp64 0 explicit, 3 compact */
     int32_t kernel_smem;       /* its dynamic shared memory per CTA */
 } ss_info;
 int ss_get_info(ss_engine *h, ss_info *info);

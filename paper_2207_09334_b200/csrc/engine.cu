@@ -1484,7 +1484,7 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
-        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1) : 0;
+        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1) : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
         info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->smem_bytes);
     } else {
         info->ell_width_own = h->lay.W;
@@ -1530,7 +1530,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     info->kernel_smem = info->smem_per_block;
-    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : 0;
+    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : (tl.compact ? 3 : 0);
     return SS_OK;
 }
 

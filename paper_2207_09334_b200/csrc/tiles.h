@@ -13,7 +13,15 @@ constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compa
 // [0, off_cnt) (header + halo ids) is copied first so the halo gather
 // overlaps the record stream.
 //
-// fp64 builds (bit parity, tiles.cpp build_tiles): 32-wide ELL slices.
+// fp64 compact builds (bit parity, the default; tiles.cpp
+// build_tiles_f64_compact): canonical bit 1 set, one 256-wide ELL slice.
+//   header | halo ids | counts (n_inc << 8) | incidences u16 at off_oo,
+//   slot q*256 + l, = partner slot (10 bits) | dictionary index << 10, in
+//   ascending spring id (the reference's serial order for every mass) |
+//   dictionary of n_dict (k, l0) double pairs at off_okl | int8 groups at
+//   off_og.
+//
+// fp64 explicit builds (the fallback; tiles.cpp build_tiles): 32-wide ELL slices.
 //   Section order: header | halo ids | counts | own other | own (k,l0) |
 //   own grp | refs | foreign owner | foreign (k,l0) | foreign grp.
 //   counts: n_own | n_ref << 8.  A mass sums references then own records,

@@ -146,6 +146,24 @@ def test_tile_plan_statistics_on_host():
     assert ragged["smem_per_block"] <= 76 * 1024
 
 
+def test_fp64_compact_tile_plan_on_host(monkeypatch):
+    """fp64 tiles use the compact format (spring-id ordered incidence lists
+    over a per-tile (k, l0, group) dictionary) when every tile has at most 64
+    distinct records; a tile with more falls back to the explicit format, and
+    SS_TILE_DICT=0 forces it."""
+    from paper_2207_09334_b200.engine import plan
+    cube = L.block_scene(15)
+    info = plan(cube, precision="f64")
+    assert info["tile_kernel"] == 3
+    assert info["tile_foreign_frac"] == 0.0
+    assert info["smem_per_block"] <= 40 * 1024
+    rnd = L.block_scene(15)
+    rnd.k = rnd.k * (1.0 + 1e-6 * np.arange(rnd.k.size))    # every spring distinct
+    assert plan(rnd, precision="f64")["tile_kernel"] == 0
+    monkeypatch.setenv("SS_TILE_DICT", "0")
+    assert plan(cube, precision="f64")["tile_kernel"] == 0
+
+
 def test_engine_without_gpu_fails_loudly():
     """No CPU fallback: on a host without a device, construction raises."""
     if _lib.device_count() > 0:
