@@ -89,10 +89,11 @@ struct ss_engine {
     void *scale = nullptr;
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
-    void *pinned = nullptr;                    // page-locked staging for state transfers
-    size_t pinned_bytes = 0;
-    void *pinned2 = nullptr;                   // second staging buffer (x_prev = x - u)
-    size_t pinned2_bytes = 0;
+    void *pinned[3] = {nullptr, nullptr, nullptr};   // page-locked staging for state transfers
+    size_t pinned_bytes[3] = {0, 0, 0};
+    cudaEvent_t staged = nullptr;              // recorded after asynchronous uploads from `pinned`
+    cudaEvent_t chunk_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // chunked downloads
+    bool staged_pending = false;
     // on-device sampling (ss_energy_setup / ss_step_sampled)
     int *d_ssi = nullptr, *d_ssj = nullptr, *d_sgrp = nullptr;
     double *d_sk = nullptr, *d_sl0 = nullptr, *d_smass = nullptr, *d_sx0 = nullptr;
@@ -140,8 +141,12 @@ struct ss_engine {
             if (const NcclApi *api = nccl_api()) api->commDestroy(nccl);
         }
         for (auto &b : bufs) cudaFree(b.p);
-        if (pinned) cudaFreeHost(pinned);
-        if (pinned2) cudaFreeHost(pinned2);
+        if (stream) cudaStreamSynchronize(stream);
+        for (void *b : pinned)
+            if (b) cudaFreeHost(b);
+        if (staged) cudaEventDestroy(staged);
+        for (cudaEvent_t e : chunk_ev)
+            if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -221,9 +226,9 @@ void pack_vec(const ss_engine *h, const double *v, T4 *out) {
 }
 
 template <typename T, typename T4>
-void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
+void unpack_positions(const ss_engine *h, const T4 *in, double *x, int64_t i0, int64_t i1) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->ND; ++i) {
+    for (int64_t i = i0; i < i1; ++i) {
         const int64_t s = h->src_of(i);
         if (s < 0) continue;
         if constexpr (std::is_same<T, float>::value) {
@@ -247,9 +252,9 @@ void unpack_positions(const ss_engine *h, const T4 *in, double *x) {
 }
 
 template <typename T, typename T4>
-void unpack_vec(const ss_engine *h, const T4 *in, double *v) {
+void unpack_vec(const ss_engine *h, const T4 *in, double *v, int64_t i0, int64_t i1) {
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < h->ND; ++i) {
+    for (int64_t i = i0; i < i1; ++i) {
         const int64_t s = h->src_of(i);
         if (s < 0) continue;
         v[3 * s + 0] = (double)in[i].x;
@@ -266,6 +271,30 @@ int upload(ss_engine *h, void *dst, const void *src, size_t bytes) {
 int download(ss_engine *h, void *dst, const void *src, size_t bytes) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    return SS_OK;
+}
+
+// Device state vector src (ND slots) -> pinned dst in chunks, each chunk
+// handed to `consume(i0, i1)` (the unpacking loop) as soon as it has
+// landed, while the next chunks are still crossing the bus.
+template <typename T4, typename Fn>
+int download_overlapped(ss_engine *h, T4 *dst, const void *src, Fn &&consume) {
+    constexpr int kChunks = 4;
+    const int64_t ND = h->ND;
+    if (!h->chunk_ev[0])
+        for (auto &e : h->chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int64_t lo[kChunks + 1];
+    for (int c = 0; c <= kChunks; ++c) lo[c] = ND * c / kChunks;
+    for (int c = 0; c < kChunks; ++c) {
+        const size_t n = (size_t)(lo[c + 1] - lo[c]);
+        if (n) CK(cudaMemcpyAsync(dst + lo[c], reinterpret_cast<const T4 *>(src) + lo[c], n * sizeof(T4),
+                                  cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaEventRecord(h->chunk_ev[c], h->stream));
+    }
+    for (int c = 0; c < kChunks; ++c) {
+        CK(cudaEventSynchronize(h->chunk_ev[c]));
+        consume(lo[c], lo[c + 1]);
+    }
     return SS_OK;
 }
 
@@ -855,14 +884,20 @@ int forces_impl(ss_engine *h, const double *x, const double *v, double t) {
     });
 }
 
-// Page-locked staging buffer for one (ND) state vector, kept for the
-// engine's lifetime: transfers run at full PCIe/C2C speed and the packing
-// loop never page-faults a fresh allocation.
+// Page-locked staging buffer `which` (0-2) for one (ND) state vector, kept
+// for the engine's lifetime: transfers run at full PCIe/C2C speed and the
+// packing loop never page-faults a fresh allocation.  Uploads from these
+// buffers are asynchronous (set_state_impl); a buffer is handed out for
+// host writes only after they have completed.
 template <typename T4>
 int staging(ss_engine *h, T4 **out, int which = 0) {
     const size_t bytes = (size_t)h->ND * sizeof(T4);
-    void *&buf = which ? h->pinned2 : h->pinned;
-    size_t &have = which ? h->pinned2_bytes : h->pinned_bytes;
+    if (h->staged_pending) {
+        CK(cudaEventSynchronize(h->staged));
+        h->staged_pending = false;
+    }
+    void *&buf = h->pinned[which];
+    size_t &have = h->pinned_bytes[which];
     if (have < bytes) {
         if (buf) cudaFreeHost(buf);
         buf = nullptr;
@@ -883,12 +918,16 @@ int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     if (rc) return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);
     if (x) {
-        if ((rc = download(h, tmp, h->X[h->cur], bytes))) return rc;
-        unpack_positions<T, T4>(h, tmp, x);
+        if ((rc = download_overlapped(h, tmp, h->X[h->cur], [&](int64_t i0, int64_t i1) {
+                 unpack_positions<T, T4>(h, tmp, x, i0, i1);
+             })))
+            return rc;
     }
     if (v) {
-        if ((rc = download(h, tmp, h->V, bytes))) return rc;
-        unpack_vec<T, T4>(h, tmp, v);
+        if ((rc = download_overlapped(h, tmp, h->V, [&](int64_t i0, int64_t i1) {
+                 unpack_vec<T, T4>(h, tmp, v, i0, i1);
+             })))
+            return rc;
     }
     if (x_prev && h->has_prev) {
         if (F32 && h->U) {                        // x_prev = x - u, in fp64
@@ -908,8 +947,10 @@ int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
                 }
             }
         } else {
-            if ((rc = download(h, tmp, h->X[h->cur ^ 1], bytes))) return rc;
-            unpack_positions<T, T4>(h, tmp, x_prev);
+            if ((rc = download_overlapped(h, tmp, h->X[h->cur ^ 1], [&](int64_t i0, int64_t i1) {
+                     unpack_positions<T, T4>(h, tmp, x_prev, i0, i1);
+                 })))
+                return rc;
         }
     }
     return SS_OK;
@@ -927,17 +968,27 @@ int set_state_impl(ss_engine *h, const double *x, const double *v, const double 
         if (r0) return r0;
         x_prev = keep_prev.data();
     }
-    T4 *tmp;
-    int rc = staging<T4>(h, &tmp);
-    if (rc) return rc;
+    // each vector is packed into its own staging buffer and its upload is
+    // queued at once, so packing the next vector overlaps the DMA of the
+    // previous one; the stream orders the uploads before the next step
+    T4 *bx, *bv, *tmp;
+    int rc;
+    if ((rc = staging<T4>(h, &bx, 0)) || (rc = staging<T4>(h, &bv, 1)) || (rc = staging<T4>(h, &tmp, 2)))
+        return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);
+    auto upload_async = [&](void *dst, const void *src) -> int {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaEventRecord(h->staged, h->stream));
+        h->staged_pending = true;
+        return SS_OK;
+    };
     if (x) {
-        pack_positions<T, T4>(h, x, tmp);
-        if ((rc = upload(h, h->X[h->cur], tmp, bytes))) return rc;
+        pack_positions<T, T4>(h, x, bx);
+        if ((rc = upload_async(h->X[h->cur], bx))) return rc;
     }
     if (v) {
-        pack_vec<T, T4>(h, v, tmp);
-        if ((rc = upload(h, h->V, tmp, bytes))) return rc;
+        pack_vec<T, T4>(h, v, bv);
+        if ((rc = upload_async(h->V, bv))) return rc;
     }
     if (x_prev) {
         if (F32 && h->U) {                        // u = x - x_prev, in fp64 then rounded once
@@ -947,6 +998,7 @@ int set_state_impl(ss_engine *h, const double *x, const double *v, const double 
                 xc.resize((size_t)h->N * 3);
                 if ((rc = get_state_impl<F32>(h, xc.data(), nullptr, nullptr))) return rc;
                 xs = xc.data();
+                if ((rc = staging<T4>(h, &tmp, 2))) return rc;
             }
 #pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < h->ND; ++i) {
@@ -959,10 +1011,10 @@ int set_state_impl(ss_engine *h, const double *x, const double *v, const double 
                 }
                 tmp[i] = o;
             }
-            if ((rc = upload(h, h->U, tmp, bytes))) return rc;
+            if ((rc = upload_async(h->U, tmp))) return rc;
         } else {
             pack_positions<T, T4>(h, x_prev, tmp);
-            if ((rc = upload(h, h->X[h->cur ^ 1], tmp, bytes))) return rc;
+            if ((rc = upload_async(h->X[h->cur ^ 1], tmp))) return rc;
         }
         h->has_prev = true;
     }
@@ -1040,6 +1092,7 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
 
     CK(cudaSetDevice(h->device));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->staged, cudaEventDisableTiming));
     int rc;
     if ((rc = h->alloc(&h->d_degenerate, sizeof(unsigned long long)))) return rc;
     if ((rc = h->alloc(&h->d_div_step, sizeof(long long)))) return rc;

@@ -281,13 +281,14 @@ class Engine:
         _lib.check(_lib.lib().ss_get_info(self._h, C.byref(inf)), "ss_get_info")
         return {f: getattr(inf, f) for f, _ in _lib.Info._fields_}
 
-    def _download(self) -> None:
-        """Refresh stale host mirrors of x / v / x_prev."""
+    def _download(self, which: str) -> None:
+        """Refresh the host mirror ``which`` ("x", "v" or "x_prev") if stale;
+        only that one crosses the bus."""
         lib = _lib.lib()
         n = self.mass_count
-        need_x = self._x.stale
-        need_v = self._v.stale
-        need_p = self._xp.stale and self.integrator == VERLET
+        need_x = which == "x" and self._x.stale
+        need_v = which == "v" and self._v.stale
+        need_p = which == "x_prev" and self._xp.stale and self.integrator == VERLET
         if not (need_x or need_v or need_p):
             return
         has_prev = C.c_int(0)
@@ -357,7 +358,7 @@ class Engine:
 
     @property
     def x(self) -> np.ndarray:
-        self._download()
+        self._download("x")
         self._x.lent = True
         return self._x.arr
 
@@ -370,7 +371,7 @@ class Engine:
 
     @property
     def v(self) -> np.ndarray:
-        self._download()
+        self._download("v")
         self._v.lent = True
         return self._v.arr
 
@@ -383,7 +384,7 @@ class Engine:
     def x_prev(self):
         if self.integrator != VERLET:
             return self._host_prev_nonverlet
-        self._download()
+        self._download("x_prev")
         self._xp.lent = True
         return self._xp.arr
 

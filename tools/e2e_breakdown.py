@@ -29,3 +29,19 @@ def api():
     eng.x = x; eng.v = v; eng.x_prev = xp; eng.step(100); _ = eng.x
 res["api_e2e_ms"] = t(api)
 print(res, flush=True)
+
+# the public-API step, piece by piece
+def piece(name, f, acc):
+    a = time.perf_counter(); f(); acc[name] = acc.get(name, 0.0) + time.perf_counter() - a
+acc = {}
+reps = 5
+for _ in range(reps):
+    eng.x = x; eng.v = v; eng.x_prev = xp
+    piece("drain", eng.drain_commands, acc)
+    piece("upload_lent", eng._upload_lent, acc)
+    piece("push_params", eng._push_params, acc)
+    res = _lib.StepResult()
+    piece("ss_step", lambda: lib.ss_step(eng._h, 100, C.byref(res)), acc)
+    eng._mark_stepped()
+    piece("get_x", lambda: eng.x, acc)
+print({k: round(1e3 * v / reps, 3) for k, v in acc.items()}, flush=True)
