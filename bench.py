@@ -229,15 +229,26 @@ def run_single(args):
     x_host = eng.x.copy()
     v_host = eng.v.copy()
     xp_host = eng.x_prev.copy()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(2, min(args.steps, 10))
+    for _ in range(max(1, min(args.warmup, 2))):          # untimed: staging buffers, events
+        eng.x = x_host
+        eng.v = v_host
+        eng.x_prev = xp_host
+        eng.step(sub)
+        _ = eng.x
     t0 = time.perf_counter()
+    marks = []
     for _ in range(e2e_steps):
         eng.x = x_host
         eng.v = v_host
         eng.x_prev = xp_host
         eng.step(sub)
         out = eng.x
+        marks.append(time.perf_counter())
     e2e_wall = time.perf_counter() - t0
+    if os.environ.get("BENCH_E2E_DEBUG"):
+        print("e2e ms per step:", [round(1e3 * (b - a), 2) for a, b in zip([t0] + marks[:-1], marks)],
+              file=sys.stderr)
     _ = out
     vec = 16 if args.precision == "f32" else 32
     h2d = 3 * N * vec
