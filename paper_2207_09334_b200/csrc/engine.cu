@@ -134,9 +134,20 @@ struct ss_engine {
     ncclComm_t nccl = nullptr;
     int nccl_peer[2] = {-1, -1};
     int64_t halo_exchanges = 0;
+    // peer-memory transport (halo.cuh): own mailbox, the neighbours' (IPC-mapped
+    // or, for shards of one process, plain) mailboxes and their plane sizes
+    void *mailbox = nullptr;
+    void *peer_mailbox[2] = {nullptr, nullptr};
+    bool peer_ipc[2] = {false, false};
+    int64_t peer_n_recv[2][2] = {{0, 0}, {0, 0}};
+    bool p2p_on = false;
+    bool group_mode = false;       // ss_step_group orders the exchange itself
 
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (int s = 0; s < 2; ++s)
+            if (peer_ipc[s] && peer_mailbox[s]) cudaIpcCloseMemHandle(peer_mailbox[s]);
         if (nccl) {
             if (const NcclApi *api = nccl_api()) api->commDestroy(nccl);
         }
@@ -416,6 +427,65 @@ int with_layout(const ss_engine *h, Fn &&fn) {
 // After a substep: pack the boundary planes of the new positions, exchange
 // them with the neighbouring ranks (NCCL send/recv on the engine stream) and
 // write the received planes into the halo slots.
+// Byte offset of side `side`, parity `par` plane buffer in a mailbox whose
+// owner receives n_recv[0] / n_recv[1] masses from its lower / upper side.
+inline size_t mailbox_plane(const int64_t n_recv[2], int side, int par, size_t vec) {
+    size_t off = kMailboxHead;
+    if (side == 1) off += 2 * (size_t)n_recv[0] * vec;
+    return off + (size_t)par * (size_t)n_recv[side] * vec;
+}
+
+template <typename T4>
+int p2p_push(ss_engine *h, long long step) {
+    PushArgs<T4> a{};
+    a.X = reinterpret_cast<const T4 *>(h->X[h->cur]);
+    int blocks[2] = {0, 0};
+    for (int s = 0; s < 2; ++s) {
+        if (!h->peer_mailbox[s]) continue;
+        unsigned char *pm = reinterpret_cast<unsigned char *>(h->peer_mailbox[s]);
+        const int ps = 1 - s;                               // the neighbour receives on its other side
+        a.send_idx[s] = h->halo_send_idx[s];
+        a.n_send[s] = h->halo_n_send[s];
+        a.peer_buf[s] = reinterpret_cast<T4 *>(pm + mailbox_plane(h->peer_n_recv[s], ps, (int)(step & 1), sizeof(T4)));
+        a.peer_flag[s] = &reinterpret_cast<MailboxHead *>(pm)->flag[ps];
+        a.counter[s] = &reinterpret_cast<MailboxHead *>(h->mailbox)->counter[s];
+        blocks[s] = std::max(1, (h->halo_n_send[s] + 255) / 256);
+    }
+    a.blocks0 = blocks[0];
+    a.step = step;
+    if (blocks[0] + blocks[1] == 0) return SS_OK;
+    halo_push_kernel<T4><<<blocks[0] + blocks[1], 256, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    h->launches += 1;
+    return SS_OK;
+}
+
+template <typename T4>
+int p2p_land(ss_engine *h, long long step) {
+    LandArgs<T4> a{};
+    a.X = reinterpret_cast<T4 *>(h->X[h->cur]);
+    unsigned char *mb = reinterpret_cast<unsigned char *>(h->mailbox);
+    const int64_t nr[2] = {h->halo_n_recv[0], h->halo_n_recv[1]};
+    int blocks[2] = {0, 0};
+    for (int s = 0; s < 2; ++s) {
+        if (!h->peer_mailbox[s]) continue;
+        a.recv_idx[s] = h->halo_recv_idx[s];
+        a.n_recv[s] = h->halo_n_recv[s];
+        a.buf[s] = reinterpret_cast<const T4 *>(mb + mailbox_plane(nr, s, (int)(step & 1), sizeof(T4)));
+        a.flag[s] = &reinterpret_cast<MailboxHead *>(mb)->flag[s];
+        blocks[s] = std::max(1, (h->halo_n_recv[s] + 255) / 256);
+    }
+    a.error = &reinterpret_cast<MailboxHead *>(mb)->error;
+    a.blocks0 = blocks[0];
+    a.step = step;
+    if (blocks[0] + blocks[1] == 0) return SS_OK;
+    halo_land_kernel<T4><<<blocks[0] + blocks[1], 256, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    h->launches += 1;
+    h->halo_exchanges += 1;
+    return SS_OK;
+}
+
 template <typename T4>
 int halo_exchange_nccl(ss_engine *h) {
     const NcclApi *api = nccl_api();
@@ -493,7 +563,7 @@ int launch_steps(ss_engine *h, int64_t count) {
     const size_t smem = LAYOUT >= 3 ? h->smem_bytes : 0;
     Params<T> p = base_params<T>(h);
     const T *scale = reinterpret_cast<const T *>(h->scale);
-    if (h->integrator != SS_RK4 && !h->nccl && count >= 2 && h->persist_max_grid >= grid) {
+    if (h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2 && h->persist_max_grid >= grid) {
         // small scene: one cooperative launch steps the whole batch
         // (kernels.cuh persist_step_kernel / tile_f32.cuh persist_lean_kernel)
         PersistArgs<T> a{};
@@ -570,6 +640,10 @@ int launch_steps(ss_engine *h, int64_t count) {
             if (h->nccl) {                                   // boundary planes -> neighbours' halos
                 int rc = halo_exchange_nccl<T4>(h);
                 if (rc) return rc;
+            } else if (h->p2p_on && !h->group_mode) {        // ... over peer memory (halo.cuh)
+                int rc = p2p_push<T4>(h, p.step);
+                if (!rc) rc = p2p_land<T4>(h, p.step);
+                if (rc) return rc;
             }
         } else {
             T4 *XA = reinterpret_cast<T4 *>(h->XA), *XB = reinterpret_cast<T4 *>(h->XB);
@@ -635,6 +709,11 @@ int reset_divergence(ss_engine *h) {
 // After an enqueued batch: read the divergence record, fix up n/t/cur.
 int finish_batch(ss_engine *h, int64_t count, int64_t n0, int cur0, ss_step_result *res) {
     CK(cudaStreamSynchronize(h->stream));
+    if (h->p2p_on) {
+        int err = 0;
+        CK(cudaMemcpy(&err, &reinterpret_cast<MailboxHead *>(h->mailbox)->error, sizeof err, cudaMemcpyDeviceToHost));
+        if (err) return ss::fail(SS_ECUDA, "halo exchange: a neighbour did not publish its boundary planes within 20 s");
+    }
     long long dstep = LLONG_MAX;
     int dmass = INT_MAX;
     CK(cudaMemcpy(&dstep, h->d_div_step, sizeof dstep, cudaMemcpyDeviceToHost));
@@ -1662,6 +1741,115 @@ extern "C" int ss_halo_nccl(ss_engine *h, const unsigned char id[128], int nrank
     return SS_OK;
 }
 
+// ------------------------------------------------ peer-memory halo transport
+
+namespace {
+
+constexpr char kMailboxMagic[8] = {'S', 'S', 'M', 'B', 'O', 'X', '0', '1'};
+
+struct MailboxBlob {               // what ss_halo_p2p_export hands to the neighbours (256 B)
+    char magic[8];
+    cudaIpcMemHandle_t handle;     // 64 B
+    int64_t n_recv[2];
+    int64_t vec;
+    int64_t n;
+    int32_t cur;
+    int32_t device;
+};
+static_assert(sizeof(MailboxBlob) <= 256, "mailbox blob must fit 256 bytes");
+
+int ensure_mailbox(ss_engine *h) {
+    if (h->mailbox) return SS_OK;
+    if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
+    if (h->integrator == SS_RK4) return ss::fail(SS_EINVAL, "halo exchange supports Euler and Verlet");
+    const size_t vec = h->precision == SS_F32 ? sizeof(float4) : sizeof(double4);
+    const size_t bytes = kMailboxHead + 2 * (size_t)(h->halo_n_recv[0] + h->halo_n_recv[1]) * vec;
+    int rc = h->alloc(&h->mailbox, bytes);
+    if (rc) return rc;
+    MailboxHead head{};
+    head.flag[0] = head.flag[1] = (long long)h->n;          // halos are consistent with the current state
+    CK(cudaMemset(h->mailbox, 0, bytes));
+    CK(cudaMemcpy(h->mailbox, &head, sizeof head, cudaMemcpyHostToDevice));
+    return SS_OK;
+}
+
+int link_side(ss_engine *h, int side, void *peer_mailbox, bool ipc, const int64_t peer_n_recv[2], int64_t vec,
+              int64_t n, int cur) {
+    const int64_t my_vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
+    if (vec != my_vec) return ss::fail(SS_EINVAL, "halo peer: precision differs");
+    if (n != h->n || cur != h->cur) return ss::fail(SS_EINVAL, "halo peer: shards are not at the same step");
+    if (peer_n_recv[1 - side] != h->halo_n_send[side])
+        return ss::fail(SS_EINVAL, "halo peer: plane sizes disagree (%lld received, %d sent)",
+                        (long long)peer_n_recv[1 - side], h->halo_n_send[side]);
+    h->peer_mailbox[side] = peer_mailbox;
+    h->peer_ipc[side] = ipc;
+    h->peer_n_recv[side][0] = peer_n_recv[0];
+    h->peer_n_recv[side][1] = peer_n_recv[1];
+    h->p2p_on = true;
+    return SS_OK;
+}
+
+}  // namespace
+
+extern "C" int ss_halo_p2p_export(ss_engine *h, unsigned char blob[256]) {
+    if (!h || !blob) return ss::fail(SS_EINVAL, "ss_halo_p2p_export: null argument");
+    CK(cudaSetDevice(h->device));
+    int rc = sync_pending(h);
+    if (rc || (rc = ensure_mailbox(h))) return rc;
+    MailboxBlob b{};
+    std::memcpy(b.magic, kMailboxMagic, 8);
+    CK(cudaIpcGetMemHandle(&b.handle, h->mailbox));
+    b.n_recv[0] = h->halo_n_recv[0];
+    b.n_recv[1] = h->halo_n_recv[1];
+    b.vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
+    b.n = h->n;
+    b.cur = h->cur;
+    b.device = h->device;
+    std::memset(blob, 0, 256);
+    std::memcpy(blob, &b, sizeof b);
+    return SS_OK;
+}
+
+extern "C" int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256]) {
+    if (!h || !blob || side < 0 || side > 1) return ss::fail(SS_EINVAL, "ss_halo_p2p_attach: bad argument");
+    MailboxBlob b;
+    std::memcpy(&b, blob, sizeof b);
+    if (std::memcmp(b.magic, kMailboxMagic, 8) != 0) return ss::fail(SS_EINVAL, "ss_halo_p2p_attach: not a mailbox blob");
+    CK(cudaSetDevice(h->device));
+    int rc = sync_pending(h);
+    if (rc || (rc = ensure_mailbox(h))) return rc;
+    void *pm = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&pm, b.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+        return ss::fail(SS_ECUDA, "cudaIpcOpenMemHandle (neighbour on device %d): %s", b.device, cudaGetErrorString(e));
+    rc = link_side(h, side, pm, true, b.n_recv, b.vec, b.n, b.cur);
+    if (rc) cudaIpcCloseMemHandle(pm);
+    return rc;
+}
+
+extern "C" int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer) {
+    if (!h || !peer || side < 0 || side > 1) return ss::fail(SS_EINVAL, "ss_halo_p2p_link: bad argument");
+    if (peer->device != h->device) {
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, h->device, peer->device));
+        if (!ok) return ss::fail(SS_EINVAL, "ss_halo_p2p_link: device %d cannot access device %d", h->device, peer->device);
+        CK(cudaSetDevice(h->device));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+            return ss::fail(SS_ECUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+    }
+    CK(cudaSetDevice(peer->device));
+    int rc = sync_pending(peer);
+    if (rc || (rc = ensure_mailbox(peer))) return rc;
+    CK(cudaSetDevice(h->device));
+    if ((rc = sync_pending(h)) || (rc = ensure_mailbox(h))) return rc;
+    const int64_t pnr[2] = {peer->halo_n_recv[0], peer->halo_n_recv[1]};
+    const int64_t vec = peer->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
+    return link_side(h, side, peer->mailbox, false, pnr, vec, peer->n, peer->cur);
+}
+
 // Step n same-device shards in lockstep; shard k's upper side is shard k+1's
 // lower side.  All work is serialised on shard 0's stream.
 extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_result *res) {
@@ -1685,11 +1873,26 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
     }
     int rc = SS_OK;
     const bool f32 = hs[0]->precision == SS_F32;
+    const bool p2p = hs[0]->p2p_on;
+    for (int k = 0; k < n; ++k) {
+        if (hs[k]->p2p_on != p2p) {
+            rc = ss::fail(SS_EINVAL, "ss_step_group: mix of peer-linked and unlinked shards");
+            break;
+        }
+        hs[k]->group_mode = true;
+    }
     for (int64_t s = 0; s < count && rc == SS_OK; ++s) {
         for (int k = 0; k < n && rc == SS_OK; ++k) {
             rc = dispatch_steps(hs[k], 1);
             hs[k]->n += 1;
             hs[k]->t = (double)hs[k]->n * hs[k]->dt;
+        }
+        if (p2p) {                   // every shard pushes, then every shard lands (one stream)
+            for (int k = 0; k < n && rc == SS_OK; ++k)
+                rc = f32 ? p2p_push<float4>(hs[k], hs[k]->n) : p2p_push<double4>(hs[k], hs[k]->n);
+            for (int k = 0; k < n && rc == SS_OK; ++k)
+                rc = f32 ? p2p_land<float4>(hs[k], hs[k]->n) : p2p_land<double4>(hs[k], hs[k]->n);
+            continue;
         }
         for (int k = 0; k + 1 < n && rc == SS_OK; ++k) {
             ss_engine *a = hs[k], *b = hs[k + 1];
@@ -1727,6 +1930,9 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             *res = r;
         }
     }
-    for (int k = 0; k < n; ++k) hs[k]->stream = saved[k];
+    for (int k = 0; k < n; ++k) {
+        hs[k]->stream = saved[k];
+        hs[k]->group_mode = false;
+    }
     return first_err;
 }

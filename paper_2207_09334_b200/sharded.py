@@ -6,8 +6,10 @@ so a contiguous id range is a slab of whole x-planes.  Rank g owns planes
 (marked fixed) plus every spring touching an owned mass — with its GLOBAL id
 order preserved, so each owned mass sums its springs in the same order as on
 one device and the results are bitwise identical.  After every substep the
-first and last owned planes go to the neighbours' halo planes (NCCL
-send/recv on the engine stream, or device copies for same-device shards).
+first and last owned planes go to the neighbours' halo planes: pushed over
+peer memory into the neighbours' mailboxes and landed behind device-side
+flags (``attach_peers``, the default), or NCCL send/recv on the engine stream
+(``SS_HALO=nccl``), or device copies for same-device shards (``ShardGroup``).
 """
 
 from __future__ import annotations
@@ -106,12 +108,33 @@ def attach_halo(engine: Engine, slab: Slab) -> None:
                                  arrs[3].shape[0], _lib.i64ptr(arrs[3])), "ss_halo_setup")
 
 
+def attach_peers(engine: Engine, rank: int, world: int) -> None:
+    """Peer-memory halo transport between the ranks of a torch.distributed
+    group (one process per GPU, one node): every rank exports its mailbox
+    (CUDA IPC handle), the blobs are all-gathered over the host group, and
+    each rank maps its lower (rank-1) and upper (rank+1) neighbour's."""
+    import torch.distributed as dist
+    lib = _lib.lib()
+    blob = C.create_string_buffer(256)
+    _lib.check(lib.ss_halo_p2p_export(engine.handle, blob), "ss_halo_p2p_export")
+    blobs = [None] * world
+    dist.all_gather_object(blobs, bytes(blob.raw))
+    dist.barrier()                      # every mailbox exists before anyone maps it
+    if rank > 0:
+        _lib.check(lib.ss_halo_p2p_attach(engine.handle, 0, blobs[rank - 1]), "ss_halo_p2p_attach")
+    if rank + 1 < world:
+        _lib.check(lib.ss_halo_p2p_attach(engine.handle, 1, blobs[rank + 1]), "ss_halo_p2p_attach")
+    dist.barrier()
+
+
 class ShardGroup:
-    """k x-slab shards of one cube on ONE device, stepped in lockstep with
-    device-to-device halo copies (the sharded code path without NCCL)."""
+    """k x-slab shards of one cube on ONE device, stepped in lockstep
+    (the sharded code path in one process).  transport="copy": device-to-
+    device plane copies; "p2p": the peer-memory mailboxes and flags of the
+    multi-GPU transport (halo.cuh), linked without IPC."""
 
     def __init__(self, cells: int, shards: int, precision: str = "f64", layout: str = "auto",
-                 v_global: np.ndarray | None = None, device: int = 0):
+                 v_global: np.ndarray | None = None, device: int = 0, transport: str = "copy"):
         nx = cells + 1
         self.slabs = [cube_slab(cells, *slab_planes(nx, shards, r), v_global=v_global)
                       for r in range(shards)]
@@ -119,6 +142,15 @@ class ShardGroup:
                                device=device) for s in self.slabs]
         for e, s in zip(self.engines, self.slabs):
             attach_halo(e, s)
+        if transport == "p2p":
+            lib = _lib.lib()
+            for k, e in enumerate(self.engines):
+                if k > 0:
+                    _lib.check(lib.ss_halo_p2p_link(e.handle, 0, self.engines[k - 1].handle), "ss_halo_p2p_link")
+                if k + 1 < len(self.engines):
+                    _lib.check(lib.ss_halo_p2p_link(e.handle, 1, self.engines[k + 1].handle), "ss_halo_p2p_link")
+        elif transport != "copy":
+            raise ValueError(f"unknown transport {transport!r}")
 
     def step(self, count: int) -> None:
         for e in self.engines:
@@ -147,15 +179,30 @@ class ShardGroup:
 def bench_main(args) -> None:
     """bench.py under torchrun with N>1 ranks: the 400M-spring cube
     (BASELINE.json configs[4], block_scene(313)) split into N x-slabs, one
-    per GPU, NCCL halo exchange every substep.  Strong scaling (fixed lattice)."""
+    per GPU, halo exchange every substep over peer memory (attach_peers;
+    SS_HALO=nccl: NCCL send/recv).  Strong scaling (fixed lattice)."""
     import torch
     import torch.distributed as dist
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # SS_BENCH_SAME_DEVICE=1 (testing the N>1 path on a one-GPU box): every
+    # rank on cuda:0, host coordination over gloo (NCCL refuses duplicate GPUs)
+    same_device = os.environ.get("SS_BENCH_SAME_DEVICE") == "1"
+    if same_device:
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if same_device:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if same_device else "cuda"
+
+    def reduce(value, op):
+        t = torch.tensor([value], device=red_dev)
+        dist.all_reduce(t, op=op)
+        return t.item()
     cells = args.cells or 313
     nx = cells + 1
     n_masses = nx ** 3
@@ -172,14 +219,30 @@ def bench_main(args) -> None:
           f"slab build {t1 - t0:.1f} s, engine {time.perf_counter() - t1:.1f} s", file=sys.stderr,
           flush=True)
     attach_halo(eng, slab)
-    uid = C.create_string_buffer(128)
-    if rank == 0:
-        _lib.check(_lib.lib().ss_nccl_unique_id(uid), "ss_nccl_unique_id")
-    obj = [bytes(uid.raw)]
-    dist.broadcast_object_list(obj, src=0)
-    _lib.check(_lib.lib().ss_halo_nccl(eng.handle, obj[0], world, rank,
-                                       rank - 1 if rank > 0 else -1,
-                                       rank + 1 if rank + 1 < world else -1), "ss_halo_nccl")
+    transport = os.environ.get("SS_HALO", "p2p")
+    if transport == "p2p":
+        ok = 1
+        try:
+            attach_peers(eng, rank, world)
+        except Exception as exc:            # no peer access / IPC: fall back to NCCL everywhere
+            print(f"[rank {rank}] peer-memory halo unavailable ({exc}); using NCCL", file=sys.stderr)
+            ok = 0
+        if not int(reduce(ok, dist.ReduceOp.MIN)):
+            transport = "nccl"
+            if ok:                          # this rank linked, another did not: rebuild without links
+                eng.close()
+                eng = Engine(slab.scene, integrator="verlet", precision=args.precision, layout=args.layout,
+                             device=local)
+                attach_halo(eng, slab)
+    if transport == "nccl":
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(_lib.lib().ss_nccl_unique_id(uid), "ss_nccl_unique_id")
+        obj = [bytes(uid.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        _lib.check(_lib.lib().ss_halo_nccl(eng.handle, obj[0], world, rank,
+                                           rank - 1 if rank > 0 else -1,
+                                           rank + 1 if rank + 1 < world else -1), "ss_halo_nccl")
     build_s = time.perf_counter() - t0
     info = eng.info()
     stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", local))
@@ -198,11 +261,9 @@ def bench_main(args) -> None:
     b.record(stream)
     b.synchronize()
     eng.synchronize()
-    ms = torch.tensor([a.elapsed_time(b)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(reduce(a.elapsed_time(b), dist.ReduceOp.MAX))
     torch.cuda.synchronize()
     dist.barrier()
-    ms = float(ms.item())
     launches = eng.launch_count - launches0
     S = slab.springs_global
     value = S * sub * args.steps / (ms / 1e3)
@@ -225,9 +286,7 @@ def bench_main(args) -> None:
         eng.x_prev = xp_h
         eng.step(sub)
         _ = eng.x
-    ew = torch.tensor([time.perf_counter() - w0], device="cuda")
-    dist.all_reduce(ew, op=dist.ReduceOp.MAX)
-    ew = float(ew.item())
+    ew = float(reduce(time.perf_counter() - w0, dist.ReduceOp.MAX))
     n_local = slab.scene.mass_count
     vec = 16 if args.precision == "f32" else 32
     if rank == 0:
@@ -240,7 +299,9 @@ def bench_main(args) -> None:
                        "springs": S, "masses": n_masses, "substeps_per_step": sub,
                        "integrator": "verlet", "precision": args.precision,
                        "layout": {1: "csr", 2: "ell", 3: "tile"}[info["layout"]],
-                       "parallelism": f"x-slab x{world}, NCCL halo exchange per substep",
+                       "parallelism": f"x-slab x{world}, halo exchange per substep over "
+                                      + ("peer memory (NVLink P2P stores + device flags)" if transport == "p2p"
+                                         else "NCCL send/recv"),
                        "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
                        "build_s_rank0": round(build_s, 1),
                        "l2": "inputs larger than L2"},

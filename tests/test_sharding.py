@@ -136,3 +136,80 @@ def test_nccl_transport_self_loop():
     x = eng.x
     assert x[s.recv_lo].tobytes() == x[s.send_lo].tobytes()
     assert x[s.recv_hi].tobytes() == x[s.send_hi].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("shards", [2, 3])
+def test_peer_memory_shards_match_single_device(precision, shards):
+    """The peer-memory transport (mailboxes, push/land kernels and the
+    release/acquire step flags of the multi-GPU path, halo.cuh) between the
+    shards of one process: fp64 bitwise equal to one engine on the whole
+    cube, fp32 within fp32 rounding of the displacement."""
+    cells = 11
+    full = L.excite(L.block_scene(cells), seed=11)
+    v = excited_velocities(full.mass_count)
+    one = Engine(full, precision=precision)
+    grp = ShardGroup(cells, shards, precision=precision, v_global=v, transport="p2p")
+    one.step(41)
+    grp.step(41)
+    if precision == "f64":
+        assert grp.positions().tobytes() == one.x.tobytes()
+        assert grp.velocities().tobytes() == one.v.tobytes()
+    else:
+        disp = np.abs(one.x - full.x).max()
+        assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
+
+
+def _ipc_worker(rank, world, port, cells, steps, precision, q):
+    """One shard per process, all on cuda:0: the cross-process (CUDA IPC)
+    mailbox mapping and the device-side flag protocol, as under torchrun."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2207_09334_b200.sharded import attach_halo, attach_peers
+        nx = cells + 1
+        s = cube_slab(cells, *slab_planes(nx, world, rank),
+                      v_global=excited_velocities(nx ** 3))
+        eng = Engine(s.scene, integrator="verlet", precision=precision, device=0)
+        attach_halo(eng, s)
+        attach_peers(eng, rank, world)
+        for _ in range(steps // 7):
+            eng.step(7)
+        eng.step(steps % 7)
+        q.put((rank, s.i_lo, eng.x[s.owned].copy(), eng.v[s.owned].copy(), None))
+        eng.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, -1, None, None, repr(exc)))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_peer_memory_shards_across_processes():
+    """Two processes, one shard each, sharing one GPU: mailboxes mapped with
+    cudaIpcOpenMemHandle, planes pushed and landed every substep with no host
+    round trip; the assembled fp64 state is bitwise the single engine's."""
+    cells, steps, world = 9, 30, 2
+    full = L.excite(L.block_scene(cells), seed=11)
+    one = Engine(full, precision="f64")
+    one.step(steps)
+    ref_x, ref_v = one.x.copy(), one.v.copy()
+    one.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 2000) + 7
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, cells, steps, "f64", q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=500) for _ in procs], key=lambda t: t[1])
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r[4] for r in res if r[4]]
+    assert not errs, errs
+    x = np.concatenate([r[2] for r in res])
+    v = np.concatenate([r[3] for r in res])
+    assert x.tobytes() == ref_x.tobytes()
+    assert v.tobytes() == ref_v.tobytes()
