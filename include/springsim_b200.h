@@ -200,6 +200,13 @@ int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every,
                     const int64_t *ids, int64_t n_ids, int64_t max_rows,
                     double *times_out, double *pos_out, double *energy_out,
                     int64_t *rows_out, ss_step_result *res);
+/* Steering snapshot (service.py:378-389 SteerServer._snapshot_bytes): the
+ * positions of the n_ids masses `ids` (caller ids) and (epe, gpe, ke, total)
+ * at the current state (x, v, actuation at t; Engine.energies()), gathered
+ * and reduced on the device.  pos_out: n_ids x 3; energy_out: 4 (may be
+ * null).  Needs ss_energy_setup. */
+int ss_snapshot(ss_engine *h, const int64_t *ids, int64_t n_ids, double gpe_datum, double *pos_out,
+                double *energy_out);
 
 /* Kernel launches issued so far (for the bench's gpu_launches claim). */
 int64_t ss_launch_count(ss_engine *h);

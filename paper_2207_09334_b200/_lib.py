@@ -87,6 +87,7 @@ SIGNATURES = {
     "ss_launch_count": (C.c_int64, [C.c_void_p]),
     "ss_energy_setup": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _dp, _dp,
                                   C.POINTER(C.c_int32), C.c_double]),
+    "ss_snapshot": (C.c_int, [C.c_void_p, _i64p, C.c_int64, C.c_double, _dp, _dp]),
     "ss_step_sampled": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int64,
                                   _dp, _dp, _dp, _i64p, C.POINTER(StepResult)]),
     "ss_plan": (C.c_int, [C.POINTER(SceneDesc), C.POINTER(Info)]),

@@ -1462,6 +1462,46 @@ int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every, const int
     return rc;
 }
 
+// Steering snapshot (service.py:378-389 _snapshot_bytes): the positions of
+// `ids` and (epe, gpe, ke, total) at the current state (x, v; l0 scaled at
+// t), gathered and reduced on the device -- no full-state download, no
+// host-side O(S) energy pass.
+int ss_snapshot(ss_engine *h, const int64_t *ids, int64_t n_ids, double gpe_datum, double *pos_out,
+                double *energy_out) {
+    if (!h || n_ids < 0 || (n_ids && (!ids || !pos_out))) return ss::fail(SS_EINVAL, "ss_snapshot: bad arguments");
+    if (h->energy_springs < 0) return ss::fail(SS_EINVAL, "ss_snapshot: call ss_energy_setup first");
+    CK(cudaSetDevice(h->device));
+    int rc = sync_pending(h);
+    if (rc) return rc;
+    for (int64_t i = 0; i < n_ids; ++i)
+        if (ids[i] < 0 || ids[i] >= h->N) return ss::fail(SS_EINVAL, "ss_snapshot: mass id %lld out of range", (long long)ids[i]);
+    const size_t G = std::max<size_t>(h->groups.size(), 1);
+    std::vector<double> sc(G, 1.0);
+    if (!h->groups.empty()) scales_at(h, h->t, sc.data());
+    std::vector<int> dids((size_t)std::max<int64_t>(n_ids, 1), 0);
+    for (int64_t i = 0; i < n_ids; ++i) dids[i] = (int)dev_of(h, ids[i]);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = std::max(1, std::min(4 * sms, (int)((std::max<int64_t>(h->energy_springs, h->ND) + 255) / 256)));
+    if ((rc = ensure(h, h->d_sids, dids.size() * sizeof(int))) ||
+        (rc = ensure(h, h->d_srows, (size_t)std::max<int64_t>(n_ids, 1) * 3 * sizeof(double))) ||
+        (rc = ensure(h, h->d_serows, 4 * sizeof(double))) || (rc = ensure(h, h->d_sscale, G * sizeof(double))) ||
+        (rc = ensure(h, h->d_spartial, (size_t)grid * 3 * sizeof(double))))
+        return rc;
+    if ((rc = upload(h, h->d_sids.p, dids.data(), dids.size() * sizeof(int))) ||
+        (rc = upload(h, h->d_sscale.p, sc.data(), G * sizeof(double))))
+        return rc;
+    const double datum = h->gpe_datum;
+    h->gpe_datum = gpe_datum;
+    rc = launch_sample(h, 0, (int)n_ids, 0, grid);
+    h->gpe_datum = datum;
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    if (n_ids) CK(cudaMemcpy(pos_out, h->d_srows.p, (size_t)n_ids * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (energy_out) CK(cudaMemcpy(energy_out, h->d_serows.p, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    return SS_OK;
+}
+
 int ss_sync(ss_engine *h, ss_step_result *res) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     CK(cudaSetDevice(h->device));

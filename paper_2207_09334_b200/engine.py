@@ -511,14 +511,7 @@ class Engine:
         self._upload_lent()
         self._push_params()
         lib = _lib.lib()
-        if not getattr(self, "_energy_ready", False):
-            grp = np.ascontiguousarray(self._group_of, dtype=np.int32)
-            _lib.check(lib.ss_energy_setup(self._h, self.spring_count, _lib.i64ptr(self._si),
-                                           _lib.i64ptr(self._sj), _lib.dptr(self._sk),
-                                           _lib.dptr(self._l0),
-                                           grp.ctypes.data_as(C.POINTER(C.c_int32)),
-                                           float(self.gpe_datum)), "ss_energy_setup")
-            self._energy_ready = True
+        self._energy_setup()
         max_rows = count // sample_every + 2
         times = np.empty(max_rows)
         pos = np.empty((max_rows, max(ids.size, 1), 3))
@@ -534,6 +527,46 @@ class Engine:
         _lib.check(rc, "ss_step_sampled")
         r = int(rows.value)
         return times[:r], pos[:r, :ids.size], en[:r]
+
+    def _energy_setup(self) -> None:
+        """Spring list for the device energy reduction, uploaded once."""
+        if getattr(self, "_energy_ready", False):
+            return
+        grp = np.ascontiguousarray(self._group_of, dtype=np.int32)
+        _lib.check(_lib.lib().ss_energy_setup(self._h, self.spring_count, _lib.i64ptr(self._si),
+                                              _lib.i64ptr(self._sj), _lib.dptr(self._sk), _lib.dptr(self._l0),
+                                              grp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                              float(self.gpe_datum)), "ss_energy_setup")
+        self._energy_ready = True
+
+    def snapshot(self, decimate: int = 1, ids=None):
+        """Steering snapshot from the device (service.py:378-389): positions
+        of every ``decimate``-th mass (or of ``ids``) and (epe, gpe, ke, total)
+        at the current state -- ``Engine.energies()`` reduced on the device,
+        without downloading the full state.  Returns (ids, positions (n,3),
+        energies (4,))."""
+        if ids is None:
+            if decimate < 1:
+                raise ValueError("decimate must be >= 1")
+            ids = np.arange(0, self.mass_count, int(decimate), dtype=np.int64)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        self._upload_lent()
+        self._push_params()
+        self._energy_setup()
+        pos = np.empty((ids.size, 3))
+        en = np.empty(4)
+        _lib.check(_lib.lib().ss_snapshot(self._h, _lib.i64ptr(ids) if ids.size else None, int(ids.size),
+                                          float(self.gpe_datum), _lib.dptr(pos), _lib.dptr(en)), "ss_snapshot")
+        return ids, pos, en
+
+    def snapshot_message(self, decimate: int = 1, throughput: float = 0.0) -> dict:
+        """The reference steering server's snapshot message (service.py:380-389)
+        built from :meth:`snapshot` -- same keys and layout, ready for its
+        ``encode_message``."""
+        ids, pos, en = self.snapshot(decimate)
+        return {"type": "snapshot", "t": self.t, "n": self.n,
+                "positions": [[int(i), *map(float, p)] for i, p in zip(ids, pos)],
+                "energies": [float(en[0]), float(en[1]), float(en[2])], "throughput": throughput}
 
     def step_async(self, count: int) -> None:
         """Enqueue ``count`` steps without synchronising (benchmarks)."""

@@ -334,3 +334,23 @@ def test_persistent_small_scene_stepping_is_bitwise_identical(precision, integra
     assert out[0][0].tobytes() == out[1][0].tobytes()
     assert out[0][1].tobytes() == out[1][1].tobytes()
     assert out[0][2] == out[1][2] == 777
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_steering_snapshot_from_device(precision):
+    """Engine.snapshot (service.py:378-389): decimated positions bitwise equal
+    to the host mirror, energies equal to Engine.energies() up to summation
+    order; the message keeps the reference's layout."""
+    from paper_2207_09334_b200 import crawler_scene, replicate
+    batch = replicate(crawler_scene(), 8, jitter=1e-6, seed=1)      # gravity, contact, 2 actuation groups
+    eng = Engine(batch, integrator="verlet", precision=precision)
+    eng.step(777)
+    ids, pos, en = eng.snapshot(decimate=3)
+    assert ids.tolist() == list(range(0, eng.mass_count, 3))
+    assert pos.tobytes() == np.ascontiguousarray(eng.x[ids]).tobytes()
+    ref = eng.energies()
+    for got, want in zip(en, ref):
+        assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+    msg = eng.snapshot_message(decimate=5, throughput=1.0)
+    assert list(msg) == ["type", "t", "n", "positions", "energies", "throughput"]
+    assert msg["n"] == 777 and msg["positions"][1][0] == 5 and len(msg["energies"]) == 3
