@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -27,6 +29,7 @@
 #include "springsim_b200.h"
 #include "tiles.h"
 #include "halo.cuh"
+#include "resident.cuh"
 #include "nccl_shim.h"
 
 using namespace ss;
@@ -142,6 +145,11 @@ struct ss_engine {
     int64_t peer_n_recv[2][2] = {{0, 0}, {0, 0}};
     bool p2p_on = false;
     bool group_mode = false;       // ss_step_group orders the exchange itself
+    // CTA-resident small-scene kernel (resident.cuh): record image and launch shape
+    void *res_image = nullptr;
+    unsigned res_image_bytes = 0, res_off[4] = {0, 0, 0, 0};
+    size_t res_smem = 0;
+    int res_nnz = 0, res_n_dict = 0, res_g = 0, res_threads = 0;
 
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
@@ -563,6 +571,43 @@ int launch_steps(ss_engine *h, int64_t count) {
     const size_t smem = LAYOUT >= 3 ? h->smem_bytes : 0;
     Params<T> p = base_params<T>(h);
     const T *scale = reinterpret_cast<const T *>(h->scale);
+    if (h->res_image && h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2) {
+        // small scene: one CTA keeps the state on chip for the whole batch (resident.cuh)
+        ResidentArgs a{};
+        a.image = reinterpret_cast<const uint4 *>(h->res_image);
+        a.image_bytes = h->res_image_bytes;
+        a.nnz = h->res_nnz;
+        a.n_dict = h->res_n_dict;
+        a.nd = (int)h->ND;
+        a.cur0 = h->cur;
+        a.count = count;
+        a.step0 = h->n;
+        a.bootstrap0 = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
+        a.G = (int)G;
+        a.off_row = h->res_off[0];
+        a.off_inc = h->res_off[1];
+        a.off_dict = h->res_off[2];
+        a.off_grp = h->res_off[3];
+        p.X = reinterpret_cast<const T4 *>(h->X[0]);
+        p.Xout = reinterpret_cast<T4 *>(h->X[1]);
+        p.V = reinterpret_cast<T4 *>(h->V);
+        p.Vout = reinterpret_cast<T4 *>(h->V);
+        p.Xprev = reinterpret_cast<const T4 *>(h->X[h->cur ^ 1]);
+        if (F32 && h->U) {
+            p.Xprev = reinterpret_cast<const T4 *>(h->U);
+            p.U = reinterpret_cast<T4 *>(h->U);
+        }
+        p.scale = G ? scale : nullptr;
+        const bool euler = h->integrator == SS_EULER;
+        auto *k = h->res_g == 8 ? (euler ? resident_kernel<F32, 0, 8> : resident_kernel<F32, 1, 8>)
+                                : (euler ? resident_kernel<F32, 0, 4> : resident_kernel<F32, 1, 4>);
+        k<<<1, h->res_threads, h->res_smem, h->stream>>>(p, a);
+        CK(cudaGetLastError());
+        h->launches += 1;
+        h->cur ^= (int)(count & 1);
+        if (h->integrator == SS_VERLET) h->has_prev = true;
+        return SS_OK;
+    }
     if (h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2 && h->persist_max_grid >= grid) {
         // small scene: one cooperative launch steps the whole batch
         // (kernels.cuh persist_step_kernel / tile_f32.cuh persist_lean_kernel)
@@ -748,6 +793,123 @@ int up_vec(ss_engine *h, void **dst, const std::vector<T> &src) {
     return upload(h, *dst, src.data(), src.size() * sizeof(T));
 }
 
+// Record image of the CTA-resident kernel (resident.cuh) for scenes of at
+// most kResidentMaxSlots device slots whose image fits shared memory; every
+// mass's incidences in ascending spring id (the reference's summation order),
+// springs deduplicated into a dictionary.  SS_RESIDENT=0 disables it.
+template <bool F32>
+int setup_resident(ss_engine *h, const ss_scene_desc *d) {
+    using T4 = typename Prec<F32>::T4;
+    if (h->integrator == SS_RK4 || h->ND > kResidentMaxSlots || (F32 && !h->rx0) ||
+        h->groups.size() > (size_t)kResidentMaxGroups)
+        return SS_OK;
+    if (const char *e = getenv("SS_RESIDENT"))
+        if (atoi(e) == 0) return SS_OK;
+    const int64_t ND = h->ND, S = h->S;
+    std::vector<int64_t> dev(h->N);
+    for (int64_t i = 0; i < h->N; ++i)
+        dev[i] = h->tl.new_of.empty() || h->orig_of.empty() ? i : (int64_t)h->tl.new_of[i];
+    std::vector<uint32_t> row((size_t)ND + 1, 0);
+    for (int64_t s = 0; s < S; ++s) {
+        row[dev[d->si[s]] + 1]++;
+        row[dev[d->sj[s]] + 1]++;
+    }
+    for (int64_t i = 0; i < ND; ++i) row[i + 1] += row[i];
+    const int64_t nnz = row[ND];
+    std::vector<uint32_t> inc((size_t)nnz), fill(row.begin(), row.end() - 1);
+    const bool has_g = d->group && !h->groups.empty();
+    // dictionary: fp64 (k, l0, group) bit patterns; fp32 (k, k*l0, D, group) as tiles_f32.cpp
+    std::map<std::array<uint64_t, 4>, uint32_t> dict;
+    std::vector<std::array<uint64_t, 4>> keys;
+    auto key_of = [&](int64_t s, int64_t me, int64_t other) {
+        std::array<uint64_t, 4> k{};
+        const int64_t g = has_g ? d->group[s] : -1;
+        if constexpr (F32) {
+            const float kf = (float)d->k[s], kl = (float)(d->k[s] * d->l0[s]);
+            float D[3];
+            for (int c = 0; c < 3; ++c) D[c] = (float)(d->x[3 * other + c] - d->x[3 * me + c]);
+            uint32_t b[5];
+            std::memcpy(&b[0], &kf, 4);
+            std::memcpy(&b[1], &kl, 4);
+            std::memcpy(&b[2], D, 12);
+            k[0] = ((uint64_t)b[0] << 32) | b[1];
+            k[1] = ((uint64_t)b[2] << 32) | b[3];
+            k[2] = b[4];
+        } else {
+            std::memcpy(&k[0], &d->k[s], 8);
+            std::memcpy(&k[1], &d->l0[s], 8);
+        }
+        k[3] = (uint64_t)(g + 1);
+        return k;
+    };
+    for (int64_t s = 0; s < S; ++s) {
+        const int64_t a = d->si[s], b = d->sj[s];
+        for (int end = 0; end < 2; ++end) {
+            const int64_t me = end ? b : a, other = end ? a : b;
+            const auto key = key_of(s, me, other);
+            auto it = dict.find(key);
+            uint32_t di;
+            if (it == dict.end()) {
+                di = (uint32_t)keys.size();
+                if (di >= (1u << 19)) return SS_OK;                 // too many distinct springs: not resident
+                dict.emplace(key, di);
+                keys.push_back(key);
+            } else {
+                di = it->second;
+            }
+            const uint32_t owner = me < other ? 0x1000u : 0u;      // degenerate springs counted at the lower id
+            inc[fill[dev[me]]++] = (uint32_t)dev[other] | owner | (di << 13);
+        }
+    }
+    const int64_t nd = (int64_t)keys.size();
+    auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    const size_t off_row = 2 * (size_t)ND * sizeof(T4);
+    const size_t off_inc = off_row + al16(((size_t)ND + 1) * 4);
+    const size_t off_dict = off_inc + al16((size_t)nnz * 4);
+    const size_t off_grp = off_dict + al16((size_t)nd * (F32 ? 32 : 16));
+    const size_t end = off_grp + (F32 ? 0 : al16((size_t)nd * 4));
+    int dev_max = 0;
+    CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    if (end + 64 > (size_t)dev_max) return SS_OK;                   // does not fit one SM
+    std::vector<unsigned char> img(end - off_row, 0);
+    std::memcpy(img.data(), row.data(), row.size() * 4);
+    std::memcpy(img.data() + (off_inc - off_row), inc.data(), inc.size() * 4);
+    for (int64_t q = 0; q < nd; ++q) {
+        const auto &k = keys[q];
+        unsigned char *e = img.data() + (off_dict - off_row) + (size_t)q * (F32 ? 32 : 16);
+        const int32_t g = (int32_t)((int64_t)k[3] - 1);
+        if constexpr (F32) {
+            const uint32_t b[6] = {(uint32_t)(k[0] >> 32), (uint32_t)k[0], (uint32_t)(k[1] >> 32), (uint32_t)k[1],
+                                   (uint32_t)k[2], (uint32_t)g};
+            std::memcpy(e, b, 24);                                  // k, k*l0, Dx, Dy | Dz, group, 0, 0
+        } else {
+            std::memcpy(e, &k[0], 8);
+            std::memcpy(e + 8, &k[1], 8);
+            std::memcpy(img.data() + (off_grp - off_row) + (size_t)q * 4, &g, 4);
+        }
+    }
+    int rc = h->alloc(&h->res_image, img.size());
+    if (rc || (rc = upload(h, h->res_image, img.data(), img.size()))) return rc;
+    h->res_image_bytes = (unsigned)img.size();
+    h->res_off[0] = (unsigned)off_row;
+    h->res_off[1] = (unsigned)off_inc;
+    h->res_off[2] = (unsigned)off_dict;
+    h->res_off[3] = (unsigned)off_grp;
+    h->res_smem = end;
+    h->res_nnz = (int)nnz;
+    h->res_n_dict = (int)nd;
+    // lanes per mass slot; only slots up to the last real mass get threads
+    int64_t used = 0;
+    for (int64_t i = 0; i < ND; ++i)
+        if (h->src_of(i) >= 0) used = i + 1;
+    h->res_g = used * 8 <= 1024 ? 8 : 4;
+    h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
+    for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
+                           (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>})
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)end));
+    return SS_OK;
+}
+
 template <bool F32>
 int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     using T = typename Prec<F32>::T;
@@ -872,7 +1034,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             }
         }
         h->lay.canonical = L.canonical;
-        return SS_OK;
+        return setup_resident<F32>(h, d);
     }
     LayoutInput li{N, S, d->si, d->sj};
     if ((rc = build_layout(li, layout, h->lay))) return rc;
@@ -918,7 +1080,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         if ((rc = up_int(&h->r_pos, L.r_pos))) return rc;
         if ((rc = up_int(&h->cnt, L.cnt))) return rc;
     }
-    return SS_OK;
+    return setup_resident<F32>(h, d);
 }
 
 int64_t algorithmic_bytes(const ss_engine *h) {

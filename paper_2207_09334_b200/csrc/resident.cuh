@@ -1,0 +1,328 @@
+// CTA-resident kernel for small scenes ("small scenes").
+//
+// A scene of at most kResidentMaxSlots device slots (the walker, the
+// cantilever, a few dozen robots) is stepped by ONE CTA for a whole batch:
+// positions live in shared memory (double-buffered by step parity), every
+// mass's incidence list and a dictionary of distinct spring records are
+// staged into shared memory once per launch, and each thread keeps its
+// masses' velocity and history (x_prev / u) in registers.  A step is then a
+// pass over shared memory plus one __syncthreads -- no launch, no grid
+// barrier, no global-memory round trip -- which is what "many small-dt
+// substeps batched into a persistent kernel" (north_star) needs when the
+// whole scene is a few microseconds of work per launch.
+//
+// Arithmetic is that of the multi-CTA kernels: fp64 sums each mass's
+// springs in ascending spring id with the reference's op order
+// (_kernels.py:51-70, engine.py:273-328), so results are bitwise those of
+// step_kernel and of the reference; fp32 uses the displacement form
+// d = D + (r_o - r_m) of tile_f32.cuh.
+#pragma once
+
+#include "kernels.cuh"
+#include "tile_f32.cuh"
+
+namespace ss {
+
+constexpr int kResidentMaxSlots = 256;      // one tile: beyond it the multi-CTA kernels win
+constexpr int kResidentMaxGroups = 64;      // actuation groups staged in shared memory
+
+// add_external (kernels.cuh) with f_ext from registers: same op order.
+template <bool F32>
+__device__ __forceinline__ V3<typename Prec<F32>::T>
+add_external_fe(const Params<typename Prec<F32>::T> &p, V3<typename Prec<F32>::T> a, V3<typename Prec<F32>::T> x,
+                const typename Prec<F32>::T4 &v4, typename Prec<F32>::T mass, const typename Prec<F32>::T *fe) {
+    using T = typename Prec<F32>::T;
+    a.x = a.x + mass * p.g[0];
+    a.y = a.y + mass * p.g[1];
+    a.z = a.z + mass * p.g[2];
+    if (p.F) {
+        a.x = a.x + fe[0];
+        a.y = a.y + fe[1];
+        a.z = a.z + fe[2];
+    }
+    for (int q = 0; q < p.n_planes; ++q) {
+        const T n0 = p.pn[q][0], n1 = p.pn[q][1], n2 = p.pn[q][2];
+        const T depth = p.poff[q] - ((x.x * n0 + x.y * n1) + x.z * n2);
+        if (!(depth > (T)0)) continue;
+        const T fn = p.ppen[q] * depth;
+        a.x = a.x + fn * n0;
+        a.y = a.y + fn * n1;
+        a.z = a.z + fn * n2;
+        if (p.pfric[q] > (T)0) {
+            const T vn = (v4.x * n0 + v4.y * n1) + v4.z * n2;
+            const T tx = v4.x - vn * n0, ty = v4.y - vn * n1, tz = v4.z - vn * n2;
+            const T speed = sqrt((tx * tx + ty * ty) + tz * tz);
+            if (speed > (T)1e-15) {
+                const T mag = fmin(p.pfric[q] * fn, (speed * mass) / p.dt);
+                const T r = mag / speed;
+                a.x = a.x - r * tx;
+                a.y = a.y - r * ty;
+                a.z = a.z - r * tz;
+            }
+        }
+    }
+    return a;
+}
+
+// incidence word: partner slot (bits 0-11) | counts a degenerate spring (bit
+// 12: this endpoint is the spring's lower caller id) | dictionary index << 13
+// Shared memory: positions [2][nd] T4, then an image of the records built by
+// the host (engine.cu build_resident), copied in verbatim:
+//   row   u32 [nd + 1]   offsets into inc (device slot order)
+//   inc   u32 [nnz]      incidence words, per mass in ascending spring id
+//   dict  fp64: double2 (k, l0) [n_dict]; fp32: float4 (k, k*l0, Dx, Dy),
+//         float4 (Dz, group bits, 0, 0) [n_dict]
+//   grp   fp64: int32 group per dictionary entry (-1 passive) [n_dict]
+// each section 16-byte aligned.
+struct ResidentArgs {
+    const uint4 *image;           // the record image (global memory)
+    unsigned image_bytes;         // multiple of 16
+    int nnz, n_dict, nd;
+    int cur0;                     // X buffer holding the positions at the start
+    long long count, step0;
+    int bootstrap0;               // Verlet without x_prev at the first step
+    int G;                        // actuation groups (scale row stride)
+    unsigned off_row, off_inc, off_dict, off_grp;   // shared-memory byte offsets (positions first)
+};
+
+// Spring sum of mass m by a group of G lanes (lane j = 0..G-1 of the group):
+// round r evaluates incidences r*G + j side by side.  fp64: the group leader
+// adds the G forces of a round in list order -- the serial spring-id order,
+// bitwise -- skipping degenerate springs exactly like the reference; fp32:
+// every lane sums its own incidences and the group reduces in a fixed order.
+// The sum is returned to every lane of the group.
+template <bool F32, int G>
+__device__ __forceinline__ V3<typename Prec<F32>::T>
+resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const typename Prec<F32>::T4 *xs, int m,
+                    const typename Prec<F32>::T4 &x4, const typename Prec<F32>::T *scale, int lane, unsigned gmask,
+                    int leader, unsigned &deg) {
+    using T = typename Prec<F32>::T;
+    const uint32_t *row = reinterpret_cast<const uint32_t *>(smem + a.off_row);
+    const uint32_t *inc = reinterpret_cast<const uint32_t *>(smem + a.off_inc);
+    V3<T> s = {(T)0, (T)0, (T)0};
+    const int q0 = (int)row[m], n = (int)row[m + 1] - q0;
+    if constexpr (F32) {
+        const float4 *dict = reinterpret_cast<const float4 *>(smem + a.off_dict);
+        for (int q = lane; q < n; q += G) {
+            const uint32_t e = inc[q0 + q];
+            const float4 kd = dict[2 * (e >> 13)], ez = dict[2 * (e >> 13) + 1];
+            float kl0 = kd.y;
+            if (scale) {
+                const int g = __float_as_int(ez.y);
+                if (g >= 0) kl0 = kl0 * scale[g];
+            }
+            const float4 ro = xs[e & 0xfffu];
+            const float dx = kd.z + (ro.x - x4.x), dy = kd.w + (ro.y - x4.y), dz = ez.x + (ro.z - x4.z);
+            float d2;
+            const float c = spring_c(dx, dy, dz, kd.x, kl0, d2);
+            if (d2 < 1e-24f && (e & 0x1000u)) ++deg;
+            s.x = __fmaf_rn(c, dx, s.x);
+            s.y = __fmaf_rn(c, dy, s.y);
+            s.z = __fmaf_rn(c, dz, s.z);
+        }
+#pragma unroll
+        for (int w = G / 2; w > 0; w >>= 1) {               // fixed-order tree over the group
+            s.x = s.x + __shfl_down_sync(gmask, s.x, w, G);
+            s.y = s.y + __shfl_down_sync(gmask, s.y, w, G);
+            s.z = s.z + __shfl_down_sync(gmask, s.z, w, G);
+        }
+    } else {
+        const double2 *dict = reinterpret_cast<const double2 *>(smem + a.off_dict);
+        const int *dg = reinterpret_cast<const int *>(smem + a.off_grp);
+        for (int r0 = 0; r0 < n; r0 += G) {
+            const int q = r0 + lane;
+            double fx = 0.0, fy = 0.0, fz = 0.0;
+            bool add = false;
+            if (q < n) {
+                const uint32_t e = inc[q0 + q], di = e >> 13;
+                const double2 kl = dict[di];
+                double l0 = kl.y;
+                if (scale) {
+                    const int g = dg[di];
+                    if (g >= 0) l0 = l0 * scale[g];
+                }
+                const double4 xo = xs[e & 0xfffu];
+                const double dx = xo.x - x4.x, dy = xo.y - x4.y, dz = xo.z - x4.z;
+                const double len = sqrt((dx * dx + dy * dy) + dz * dz);
+                if (len < 1e-12) {                          // skipped and counted (_kernels.py:58-60)
+                    if (e & 0x1000u) ++deg;
+                } else {
+                    const double c = (kl.x * (len - l0)) / len;
+                    fx = c * dx;
+                    fy = c * dy;
+                    fz = c * dz;
+                    add = true;
+                }
+            }
+            const unsigned ballot = __ballot_sync(gmask, add) >> leader;
+#pragma unroll
+            for (int i = 0; i < G; ++i) {                   // list order: s = s + f (the serial loop)
+                const double gx = __shfl_sync(gmask, fx, i, G);
+                const double gy = __shfl_sync(gmask, fy, i, G);
+                const double gz = __shfl_sync(gmask, fz, i, G);
+                if ((ballot >> i) & 1u) {
+                    s.x = s.x + gx;
+                    s.y = s.y + gy;
+                    s.z = s.z + gz;
+                }
+            }
+        }
+    }
+    s.x = __shfl_sync(gmask, s.x, 0, G);
+    s.y = __shfl_sync(gmask, s.y, 0, G);
+    s.z = __shfl_sync(gmask, s.z, 0, G);
+    return s;
+}
+
+// INTEG: 0 Euler, 1 Verlet.  G lanes per mass slot: slot m = tid / G.
+template <bool F32, int INTEG, int G>
+__global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<F32>::T> p, ResidentArgs a) {
+    using T = typename Prec<F32>::T;
+    using T4 = typename Prec<F32>::T4;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int diverged;
+    __shared__ T sscale[2][kResidentMaxGroups];            // this and the next step's actuation scales
+    T4 *const xsb = reinterpret_cast<T4 *>(smem);          // positions: [c * nd + slot], c = step parity
+    const int tid = threadIdx.x, bs = blockDim.x;
+    const int m = tid / G, lane = tid % G;
+    const int leader = (tid & 31) & ~(G - 1);               // group's first lane within the warp
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << leader;
+    // stage the record image (16-byte copies) and the start positions
+    {
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + a.off_row);
+        const unsigned n16 = a.image_bytes / 16u;
+        for (unsigned i = tid; i < n16; i += bs) dst[i] = __ldg(a.image + i);
+    }
+    const T4 *X0 = a.cur0 ? p.Xout : p.X;                   // (host passes X[0] as X, X[1] as Xout)
+    const bool in = m < a.nd;
+    const bool act = in && (!p.orig_of || p.orig_of[m] >= 0);
+    T4 x{}, v{}, hst{}, pb{};
+    if (in) {
+        x = X0[m];
+        if (lane == 0) xsb[m] = x;
+    }
+    if (act) {
+        v = p.V[m];
+        if (INTEG == 1 && !a.bootstrap0) hst = p.Xprev[m];  // fp64: x_prev; fp32: u
+        if constexpr (F32) pb = p.P[m];
+    }
+    if (tid == 0) diverged = 0;
+    if (tid < a.G) sscale[0][tid] = p.scale[tid];
+    T fe[3] = {(T)0, (T)0, (T)0};                           // f_ext is constant over a batch
+    if (act && p.F) {
+        const T4 f4 = p.F[m];
+        fe[0] = f4.x;
+        fe[1] = f4.y;
+        fe[2] = f4.z;
+    }
+    __syncthreads();
+    unsigned deg = 0;
+    int c = 0;
+    long long done = 0;
+    for (long long s = 0; s < a.count; ++s) {
+        const T *scale = a.G ? sscale[s & 1] : nullptr;
+        // the next step's scales, fetched now and published by this step's barrier
+        T next_scale = (T)0;
+        if (tid < a.G && s + 1 < a.count) next_scale = p.scale[(size_t)(s + 1) * a.G + tid];
+        const bool boot = INTEG == 1 && s == 0 && a.bootstrap0;
+        if (act) {                                          // (uniform within a group)
+            const T4 x4 = x;
+            const T mass = F32 ? (T)fabsf((float)x4.w) : (T)fabs((double)x4.w);
+            const bool fixed = signbit(x4.w);
+            const V3<T> sp = resident_spring_sum<F32, G>(a, smem, xsb + (c ? a.nd : 0), m, x4, scale, lane, gmask,
+                                                         leader, deg);
+            V3<T> xa = {x4.x, x4.y, x4.z};                  // absolute position (contact)
+            if constexpr (F32) { xa.x = pb.x + xa.x; xa.y = pb.y + xa.y; xa.z = pb.z + xa.z; }
+            const V3<T> f = add_external_fe<F32>(p, sp, xa, v, mass, fe);   // engine.py:273-288
+            T xn[3], vn[3], un[3] = {(T)0, (T)0, (T)0};
+            const T xc[3] = {x4.x, x4.y, x4.z};
+            const T vc[3] = {v.x, v.y, v.z};
+            const T fcv[3] = {f.x, f.y, f.z};
+            if constexpr (INTEG == 0) {                     // engine.py:303-310
+                const T dtm = p.dt / mass;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    xn[k] = xc[k] + p.dt * vc[k];
+                    vn[k] = vc[k] + dtm * fcv[k];
+                    if (p.damped) vn[k] = vn[k] * p.one_minus_d;
+                }
+            } else {                                        // engine.py:312-328
+                const T coef = p.dt2_over / mass;
+                if constexpr (F32) {                        // increment form (kernels.cuh verlet_u)
+                    const float u[3] = {hst.x, hst.y, hst.z};
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const float acc = coef * fcv[k];
+                        if (boot) {
+                            un[k] = p.dt * vc[k] + 0.5f * acc;
+                            vn[k] = vc[k];
+                        } else {
+                            un[k] = (p.damped ? p.one_minus_d * u[k] : u[k]) + acc;
+                            vn[k] = (un[k] + u[k]) / p.two_dt;
+                        }
+                        xn[k] = xc[k] + un[k];
+                    }
+                } else if (boot) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        xn[k] = (xc[k] + p.dt * vc[k]) + (T)0.5 * (coef * fcv[k]);
+                        vn[k] = vc[k];
+                    }
+                } else {
+                    const T xp[3] = {hst.x, hst.y, hst.z};
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const T acc = coef * fcv[k];
+                        if (p.damped) xn[k] = (xc[k] + p.one_minus_d * (xc[k] - xp[k])) + acc;
+                        else          xn[k] = ((T)2 * xc[k] - xp[k]) + acc;
+                        vn[k] = (xn[k] - xp[k]) / p.two_dt;
+                    }
+                }
+            }
+            if (fixed) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) { xn[k] = xc[k]; vn[k] = vc[k]; un[k] = (T)0; }
+            }
+            if constexpr (INTEG == 1) {
+                if constexpr (F32) hst = T4{un[0], un[1], un[2], (T)0};
+                else hst = x4;                              // x_prev of the next step
+            }
+            x.x = xn[0];
+            x.y = xn[1];
+            x.z = xn[2];
+            v.x = vn[0];
+            v.y = vn[1];
+            v.z = vn[2];
+            if (lane == 0) {
+                xsb[(c ? 0 : a.nd) + m] = x;
+                if (!(finite3<F32>(xn[0], xn[1], xn[2]) && finite3<F32>(vn[0], vn[1], vn[2]))) {
+                    diverged = 1;
+                    atomicMin(p.div_mass, p.orig_of ? p.orig_of[m] : m);
+                }
+            }
+        }
+        if (tid < a.G) sscale[(s + 1) & 1][tid] = next_scale;
+        __syncthreads();                                    // also orders next step's writes after this step's reads
+        c ^= 1;
+        done = s + 1;
+        if (diverged) {                                     // committed; the reference raises here
+            if (tid == 0) atomicMin(p.div_step, a.step0 + s + 1);
+            break;
+        }
+    }
+    // write back: x into the buffer the host will call current, history,
+    // velocities; padding slots keep their zeros
+    if (act && lane == 0) {
+        T4 *Xc = (a.cur0 ^ (int)(done & 1)) ? p.Xout : const_cast<T4 *>(p.X);
+        T4 *Xo = (a.cur0 ^ (int)(done & 1)) ? const_cast<T4 *>(p.X) : p.Xout;
+        Xc[m] = x;
+        p.Vout[m] = v;
+        if constexpr (INTEG == 1) {
+            if constexpr (F32) p.U[m] = hst;
+            else Xo[m] = hst;
+        }
+    }
+    flush_degenerate(p.degenerate, deg);
+}
+
+}  // namespace ss

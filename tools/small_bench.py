@@ -1,21 +1,24 @@
-"""Per-step time of small scenes, persistent cooperative stepping on/off (dev tool)."""
+"""Per-step time of small scenes: CTA-resident kernel (default) vs one launch
+per step (SS_RESIDENT=0), and whether both give the same bits (dev tool)."""
 import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2207_09334_b200 import Engine, crawler_scene, lattice as L, replicate
 
 scenes = {"crawler": crawler_scene, "beam40": lambda: L.beam_lattice(length=4.0),
-          "cube12": lambda: L.excite(L.block_scene(12)), "crawler_x64": lambda: replicate(crawler_scene(), 64)}
+          "cube9": lambda: L.excite(L.block_scene(9)), "crawler_x64": lambda: replicate(crawler_scene(), 64)}
 for name, mk in scenes.items():
     for prec in ("f64", "f32"):
         row = {"scene": name, "prec": prec}
-        for persist in ("0", "1"):
-            os.environ["SS_PERSIST"] = persist
+        for res in ("1", "0"):
+            os.environ["SS_RESIDENT"] = res
             e = Engine(mk(), integrator="verlet", precision=prec)
+            row["slots"] = e.info()["n_masses"]
             e.step(100)
             n = 20000
             t0 = time.perf_counter(); e.step(n); dt = time.perf_counter() - t0
-            row["us_per_step_persist" + persist] = round(1e6 * dt / n, 2)
-            row["x_" + persist] = e.x.copy()
+            row["us_per_step_resident" + res] = round(1e6 * dt / n, 3)
+            row["x_" + res] = e.x.copy()
+            e.close()
         row["same"] = bool(row.pop("x_0").tobytes() == row.pop("x_1").tobytes())
         print(json.dumps(row), flush=True)
