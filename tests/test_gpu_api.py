@@ -354,3 +354,28 @@ def test_steering_snapshot_from_device(precision):
     msg = eng.snapshot_message(decimate=5, throughput=1.0)
     assert list(msg) == ["type", "t", "n", "positions", "energies", "throughput"]
     assert msg["n"] == 777 and msg["positions"][1][0] == 5 and len(msg["energies"]) == 3
+
+
+@pytest.mark.parametrize("integrator", ["verlet", "euler"])
+def test_resident_kernel_matches_per_step_launches(integrator, monkeypatch):
+    """One-tile scenes run the CTA-resident kernel (resident.cuh) for whole
+    batches; fp64 is bitwise the per-step launches (SS_RESIDENT=0), fp32
+    agrees to rounding (its summation order differs)."""
+    from paper_2207_09334_b200 import crawler_scene, replicate
+    batch = replicate(crawler_scene(), 12, jitter=1e-6, seed=2)     # 240 masses, contact, 2 groups
+    out = {}
+    for prec in ("f64", "f32"):
+        for res in ("1", "0"):
+            monkeypatch.setenv("SS_RESIDENT", res)
+            eng = Engine(batch, integrator=integrator, precision=prec)
+            eng.set_damping(1e-4)
+            eng.step(1)
+            eng.step(1500)
+            eng.x_prev                                              # noqa: B018  (mirror refresh)
+            out[prec, res] = (eng.x.copy(), eng.v.copy(), eng.n)
+            eng.close()
+    assert out["f64", "1"][0].tobytes() == out["f64", "0"][0].tobytes()
+    assert out["f64", "1"][1].tobytes() == out["f64", "0"][1].tobytes()
+    assert out["f64", "1"][2] == out["f64", "0"][2] == 1501
+    span = np.abs(out["f64", "0"][0] - batch.x).max()
+    assert np.abs(out["f32", "1"][0] - out["f32", "0"][0]).max() <= 1e-3 * span

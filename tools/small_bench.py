@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2207_09334_b200 import Engine, crawler_scene, lattice as L, replicate
 
-scenes = {"crawler": crawler_scene, "beam40": lambda: L.beam_lattice(length=4.0),
+scenes = {"crawler": crawler_scene, "crawler_x12": lambda: replicate(crawler_scene(), 12), "beam40": lambda: L.beam_lattice(length=4.0),
           "cube9": lambda: L.excite(L.block_scene(9)), "crawler_x64": lambda: replicate(crawler_scene(), 64)}
 for name, mk in scenes.items():
     for prec in ("f64", "f32"):
