@@ -299,9 +299,10 @@ def bench_main(args) -> None:
                        "springs": S, "masses": n_masses, "substeps_per_step": sub,
                        "integrator": "verlet", "precision": args.precision,
                        "layout": {1: "csr", 2: "ell", 3: "tile"}[info["layout"]],
-                       "parallelism": f"x-slab x{world}, halo exchange per substep over "
-                                      + ("peer memory (NVLink P2P stores + device flags)" if transport == "p2p"
-                                         else "NCCL send/recv"),
+                       "parallelism": (f"x-slab x{world}, halo exchange per substep over "
+                                       + ("peer memory (NVLink P2P stores + device flags)" if transport == "p2p"
+                                          else "NCCL send/recv")) if world > 1
+                                      else "single GPU through the sharded path (no neighbours, no exchange)",
                        "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
                        "build_s_rank0": round(build_s, 1),
                        "l2": "inputs larger than L2"},
