@@ -172,6 +172,33 @@ def test_large_block_against_oracle(precision):
         assert err / disp <= 1e-3     # displacement-relative error
 
 
+def test_full_size_10m_cube():
+    """BASELINE configs[3] at full size (block_scene(91): 9,896,068 springs,
+    the bench workload): fp64 bitwise vs the C oracle (pinned to the
+    reference) after 3 Verlet steps; fp32 vs fp64 after 100 substeps within
+    1e-3 of the displacement; total momentum of the free cube conserved."""
+    import oracle as orc
+    from paper_2207_09334_b200.model import scene_arrays
+    scene = L.excite(L.block_scene(91), seed=11)
+    arr = scene_arrays(scene)
+    e64 = Engine(scene, precision="f64")
+    e64.step(3)
+    ref = orc.OracleEngine(arr, integrator="verlet", mode="parallel-det", threads=16)
+    ref.step(3)
+    assert e64.x.tobytes() == ref.x.tobytes()
+    assert e64.v.tobytes() == ref.v.tobytes()
+    del ref
+    e64.step(97)
+    e32 = Engine(scene, precision="f32")
+    e32.step(100)
+    disp = np.abs(e64.x - scene.x).max()
+    assert np.abs(e32.x - e64.x).max() <= 1e-3 * disp
+    p0 = (arr.m[:, None] * scene.v).sum(axis=0)
+    for eng, tol in ((e64, 1e-9), (e32, 1e-5)):
+        p1 = (arr.m[:, None] * eng.v).sum(axis=0)
+        assert np.linalg.norm(p1 - p0) <= tol * np.linalg.norm(p0)
+
+
 def test_momentum_conserved_free_block():
     """tests/test_acceptance.py:169-195 momentum criterion on the GPU."""
     scene = L.excite(L.block_scene(9), seed=11)
