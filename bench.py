@@ -124,15 +124,15 @@ def profiled_traffic(workload: str, precision: str, layout: str):
     return None if entry is None else entry["bytes"]
 
 
-def cpu_sample(scene, target_s=12.0, max_steps=40, threads=None):
+def cpu_sample(scene, target_s=12.0, max_steps=40, threads=None, mode="parallel-det"):
     """Time the oracle's restatement of the reference's parallel-det mode
-    (Alg. 1 slot schedule, OpenMP) on the host: bounded sample of Verlet steps."""
+    (Alg. 1 slot schedule, OpenMP) -- or its serial mode on one core -- on
+    the host: bounded sample of Verlet steps."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     from paper_2207_09334_b200.model import scene_arrays
-    threads = threads or orc.max_threads()
-    eng = orc.OracleEngine(scene_arrays(scene), integrator="verlet", mode="parallel-det",
-                           threads=threads)
+    threads = 1 if mode == "serial" else (threads or orc.max_threads())
+    eng = orc.OracleEngine(scene_arrays(scene), integrator="verlet", mode=mode, threads=threads)
     eng.step(1)                          # warm-up (first touch of the slab)
     t0 = time.perf_counter()
     steps = 0
@@ -283,9 +283,13 @@ def run_single(args):
     cpu = None
     if not args.no_cpu:
         cv, csteps, cwall, cthreads = cpu_sample(scene)
+        sv, ssteps, swall, _ = cpu_sample(scene, target_s=3.0, max_steps=20, mode="serial")
         cpu = {"value": cv, "unit": "spring-updates/s", "cores": cthreads, "kind": "port",
                "sample": f"{csteps} Verlet steps ({cwall:.1f} s) of the same {S}-spring cube, "
-                         f"reference parallel-det Alg.1 schedule restated in C/OpenMP"}
+                         f"reference parallel-det Alg.1 schedule restated in C/OpenMP",
+               "host_threads": os.cpu_count(),
+               "serial_1core": {"value": sv, "unit": "spring-updates/s", "cores": 1,
+                                "sample": f"{ssteps} Verlet steps ({swall:.1f} s), the reference's serial mode"}}
 
     workload = f"cube_n{cells}_10M_springs_excited_verlet" if cells == 91 else f"cube_n{cells}_excited_verlet"
     layout_name = {1: "csr", 2: "ell", 3: "tile"}[info["layout"]]
