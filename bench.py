@@ -13,7 +13,7 @@ time.  N>1 (torchrun): the 400M-spring cube (configs[4]) split into x-slabs
 
 Keys beyond the driver contract: ``roofline`` (HBM: algorithmic bytes per
 substep launch / average launch time vs MEASURED_PEAKS.json), ``cpu_baseline``
-(the oracle's restatement of the reference's parallel-det schedule on the
+(the oracle's restatement of the reference's default parallel schedule on the
 host's cores, bounded sample), ``e2e`` (the same metric through the public
 Engine API with host state uploaded and positions read back every step).
 """
@@ -124,10 +124,11 @@ def profiled_traffic(workload: str, precision: str, layout: str):
     return None if entry is None else entry["bytes"]
 
 
-def cpu_sample(scene, target_s=12.0, max_steps=40, threads=None, mode="parallel-det"):
-    """Time the oracle's restatement of the reference's parallel-det mode
-    (Alg. 1 slot schedule, OpenMP) -- or its serial mode on one core -- on
-    the host: bounded sample of Verlet steps."""
+def cpu_sample(scene, target_s=12.0, max_steps=40, threads=None, mode="parallel"):
+    """Time the oracle's restatement of the reference's parallel mode (the
+    reference bench's default, bench.py:93: Alg. 1 atomic slot schedule,
+    OpenMP, all host threads) -- or its serial mode on one core -- on the
+    host: bounded sample of Verlet steps."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     from paper_2207_09334_b200.model import scene_arrays
@@ -151,8 +152,9 @@ def build_workload(cells):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port of its
-    parallel-det Alg.1 schedule, all host threads), same config/metric."""
+    """--impl reference: the reference's CPU algorithm in its bench's default
+    mode (bench.py:91-93: "parallel", the Alg. 1 atomic slot schedule; oracle
+    port, all host threads), same config/metric."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -162,8 +164,7 @@ def run_reference(args):
     import oracle as orc
     from paper_2207_09334_b200.model import scene_arrays
     threads = orc.max_threads()
-    eng = orc.OracleEngine(scene_arrays(scene), integrator="verlet", mode="parallel-det",
-                           threads=threads)
+    eng = orc.OracleEngine(scene_arrays(scene), integrator="verlet", mode="parallel", threads=threads)
     for _ in range(max(args.warmup, 1)):
         eng.step(1)
     t0 = time.perf_counter()
@@ -182,7 +183,8 @@ def run_reference(args):
                    "step": "one reference Engine.step() (1 substep) per bench step"},
         "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
                          "sample": f"{args.steps} Verlet steps of the {scene.spring_count}-spring cube, "
-                                   f"parallel-det (Alg.1 slots) restated in C/OpenMP"},
+                                   f"the reference bench's default parallel mode (Alg.1 atomic slots) "
+                                   f"restated in C/OpenMP"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -286,7 +288,7 @@ def run_single(args):
         sv, ssteps, swall, _ = cpu_sample(scene, target_s=3.0, max_steps=20, mode="serial")
         cpu = {"value": cv, "unit": "spring-updates/s", "cores": cthreads, "kind": "port",
                "sample": f"{csteps} Verlet steps ({cwall:.1f} s) of the same {S}-spring cube, "
-                         f"reference parallel-det Alg.1 schedule restated in C/OpenMP",
+                         f"the reference bench's default parallel mode (Alg.1 atomic slots) restated in C/OpenMP",
                "host_threads": os.cpu_count(),
                "serial_1core": {"value": sv, "unit": "spring-updates/s", "cores": 1,
                                 "sample": f"{ssteps} Verlet steps ({swall:.1f} s), the reference's serial mode"}}

@@ -14,7 +14,9 @@
  *   accumulate_springs_serial   _kernels.py:44-71        -> springs_serial()
  *   fill_slots / sum_slots      _kernels.py:74-155       -> springs_slots() (OpenMP,
  *        int64 atomic slot reservation, per-mass insertion sort by spring id:
- *        the "parallel-det" mode, bitwise equal to serial)
+ *        the "parallel-det" mode, bitwise equal to serial; without the sort:
+ *        the "parallel" mode, the reference bench's default, summed in slot
+ *        arrival order)
  *   Engine._rest_lengths        engine.py:250-259        -> rest_lengths()
  *   Engine.forces               engine.py:261-289        -> oracle_forces()
  *   Engine._step_euler/_verlet/_rk4  engine.py:303-354   -> step_*()
@@ -117,7 +119,7 @@ static int64_t springs_slots(oracle_engine *e, const double *x, double *acc) {
         const int64_t c = e->counter[i];
         int64_t *ss = e->slot_spring + i * stride;
         double *sl = e->slots + i * stride * 3;
-        for (int64_t a = 1; a < c; ++a) {
+        for (int64_t a = 1; a < c && e->mode == 1; ++a) {     /* parallel-det only: sort */
             const int64_t sid = ss[a];
             const double f0 = sl[3 * a], f1 = sl[3 * a + 1], f2 = sl[3 * a + 2];
             int64_t b = a - 1;

@@ -13,5 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
    --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-fp64 > gpurun_out/ncu_launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-tile_lean} -s 30 -c 1 \
    -o gpurun_out/prof python bench.py --steps 1 --warmup 3 --no-cpu --no-fp64 > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 \
+   -o gpurun_out/prof_f64 python tools/f64_probe.py > gpurun_out/ncu_f64.log 2>&1
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log
 cat gpurun_out/bench.log gpurun_out/bench_ref.log
