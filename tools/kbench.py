@@ -1,9 +1,10 @@
 """Per-substep time of the fp32 tile kernel variants on the 10M cube (dev tool).
 
-    VARIANTS="once:3,once:2,step2,once+SS_DEBUG=1" CELLS=91 python tools/kbench.py
+    VARIANTS="lean,lean+SS_PDL=0,step1,lean+SS_TILE_DICT=0,lean+SS_DEBUG=1" CELLS=91 python tools/kbench.py
 
-Each variant is SS_KERNEL[:SS_ONCE_MINB][+ENV=VAL...]; the engine reads
-these variables at creation.
+Each variant is SS_KERNEL[+ENV=VAL...] (SS_KERNEL: lean = tile_f32.cuh
+tile_lean_kernel, step1 = kernels.cuh step_kernel); the engine reads these
+variables at creation.
 Also prints max |x - x_first| against the first variant after the timed run
 (same inputs, fp32: the variants differ only in summation order)."""
 import json
@@ -21,7 +22,7 @@ integ = os.environ.get("INTEG", "verlet")
 n_steps = int(os.environ.get("NSTEPS", "200"))
 scene = L.excite(L.block_scene(cells), seed=11)
 first = None
-for var in os.environ.get("VARIANTS", "once:3,once:2,step2").split(","):
+for var in os.environ.get("VARIANTS", "lean,step1").split(","):
     head, *extra = var.split("+")
     name, _, minb = head.partition(":")
     for k in ("SS_DEBUG", "SS_ONCE_MINB", "SS_LEAN_MINB", "SS_TILE_DICT", "SS_TILE_SORT", "SS_PDL", "SS_KERNEL"):
