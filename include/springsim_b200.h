@@ -240,19 +240,22 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
  *   - ss_nccl_unique_id + ss_halo_nccl: one process per GPU; after every
  *     substep ss_step packs, exchanges (ncclSend/ncclRecv on the engine
  *     stream) and unpacks the planes;
- *   - ss_halo_p2p_export + ss_halo_p2p_attach: one process per GPU on one
- *     node; every substep the engine pushes its boundary planes into the
- *     neighbours' mailboxes over peer memory (CUDA IPC, NVLink stores) and
- *     lands the planes its neighbours pushed (device-side flags, no host
- *     round trip, no NCCL).  export returns a 256-byte blob (IPC handle of
- *     this engine's mailbox + plane sizes + step) for the neighbours; attach
- *     maps a neighbour's blob as side 0 (lower) or 1 (upper).  Replaces the
- *     NCCL transport; the reference has no multi-GPU path.
+ *   - ss_halo_p2p_export + ss_halo_recv_slots + ss_halo_p2p_attach: one
+ *     process per GPU on one node; the step kernel itself stores its
+ *     boundary planes into the neighbours' position buffers over peer
+ *     memory (CUDA IPC, NVLink stores) and synchronises through device-side
+ *     step flags -- no extra kernel, no host round trip, no NCCL.  export
+ *     returns a 256-byte blob (IPC handles of this engine's flag mailbox and
+ *     position buffers, plane sizes, step); recv_slots gives this engine's
+ *     device slots of its halo plane on `side`; attach maps a neighbour's
+ *     blob as side 0 (lower) or 1 (upper) together with the neighbour's
+ *     recv_slots for the facing plane.  The reference has no multi-GPU path
+ *     (SURVEY §8e).
  *   - ss_halo_p2p_link: the same transport between engines of one process
  *     (same device or peer-accessible devices), without IPC;
  *   - ss_step_group: several shards on one device stepped in lockstep, the
- *     planes copied device-to-device or, when peer-linked, pushed and landed
- *     through the mailboxes (virtual shards, for testing).
+ *     planes copied device-to-device or, when peer-linked, exchanged by the
+ *     step kernels (virtual shards, for testing).
  */
 int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
                   const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,
@@ -260,7 +263,9 @@ int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64
 int ss_nccl_unique_id(unsigned char id[128]);
 int ss_halo_nccl(ss_engine *h, const unsigned char id[128], int nranks, int rank, int rank_lo, int rank_hi);
 int ss_halo_p2p_export(ss_engine *h, unsigned char blob[256]);
-int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256]);
+int ss_halo_recv_slots(ss_engine *h, int side, int32_t *out);
+int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256], const int32_t *peer_slots,
+                       int64_t n_slots);
 int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer);
 int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res);
 

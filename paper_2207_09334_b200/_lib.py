@@ -96,7 +96,8 @@ SIGNATURES = {
     "ss_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "ss_halo_nccl": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ss_halo_p2p_export": (C.c_int, [C.c_void_p, C.c_char_p]),
-    "ss_halo_p2p_attach": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p]),
+    "ss_halo_recv_slots": (C.c_int, [C.c_void_p, C.c_int, _i32p]),
+    "ss_halo_p2p_attach": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _i32p, C.c_int64]),
     "ss_halo_p2p_link": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ss_step_group": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.POINTER(StepResult)]),
     "ss_lattice_box": (C.c_int, [_dp, _dp, C.c_double, C.c_double, C.c_double,

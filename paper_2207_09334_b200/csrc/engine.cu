@@ -141,10 +141,13 @@ struct ss_engine {
     // or, for shards of one process, plain) mailboxes and their plane sizes
     void *mailbox = nullptr;
     void *peer_mailbox[2] = {nullptr, nullptr};
+    void *peer_X[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][buffer]
     bool peer_ipc[2] = {false, false};
-    int64_t peer_n_recv[2][2] = {{0, 0}, {0, 0}};
+    std::vector<int32_t> peer_recv[2];          // the neighbour's device slots for this shard's planes
+    std::vector<int32_t> halo_send_host[2], halo_recv_host[2];   // this shard's plane slots
+    unsigned char *d_tile_role = nullptr;
+    int2 *d_peer_slot = nullptr;
     bool p2p_on = false;
-    bool group_mode = false;       // ss_step_group orders the exchange itself
     // CTA-resident small-scene kernel (resident.cuh): record image and launch shape
     void *res_image = nullptr;
     unsigned res_image_bytes = 0, res_off[4] = {0, 0, 0, 0};
@@ -154,8 +157,12 @@ struct ss_engine {
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        for (int s = 0; s < 2; ++s)
-            if (peer_ipc[s] && peer_mailbox[s]) cudaIpcCloseMemHandle(peer_mailbox[s]);
+        for (int s = 0; s < 2; ++s) {
+            if (!peer_ipc[s]) continue;
+            if (peer_mailbox[s]) cudaIpcCloseMemHandle(peer_mailbox[s]);
+            for (void *b : peer_X[s])
+                if (b) cudaIpcCloseMemHandle(b);
+        }
         if (nccl) {
             if (const NcclApi *api = nccl_api()) api->commDestroy(nccl);
         }
@@ -435,63 +442,23 @@ int with_layout(const ss_engine *h, Fn &&fn) {
 // After a substep: pack the boundary planes of the new positions, exchange
 // them with the neighbouring ranks (NCCL send/recv on the engine stream) and
 // write the received planes into the halo slots.
-// Byte offset of side `side`, parity `par` plane buffer in a mailbox whose
-// owner receives n_recv[0] / n_recv[1] masses from its lower / upper side.
-inline size_t mailbox_plane(const int64_t n_recv[2], int side, int par, size_t vec) {
-    size_t off = kMailboxHead;
-    if (side == 1) off += 2 * (size_t)n_recv[0] * vec;
-    return off + (size_t)par * (size_t)n_recv[side] * vec;
-}
-
-template <typename T4>
-int p2p_push(ss_engine *h, long long step) {
-    PushArgs<T4> a{};
-    a.X = reinterpret_cast<const T4 *>(h->X[h->cur]);
-    int blocks[2] = {0, 0};
+// Exchange fields of one step's Params (fused peer-memory transport): the
+// neighbours' buffers for this step's output parity, the flag words.
+template <typename T>
+void xchg_params(const ss_engine *h, Params<T> &p) {
+    using T4 = typename Params<T>::T4;
+    MailboxHead *mine = reinterpret_cast<MailboxHead *>(h->mailbox);
+    p.xchg = 1;
+    p.tile_role = h->d_tile_role;
+    p.peer_slot = h->d_peer_slot;
     for (int s = 0; s < 2; ++s) {
-        if (!h->peer_mailbox[s]) continue;
-        unsigned char *pm = reinterpret_cast<unsigned char *>(h->peer_mailbox[s]);
-        const int ps = 1 - s;                               // the neighbour receives on its other side
-        a.send_idx[s] = h->halo_send_idx[s];
-        a.n_send[s] = h->halo_n_send[s];
-        a.peer_buf[s] = reinterpret_cast<T4 *>(pm + mailbox_plane(h->peer_n_recv[s], ps, (int)(step & 1), sizeof(T4)));
-        a.peer_flag[s] = &reinterpret_cast<MailboxHead *>(pm)->flag[ps];
-        a.counter[s] = &reinterpret_cast<MailboxHead *>(h->mailbox)->counter[s];
-        blocks[s] = std::max(1, (h->halo_n_send[s] + 255) / 256);
+        p.peer_out[s] = h->peer_mailbox[s] ? reinterpret_cast<T4 *>(h->peer_X[s][h->cur ^ 1]) : nullptr;
+        p.peer_flag[s] = h->peer_mailbox[s] ? &reinterpret_cast<MailboxHead *>(h->peer_mailbox[s])->flag[1 - s]
+                                            : nullptr;
+        p.my_flag[s] = &mine->flag[s];
     }
-    a.blocks0 = blocks[0];
-    a.step = step;
-    if (blocks[0] + blocks[1] == 0) return SS_OK;
-    halo_push_kernel<T4><<<blocks[0] + blocks[1], 256, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-    h->launches += 1;
-    return SS_OK;
-}
-
-template <typename T4>
-int p2p_land(ss_engine *h, long long step) {
-    LandArgs<T4> a{};
-    a.X = reinterpret_cast<T4 *>(h->X[h->cur]);
-    unsigned char *mb = reinterpret_cast<unsigned char *>(h->mailbox);
-    const int64_t nr[2] = {h->halo_n_recv[0], h->halo_n_recv[1]};
-    int blocks[2] = {0, 0};
-    for (int s = 0; s < 2; ++s) {
-        if (!h->peer_mailbox[s]) continue;
-        a.recv_idx[s] = h->halo_recv_idx[s];
-        a.n_recv[s] = h->halo_n_recv[s];
-        a.buf[s] = reinterpret_cast<const T4 *>(mb + mailbox_plane(nr, s, (int)(step & 1), sizeof(T4)));
-        a.flag[s] = &reinterpret_cast<MailboxHead *>(mb)->flag[s];
-        blocks[s] = std::max(1, (h->halo_n_recv[s] + 255) / 256);
-    }
-    a.error = &reinterpret_cast<MailboxHead *>(mb)->error;
-    a.blocks0 = blocks[0];
-    a.step = step;
-    if (blocks[0] + blocks[1] == 0) return SS_OK;
-    halo_land_kernel<T4><<<blocks[0] + blocks[1], 256, 0, h->stream>>>(a);
-    CK(cudaGetLastError());
-    h->launches += 1;
-    h->halo_exchanges += 1;
-    return SS_OK;
+    p.done_ctas = &mine->counter[0];
+    p.xchg_error = &mine->error;
 }
 
 template <typename T4>
@@ -649,6 +616,7 @@ int launch_steps(ss_engine *h, int64_t count) {
     }
     for (int64_t s = 0; s < count; ++s) {
         p.step = h->n + s + 1;
+        if (h->p2p_on) xchg_params(h, p);                  // fused peer-memory exchange (kernels.cuh)
         T4 *Xc = reinterpret_cast<T4 *>(h->X[h->cur]);
         T4 *Xo = reinterpret_cast<T4 *>(h->X[h->cur ^ 1]);
         T4 *V = reinterpret_cast<T4 *>(h->V);
@@ -684,10 +652,6 @@ int launch_steps(ss_engine *h, int64_t count) {
             if (h->integrator == SS_VERLET) h->has_prev = true;
             if (h->nccl) {                                   // boundary planes -> neighbours' halos
                 int rc = halo_exchange_nccl<T4>(h);
-                if (rc) return rc;
-            } else if (h->p2p_on && !h->group_mode) {        // ... over peer memory (halo.cuh)
-                int rc = p2p_push<T4>(h, p.step);
-                if (!rc) rc = p2p_land<T4>(h, p.step);
                 if (rc) return rc;
             }
         } else {
@@ -1903,6 +1867,8 @@ extern "C" int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *sen
         }
         h->halo_n_send[s] = (int)ns[s];
         h->halo_n_recv[s] = (int)nr[s];
+        h->halo_send_host[s] = si;
+        h->halo_recv_host[s] = ri;
         void *p;
         if ((rc = h->alloc(&p, si.size() * sizeof(int)))) return rc;
         h->halo_send_idx[s] = (int *)p;
@@ -1947,11 +1913,12 @@ extern "C" int ss_halo_nccl(ss_engine *h, const unsigned char id[128], int nrank
 
 namespace {
 
-constexpr char kMailboxMagic[8] = {'S', 'S', 'M', 'B', 'O', 'X', '0', '1'};
+constexpr char kMailboxMagic[8] = {'S', 'S', 'M', 'B', 'O', 'X', '0', '2'};
 
 struct MailboxBlob {               // what ss_halo_p2p_export hands to the neighbours (256 B)
     char magic[8];
-    cudaIpcMemHandle_t handle;     // 64 B
+    cudaIpcMemHandle_t mailbox;    // 64 B each
+    cudaIpcMemHandle_t x[2];       // the two position buffers
     int64_t n_recv[2];
     int64_t vec;
     int64_t n;
@@ -1964,31 +1931,72 @@ int ensure_mailbox(ss_engine *h) {
     if (h->mailbox) return SS_OK;
     if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
     if (h->integrator == SS_RK4) return ss::fail(SS_EINVAL, "halo exchange supports Euler and Verlet");
-    const size_t vec = h->precision == SS_F32 ? sizeof(float4) : sizeof(double4);
-    const size_t bytes = kMailboxHead + 2 * (size_t)(h->halo_n_recv[0] + h->halo_n_recv[1]) * vec;
-    int rc = h->alloc(&h->mailbox, bytes);
+    int rc = h->alloc(&h->mailbox, kMailboxHead);
     if (rc) return rc;
     MailboxHead head{};
-    head.flag[0] = head.flag[1] = (long long)h->n;          // halos are consistent with the current state
-    CK(cudaMemset(h->mailbox, 0, bytes));
+    head.flag[0] = head.flag[1] = (long long)h->n;          // the halos match the current state
+    CK(cudaMemset(h->mailbox, 0, kMailboxHead));
     CK(cudaMemcpy(h->mailbox, &head, sizeof head, cudaMemcpyHostToDevice));
     return SS_OK;
 }
 
-int link_side(ss_engine *h, int side, void *peer_mailbox, bool ipc, const int64_t peer_n_recv[2], int64_t vec,
-              int64_t n, int cur) {
+// Per-slot push targets / ghost marks and per-CTA roles (kernels.cuh
+// xchg_*): bit 0 wait for the neighbours' previous step (the CTA reads a
+// ghost, as an own mass or through its halo, or pushes), bit 1 pushes, bit
+// 2 owns ghosts.
+int build_xchg(ss_engine *h) {
+    const int64_t ND = h->ND;
+    const int64_t nb = (ND + kBlockThreads - 1) / kBlockThreads;
+    std::vector<int2> ps((size_t)ND, make_int2(-1, -1));
+    for (int s = 0; s < 2; ++s)
+        for (int32_t slot : h->halo_recv_host[s]) ps[slot].x = -2;
+    for (int s = 0; s < 2; ++s) {
+        if (!h->peer_mailbox[s]) continue;
+        for (size_t k = 0; k < h->halo_send_host[s].size(); ++k) {
+            int2 &q = ps[h->halo_send_host[s][k]];
+            (s == 0 ? q.x : q.y) = h->peer_recv[s][k];
+        }
+    }
+    std::vector<unsigned char> role((size_t)nb, 0);
+    for (int64_t i = 0; i < ND; ++i) {
+        unsigned char &r = role[i / kBlockThreads];
+        if (ps[i].x >= 0 || ps[i].y >= 0) r |= 3;
+        if (ps[i].x == -2) r |= 5;
+    }
+    if (h->layout == SS_LAYOUT_TILE && !h->tl.blob.empty()) {
+        for (int64_t t = 0; t < h->tl.n_tiles && t < nb; ++t) {
+            TileHdr th;
+            std::memcpy(&th, h->tl.blob.data() + h->tl.off[t], sizeof th);
+            const int32_t *halo = reinterpret_cast<const int32_t *>(h->tl.blob.data() + h->tl.off[t] + th.off_halo);
+            for (uint32_t k = 0; k < th.n_halo && !(role[t] & 1); ++k)
+                if (halo[k] >= 0 && ps[halo[k]].x == -2) role[t] |= 1;
+        }
+    } else {
+        for (auto &r : role) r |= 1;                           // untiled layouts: every block may read a ghost
+    }
+    int rc;
+    if (!h->d_peer_slot && (rc = h->alloc(&h->d_peer_slot, ps.size() * sizeof(int2)))) return rc;
+    if (!h->d_tile_role && (rc = h->alloc(&h->d_tile_role, role.size()))) return rc;
+    if ((rc = upload(h, h->d_peer_slot, ps.data(), ps.size() * sizeof(int2)))) return rc;
+    return upload(h, h->d_tile_role, role.data(), role.size());
+}
+
+int link_side(ss_engine *h, int side, void *peer_mailbox, void *peer_x0, void *peer_x1, bool ipc,
+              const int64_t peer_n_recv[2], int64_t vec, int64_t n, int cur, const int32_t *peer_slots,
+              int64_t n_slots) {
     const int64_t my_vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
     if (vec != my_vec) return ss::fail(SS_EINVAL, "halo peer: precision differs");
     if (n != h->n || cur != h->cur) return ss::fail(SS_EINVAL, "halo peer: shards are not at the same step");
-    if (peer_n_recv[1 - side] != h->halo_n_send[side])
+    if (peer_n_recv[1 - side] != h->halo_n_send[side] || n_slots != h->halo_n_send[side])
         return ss::fail(SS_EINVAL, "halo peer: plane sizes disagree (%lld received, %d sent)",
                         (long long)peer_n_recv[1 - side], h->halo_n_send[side]);
     h->peer_mailbox[side] = peer_mailbox;
+    h->peer_X[side][0] = peer_x0;
+    h->peer_X[side][1] = peer_x1;
     h->peer_ipc[side] = ipc;
-    h->peer_n_recv[side][0] = peer_n_recv[0];
-    h->peer_n_recv[side][1] = peer_n_recv[1];
+    h->peer_recv[side].assign(peer_slots, peer_slots + n_slots);
     h->p2p_on = true;
-    return SS_OK;
+    return build_xchg(h);
 }
 
 }  // namespace
@@ -2000,7 +2008,9 @@ extern "C" int ss_halo_p2p_export(ss_engine *h, unsigned char blob[256]) {
     if (rc || (rc = ensure_mailbox(h))) return rc;
     MailboxBlob b{};
     std::memcpy(b.magic, kMailboxMagic, 8);
-    CK(cudaIpcGetMemHandle(&b.handle, h->mailbox));
+    CK(cudaIpcGetMemHandle(&b.mailbox, h->mailbox));
+    CK(cudaIpcGetMemHandle(&b.x[0], h->X[0]));
+    CK(cudaIpcGetMemHandle(&b.x[1], h->X[1]));
     b.n_recv[0] = h->halo_n_recv[0];
     b.n_recv[1] = h->halo_n_recv[1];
     b.vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
@@ -2012,34 +2022,51 @@ extern "C" int ss_halo_p2p_export(ss_engine *h, unsigned char blob[256]) {
     return SS_OK;
 }
 
-extern "C" int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256]) {
-    if (!h || !blob || side < 0 || side > 1) return ss::fail(SS_EINVAL, "ss_halo_p2p_attach: bad argument");
+extern "C" int ss_halo_recv_slots(ss_engine *h, int side, int32_t *out) {
+    if (!h || side < 0 || side > 1 || (!out && h->halo_n_recv[side]))
+        return ss::fail(SS_EINVAL, "ss_halo_recv_slots: bad argument");
+    if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
+    std::memcpy(out, h->halo_recv_host[side].data(), h->halo_recv_host[side].size() * sizeof(int32_t));
+    return SS_OK;
+}
+
+extern "C" int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256], const int32_t *peer_slots,
+                                  int64_t n_slots) {
+    if (!h || !blob || side < 0 || side > 1 || (n_slots && !peer_slots))
+        return ss::fail(SS_EINVAL, "ss_halo_p2p_attach: bad argument");
     MailboxBlob b;
     std::memcpy(&b, blob, sizeof b);
     if (std::memcmp(b.magic, kMailboxMagic, 8) != 0) return ss::fail(SS_EINVAL, "ss_halo_p2p_attach: not a mailbox blob");
     CK(cudaSetDevice(h->device));
     int rc = sync_pending(h);
     if (rc || (rc = ensure_mailbox(h))) return rc;
-    void *pm = nullptr;
-    const cudaError_t e = cudaIpcOpenMemHandle(&pm, b.handle, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess)
-        return ss::fail(SS_ECUDA, "cudaIpcOpenMemHandle (neighbour on device %d): %s", b.device, cudaGetErrorString(e));
-    rc = link_side(h, side, pm, true, b.n_recv, b.vec, b.n, b.cur);
-    if (rc) cudaIpcCloseMemHandle(pm);
+    void *pm[3] = {nullptr, nullptr, nullptr};
+    const cudaIpcMemHandle_t hs[3] = {b.mailbox, b.x[0], b.x[1]};
+    for (int i = 0; i < 3; ++i) {
+        const cudaError_t e = cudaIpcOpenMemHandle(&pm[i], hs[i], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(pm[j]);
+            return ss::fail(SS_ECUDA, "cudaIpcOpenMemHandle (neighbour on device %d): %s", b.device,
+                            cudaGetErrorString(e));
+        }
+    }
+    rc = link_side(h, side, pm[0], pm[1], pm[2], true, b.n_recv, b.vec, b.n, b.cur, peer_slots, n_slots);
+    if (rc)
+        for (void *q : pm) cudaIpcCloseMemHandle(q);
     return rc;
 }
 
 extern "C" int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer) {
     if (!h || !peer || side < 0 || side > 1) return ss::fail(SS_EINVAL, "ss_halo_p2p_link: bad argument");
+    if (!peer->halo_on) return ss::fail(SS_EINVAL, "ss_halo_p2p_link: the peer has no halo");
     if (peer->device != h->device) {
         int ok = 0;
         CK(cudaDeviceCanAccessPeer(&ok, h->device, peer->device));
         if (!ok) return ss::fail(SS_EINVAL, "ss_halo_p2p_link: device %d cannot access device %d", h->device, peer->device);
         CK(cudaSetDevice(h->device));
         const cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
-        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
             return ss::fail(SS_ECUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
-        }
         cudaGetLastError();
     }
     CK(cudaSetDevice(peer->device));
@@ -2049,7 +2076,9 @@ extern "C" int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer) {
     if ((rc = sync_pending(h)) || (rc = ensure_mailbox(h))) return rc;
     const int64_t pnr[2] = {peer->halo_n_recv[0], peer->halo_n_recv[1]};
     const int64_t vec = peer->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
-    return link_side(h, side, peer->mailbox, false, pnr, vec, peer->n, peer->cur);
+    const std::vector<int32_t> &slots = peer->halo_recv_host[1 - side];
+    return link_side(h, side, peer->mailbox, peer->X[0], peer->X[1], false, pnr, vec, peer->n, peer->cur,
+                     slots.data(), (int64_t)slots.size());
 }
 
 // Step n same-device shards in lockstep; shard k's upper side is shard k+1's
@@ -2081,7 +2110,6 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             rc = ss::fail(SS_EINVAL, "ss_step_group: mix of peer-linked and unlinked shards");
             break;
         }
-        hs[k]->group_mode = true;
     }
     for (int64_t s = 0; s < count && rc == SS_OK; ++s) {
         for (int k = 0; k < n && rc == SS_OK; ++k) {
@@ -2089,13 +2117,7 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             hs[k]->n += 1;
             hs[k]->t = (double)hs[k]->n * hs[k]->dt;
         }
-        if (p2p) {                   // every shard pushes, then every shard lands (one stream)
-            for (int k = 0; k < n && rc == SS_OK; ++k)
-                rc = f32 ? p2p_push<float4>(hs[k], hs[k]->n) : p2p_push<double4>(hs[k], hs[k]->n);
-            for (int k = 0; k < n && rc == SS_OK; ++k)
-                rc = f32 ? p2p_land<float4>(hs[k], hs[k]->n) : p2p_land<double4>(hs[k], hs[k]->n);
-            continue;
-        }
+        if (p2p) continue;           // the step kernels exchanged the planes themselves
         for (int k = 0; k + 1 < n && rc == SS_OK; ++k) {
             ss_engine *a = hs[k], *b = hs[k + 1];
             const int na = a->halo_n_send[1], nb = b->halo_n_send[0];
@@ -2132,9 +2154,6 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             *res = r;
         }
     }
-    for (int k = 0; k < n; ++k) {
-        hs[k]->stream = saved[k];
-        hs[k]->group_mode = false;
-    }
+    for (int k = 0; k < n; ++k) hs[k]->stream = saved[k];
     return first_err;
 }

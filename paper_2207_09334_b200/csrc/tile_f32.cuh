@@ -75,7 +75,9 @@ __device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V
 #pragma unroll
         for (int c = 0; c < 3; ++c) { xn[c] = x[c]; vn[c] = v[c]; un[c] = 0.f; }
     }
-    p.Xout[m] = make_float4(xn[0], xn[1], xn[2], x4.w);
+    const float4 xo = make_float4(xn[0], xn[1], xn[2], x4.w);
+    if (!xchg_store(p, m, xo)) return;                      // a ghost: its neighbour writes it
+    p.Xout[m] = xo;
     p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
     if constexpr (INTEG == 1) p.U[m] = make_float4(un[0], un[1], un[2], 0.f);
     if (!(finite3<true>(xn[0], xn[1], xn[2]) && finite3<true>(vn[0], vn[1], vn[2])))
@@ -209,6 +211,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     }
     // everything below reads the previous substep's state
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    xchg_wait(p);
     if (*p.div_step < p.step) return;                       // grid-uniform (an earlier step diverged)
     float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), hist = x4;
     if (active) {
@@ -256,6 +259,7 @@ __global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p)
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     lean_body<INTEG, GROUPS>(p, smem);
+    xchg_finish(p);
 }
 
 // Persistent cooperative variant for small scenes (kernels.cuh persist_step_kernel).

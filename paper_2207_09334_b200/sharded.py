@@ -117,13 +117,24 @@ def attach_peers(engine: Engine, rank: int, world: int) -> None:
     lib = _lib.lib()
     blob = C.create_string_buffer(256)
     _lib.check(lib.ss_halo_p2p_export(engine.handle, blob), "ss_halo_p2p_export")
-    blobs = [None] * world
-    dist.all_gather_object(blobs, bytes(blob.raw))
+    slots = []
+    for side in (0, 1):
+        n = engine._halo_keep[2 + side].shape[0]
+        a = np.zeros(n, dtype=np.int32)
+        _lib.check(lib.ss_halo_recv_slots(engine.handle, side, a.ctypes.data_as(C.POINTER(C.c_int32))),
+                   "ss_halo_recv_slots")
+        slots.append(a)
+    mine = (bytes(blob.raw), slots[0], slots[1])
+    got = [None] * world
+    dist.all_gather_object(got, mine)
     dist.barrier()                      # every mailbox exists before anyone maps it
-    if rank > 0:
-        _lib.check(lib.ss_halo_p2p_attach(engine.handle, 0, blobs[rank - 1]), "ss_halo_p2p_attach")
-    if rank + 1 < world:
-        _lib.check(lib.ss_halo_p2p_attach(engine.handle, 1, blobs[rank + 1]), "ss_halo_p2p_attach")
+    for side, peer in ((0, rank - 1), (1, rank + 1)):
+        if not 0 <= peer < world:
+            continue
+        pblob, p_lo, p_hi = got[peer]
+        facing = np.ascontiguousarray(p_hi if side == 0 else p_lo, dtype=np.int32)   # the neighbour's plane facing us
+        _lib.check(lib.ss_halo_p2p_attach(engine.handle, side, pblob, facing.ctypes.data_as(C.POINTER(C.c_int32)),
+                                          facing.shape[0]), "ss_halo_p2p_attach")
     dist.barrier()
 
 

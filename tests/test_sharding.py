@@ -139,18 +139,20 @@ def test_nccl_transport_self_loop():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("precision,layout", [("f64", "auto"), ("f32", "auto"), ("f64", "csr")])
 @pytest.mark.parametrize("shards", [2, 3])
-def test_peer_memory_shards_match_single_device(precision, shards):
-    """The peer-memory transport (mailboxes, push/land kernels and the
-    release/acquire step flags of the multi-GPU path, halo.cuh) between the
-    shards of one process: fp64 bitwise equal to one engine on the whole
-    cube, fp32 within fp32 rounding of the displacement."""
+def test_peer_memory_shards_match_single_device(precision, layout, shards):
+    """The fused peer-memory exchange of the multi-GPU path (step kernels
+    store boundary planes into the neighbours' buffers, release/acquire step
+    flags, ghost masses written only by their neighbour; kernels.cuh xchg_*)
+    between the shards of one process: fp64 bitwise equal to one engine on
+    the whole cube (tiled and CSR layouts), fp32 within fp32 rounding of the
+    displacement."""
     cells = 11
     full = L.excite(L.block_scene(cells), seed=11)
     v = excited_velocities(full.mass_count)
     one = Engine(full, precision=precision)
-    grp = ShardGroup(cells, shards, precision=precision, v_global=v, transport="p2p")
+    grp = ShardGroup(cells, shards, precision=precision, v_global=v, transport="p2p", layout=layout)
     one.step(41)
     grp.step(41)
     if precision == "f64":
