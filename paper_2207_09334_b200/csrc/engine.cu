@@ -121,6 +121,7 @@ struct ss_engine {
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
+    int lean_lanes = 1;            // threads per mass of that kernel (2: scenes with few tiles)
     int persist_max_grid = 0;      // co-resident CTAs of the persistent kernel (0: never persistent)
     bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
     int64_t device_bytes = 0;
@@ -518,8 +519,11 @@ void launch_pdl(void (*k)(P), int grid, int block, size_t smem, cudaStream_t str
 template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
-    if (h->pdl) launch_pdl(k, grid, kTile, h->lean_smem, h->stream, p);      // tile_f32.cuh
-    else k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+    if (h->lean_lanes == 2)
+        k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS, 6, 2> : tile_lean_kernel<1, GROUPS, 6, 2>;
+    const int block = kTile * h->lean_lanes;
+    if (h->pdl) launch_pdl(k, grid, block, h->lean_smem, h->stream, p);      // tile_f32.cuh
+    else k<<<grid, block, h->lean_smem, h->stream>>>(p);
 }
 
 template <bool F32, int LAYOUT>
@@ -991,9 +995,24 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
+                // scenes with few tiles (at most 3 per SM) use two lanes per mass:
+                // 512-thread CTAs, twice the warps for the same tiles
+                int sms = 0;
+                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+                h->lean_lanes = L.n_tiles <= 3 * (int64_t)sms ? 2 : 1;
+                if (const char *e = getenv("SS_LEAN_LANES")) h->lean_lanes = atoi(e) == 2 ? 2 : 1;
+                if (h->lean_lanes == 2) {
+                    h->lean_smem += (size_t)kTile * sizeof(float4);        // lane 1's partial sums
+                    if ((int64_t)h->lean_smem > dev_max) {
+                        h->lean_lanes = 1;
+                        h->lean_smem = h->smem_bytes;
+                    }
+                }
                 const int b = dev_max;
                 for (auto *kk : {tile_lean_kernel<0, false>, tile_lean_kernel<1, false>, tile_lean_kernel<0, true>,
-                                 tile_lean_kernel<1, true>})
+                                 tile_lean_kernel<1, true>, tile_lean_kernel<0, false, 6, 2>,
+                                 tile_lean_kernel<1, false, 6, 2>, tile_lean_kernel<0, true, 6, 2>,
+                                 tile_lean_kernel<1, true, 6, 2>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }

@@ -107,9 +107,13 @@ __device__ __forceinline__ void acc3(V3<float> &s, float c, float dx, float dy, 
 // Spring sum of tile mass l over its incidence list (own springs first),
 // from the staged displacements sR.  Returns the number of degenerate own
 // springs.
-template <bool GROUPS>
+// LANES > 1: this thread takes incidences lane, lane + LANES, ... and the
+// caller combines the lanes' sums; dmin_out gets the smallest d^2 seen (the
+// degenerate recount, by lane 0, covers all own springs).
+template <bool GROUPS, int LANES = 1>
 __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const TileView &v, int l, const float4 &rm,
-                                                  int n_own, int n_inc, V3<float> &s) {
+                                                  int n_own, int n_inc, V3<float> &s, int lane = 0,
+                                                  float *dmin_out = nullptr) {
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(v.bl + v.h->off_oo) + l;
     const float4 *dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);   // 2 float4 per entry
     float dmin = INFINITY;
@@ -130,17 +134,21 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
         dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
         acc3(s, c, dx, dy, dz_);
     };
-    int q = 0;
+    int q = lane;
 #pragma unroll 1
-    for (; q + 3 < n_inc; q += 4) {
+    for (; q + 3 * LANES < n_inc; q += 4 * LANES) {
         body(q);
-        body(q + 1);
-        body(q + 2);
-        body(q + 3);
+        body(q + LANES);
+        body(q + 2 * LANES);
+        body(q + 3 * LANES);
     }
 #pragma unroll 1
-    for (; q < n_inc; ++q) body(q);
+    for (; q < n_inc; q += LANES) body(q);
     unsigned deg = 0;
+    if (dmin_out) {
+        *dmin_out = dmin;
+        return 0;
+    }
     if (dmin < 1e-24f) {                                    // rare: count the degenerate own springs
         for (int r = 0; r < n_own; ++r) {
             const uint32_t e = inc[r << 8];
@@ -180,10 +188,15 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
 // so the next grid's CTAs fill the SM slots freed during this grid's tail and
 // stream their (step-independent) record blobs by TMA before they wait for
 // this grid's positions (griddepcontrol.wait).
-template <int INTEG, bool GROUPS>
+// LANES = 2 (scenes with few tiles): 512 threads per tile; thread t works on
+// mass l = t mod 256 with lane t / 256 taking every other incidence, and the
+// lanes' sums meet in shared memory in a fixed order -- twice the warps for
+// the same tiles, for scenes too small to fill the GPU.
+template <int INTEG, bool GROUPS, int LANES = 1>
 __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char *smem) {
     const Topology<float> &t = p.topo;
-    const int l = threadIdx.x;
+    const int tid = threadIdx.x;
+    const int l = tid % kTile, lane = tid / kTile;
     const int m = blockIdx.x * kTile + l;
     const int n = (int)(__ldg(t.tsplit + blockIdx.x) >> 24) + 1;
     const bool active = l < n;
@@ -191,7 +204,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     unsigned char *bl = smem + 128;
     float4 *sR = reinterpret_cast<float4 *>(bl + t.blob_smem);
-    if (l == 0) {
+    if (tid == 0) {
         if (p.reinit) {                                     // persistent kernel: re-arm completed barriers
             asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)));
             asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar + 1)));
@@ -201,7 +214,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (l == 0) {
+    if (tid == 0) {
         const int tb = p.debug == 2 ? 0 : blockIdx.x;       // debug 2: every CTA stages tile 0 (L2-resident)
         const unsigned long long g0 = t.toff[tb];
         const uint32_t bytes = (uint32_t)(t.toff[tb + 1] - g0);
@@ -214,7 +227,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     xchg_wait(p);
     if (*p.div_step < p.step) return;                       // grid-uniform (an earlier step diverged)
     float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), hist = x4;
-    if (active) {
+    if (active && lane == 0) {
         x4 = ldg4(p.X + m);                                 // r = x - X0, w = +-m
         hist = need_prev ? ldg4(p.Xprev + m) : ldg4(p.V + m);
         sR[l] = x4;
@@ -226,39 +239,64 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         const int nh = (int)v.h->n_halo;
         // up to 3 x 256 halo slots (compact format): all loads in flight
         // before the first store, one memory latency instead of three
-        float4 hv[3];
+        constexpr int J = (3 + LANES - 1) / LANES;
+        float4 hv[J];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const int i = l + j * kTile;
+        for (int j = 0; j < J; ++j) {
+            const int i = tid + j * kTile * LANES;
             const int gm = i < nh ? halo[i] : -1;           // -1: beyond the list or a hole
             hv[j] = gm >= 0 ? ldg4(p.X + gm) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const int i = l + j * kTile;
+        for (int j = 0; j < J; ++j) {
+            const int i = tid + j * kTile * LANES;
             if (i < nh) sR[kTile + i] = hv[j];
         }
 #pragma unroll 1
-        for (int i = l + 3 * kTile; i < nh; i += kTile) {   // (not reached by compact tiles)
+        for (int i = tid + J * kTile * LANES; i < nh; i += kTile * LANES) {   // (not reached by compact tiles)
             const int gm = halo[i];
             if (gm >= 0) sR[kTile + i] = ldg4(p.X + gm);
         }
     }
     mbar_wait_warp0(bar + 1, 0);                            // records (+ the staged states)
-    if (!active) return;
     V3<float> s = {0.f, 0.f, 0.f};
-    if (p.debug != 1) {
-        const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
-        flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt >> 8, s));
+    if constexpr (LANES == 1) {
+        if (!active) return;
+        if (p.debug != 1) {
+            const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
+            flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt >> 8, s));
+        }
+    } else {
+        // lane 1's partial sums (and its smallest d^2) meet lane 0's in shared
+        // memory behind the halo, in a fixed order
+        float4 *part = sR + kTile + t.max_halo;
+        float dmin = INFINITY;
+        uint16_t cnt = 0;
+        if (active) {
+            if (lane) x4 = sR[l];
+            cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
+            if (p.debug != 1) incidence_sum<GROUPS, LANES>(p, v, l, x4, cnt & 0xff, cnt >> 8, s, lane, &dmin);
+            if (lane) part[l] = make_float4(s.x, s.y, s.z, dmin);
+        }
+        __syncthreads();
+        if (!active || lane) return;
+        const float4 o = part[l];
+        s.x = s.x + o.x;
+        s.y = s.y + o.y;
+        s.z = s.z + o.z;
+        if (fminf(dmin, o.w) < 1e-24f && p.debug != 1) {  // rare: recount the degenerate own springs
+            V3<float> junk = {0.f, 0.f, 0.f};
+            flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt & 0xff, junk));
+        }
     }
     tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
 }
 
-template <int INTEG, bool GROUPS, int MINB = 6>
-__global__ void __launch_bounds__(kTile, MINB) tile_lean_kernel(Params<float> p) {
+template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1>
+__global__ void __launch_bounds__(kTile * LANES, LANES == 1 ? MINB : 3) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    lean_body<INTEG, GROUPS>(p, smem);
+    lean_body<INTEG, GROUPS, LANES>(p, smem);
     xchg_finish(p);
 }
 
