@@ -222,3 +222,20 @@ def test_fp32_explicit_tile_format(case, monkeypatch):
     from paper_2207_09334_b200.engine import plan  # noqa: F401  (format check below)
     d, eng = run_engine(case, "tile", precision="f32")
     assert eng.info()["tile_kernel"] in (0, 1)      # explicit records, kernels.cuh step_kernel
+
+
+@pytest.mark.parametrize("lanes", ["1", "2"])
+def test_degenerate_springs_in_tiled_fp32(lanes, monkeypatch):
+    """Coincident endpoints in a multi-tile fp32 scene: the spring is skipped
+    and counted once per step by either lean-kernel shape (one or two lanes
+    per mass), like the reference (_kernels.py:58-60)."""
+    monkeypatch.setenv("SS_LEAN_LANES", lanes)
+    scene = L.block_scene(12)
+    s0 = 5000
+    i, j = int(scene.si[s0]), int(scene.sj[s0])
+    scene.x[j] = scene.x[i]                   # spring s0 now has L = 0
+    eng = Engine(scene, integrator="verlet", precision="f32")
+    assert eng.info()["tile_kernel"] == 2
+    eng.step(1)
+    assert eng.degenerate_springs == 1
+    assert np.isfinite(eng.x).all()
