@@ -147,7 +147,7 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const type
                 if (len < 1e-12) {                          // skipped and counted (_kernels.py:58-60)
                     if (e & 0x1000u) ++deg;
                 } else {
-                    const double c = (kl.x * (len - l0)) / len;
+                    const double c = spring_c64(kl.x, len, l0);
                     fx = c * dx;
                     fy = c * dy;
                     fz = c * dz;
