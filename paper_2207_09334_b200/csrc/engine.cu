@@ -665,18 +665,24 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.V0 = V;
             p.SV = reinterpret_cast<T4 *>(h->SV);
             p.SA = reinterpret_cast<T4 *>(h->SA);
+            // tiles: stages chained by programmatic dependent launch (the
+            // kernel waits in stage_tile before its first state read)
+            auto rk4_launch = [&](void (*k)(Params<T>)) {
+                if (LAYOUT >= 3 && h->pdl) launch_pdl(k, grid, kBlock, smem, h->stream, p);
+                else k<<<grid, kBlock, smem, h->stream>>>(p);
+            };
             p.scale = G ? scale + ((size_t)s * 4 + 0) * G : nullptr;
             p.X = Xc; p.V = V; p.Xout = XA; p.Vout = VS;
-            rk4_kernel<F32, 1, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            rk4_launch(rk4_kernel<F32, 1, LAYOUT>);
             p.scale = G ? scale + ((size_t)s * 4 + 1) * G : nullptr;
             p.X = XA; p.V = VS; p.Xout = XB; p.Vout = VS;
-            rk4_kernel<F32, 2, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            rk4_launch(rk4_kernel<F32, 2, LAYOUT>);
             p.scale = G ? scale + ((size_t)s * 4 + 2) * G : nullptr;
             p.X = XB; p.V = VS; p.Xout = XA; p.Vout = VS;
-            rk4_kernel<F32, 3, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            rk4_launch(rk4_kernel<F32, 3, LAYOUT>);
             p.scale = G ? scale + ((size_t)s * 4 + 3) * G : nullptr;
             p.X = XA; p.V = VS; p.Xout = Xc; p.Vout = V;
-            rk4_kernel<F32, 4, LAYOUT><<<grid, kBlock, smem, h->stream>>>(p);
+            rk4_launch(rk4_kernel<F32, 4, LAYOUT>);
             h->launches += 4;
         }
     }
