@@ -1,5 +1,7 @@
+"""Per-iteration timing of the public-API loop (set state, step 100, read x) on the 10M cube;
+WITH_TORCH=1 adds a device timeline of one step (dev tool)."""
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 if os.environ.get("WITH_TORCH"):
     import torch

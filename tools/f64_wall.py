@@ -1,5 +1,6 @@
-import time, sys
-sys.path.insert(0, "/root/repo")
+"""fp64 Engine.step(100) wall time on the 10M cube, at rest and excited (dev tool)."""
+import os, time, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2207_09334_b200 import Engine, lattice as L
 sc = L.block_scene(91)

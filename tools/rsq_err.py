@@ -1,3 +1,4 @@
+"""Relative error of fp32 rsqrt over lattice spring lengths (dev tool)."""
 import torch
 x = torch.rand(1 << 26, device="cuda", dtype=torch.float64) * 0.09 + 0.005   # d^2 of lattice springs (0.005..0.095)
 xf = x.float()
