@@ -138,8 +138,9 @@ struct ss_engine {
     ncclComm_t nccl = nullptr;
     int nccl_peer[2] = {-1, -1};
     int64_t halo_exchanges = 0;
-    // peer-memory transport (halo.cuh): own mailbox, the neighbours' (IPC-mapped
-    // or, for shards of one process, plain) mailboxes and their plane sizes
+    // fused peer-memory exchange (kernels.cuh xchg_*): own flag mailbox, the
+    // neighbours' mailboxes and position buffers (IPC-mapped or, for shards of
+    // one process, plain), their slots for this shard's planes
     void *mailbox = nullptr;
     void *peer_mailbox[2] = {nullptr, nullptr};
     void *peer_X[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][buffer]

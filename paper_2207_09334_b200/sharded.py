@@ -6,10 +6,11 @@ so a contiguous id range is a slab of whole x-planes.  Rank g owns planes
 (marked fixed) plus every spring touching an owned mass — with its GLOBAL id
 order preserved, so each owned mass sums its springs in the same order as on
 one device and the results are bitwise identical.  After every substep the
-first and last owned planes go to the neighbours' halo planes: pushed over
-peer memory into the neighbours' mailboxes and landed behind device-side
-flags (``attach_peers``, the default), or NCCL send/recv on the engine stream
-(``SS_HALO=nccl``), or device copies for same-device shards (``ShardGroup``).
+first and last owned planes go to the neighbours' halo planes: stored by the
+step kernel itself into the neighbours' position buffers over peer memory,
+synchronised by device-side step flags (``attach_peers``, the default), or
+NCCL send/recv on the engine stream (``SS_HALO=nccl``), or device copies for
+same-device shards (``ShardGroup``).
 """
 
 from __future__ import annotations
@@ -110,9 +111,10 @@ def attach_halo(engine: Engine, slab: Slab) -> None:
 
 def attach_peers(engine: Engine, rank: int, world: int) -> None:
     """Peer-memory halo transport between the ranks of a torch.distributed
-    group (one process per GPU, one node): every rank exports its mailbox
-    (CUDA IPC handle), the blobs are all-gathered over the host group, and
-    each rank maps its lower (rank-1) and upper (rank+1) neighbour's."""
+    group (one process per GPU, one node): every rank exports CUDA IPC
+    handles of its position buffers and flag mailbox plus the device slots
+    of its halo planes; these are all-gathered over the host group, and each
+    rank maps its lower (rank-1) and upper (rank+1) neighbour's."""
     import torch.distributed as dist
     lib = _lib.lib()
     blob = C.create_string_buffer(256)
@@ -141,8 +143,8 @@ def attach_peers(engine: Engine, rank: int, world: int) -> None:
 class ShardGroup:
     """k x-slab shards of one cube on ONE device, stepped in lockstep
     (the sharded code path in one process).  transport="copy": device-to-
-    device plane copies; "p2p": the peer-memory mailboxes and flags of the
-    multi-GPU transport (halo.cuh), linked without IPC."""
+    device plane copies; "p2p": the fused peer-memory exchange of the
+    multi-GPU transport (kernels.cuh xchg_*), linked without IPC."""
 
     def __init__(self, cells: int, shards: int, precision: str = "f64", layout: str = "auto",
                  v_global: np.ndarray | None = None, device: int = 0, transport: str = "copy"):
