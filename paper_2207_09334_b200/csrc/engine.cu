@@ -149,6 +149,7 @@ struct ss_engine {
     std::vector<int32_t> halo_send_host[2], halo_recv_host[2];   // this shard's plane slots
     unsigned char *d_tile_role = nullptr;
     int2 *d_peer_slot = nullptr;
+    int xchg_arrivals = 0;         // CTAs that read ghosts or push (kernels.cuh xchg_finish)
     bool p2p_on = false;
     // CTA-resident small-scene kernel (resident.cuh): record image and launch shape
     void *res_image = nullptr;
@@ -460,6 +461,7 @@ void xchg_params(const ss_engine *h, Params<T> &p) {
         p.my_flag[s] = &mine->flag[s];
     }
     p.done_ctas = &mine->counter[0];
+    p.xchg_arrivals = h->xchg_arrivals;
     p.xchg_error = &mine->error;
 }
 
@@ -2000,6 +2002,8 @@ int build_xchg(ss_engine *h) {
     } else {
         for (auto &r : role) r |= 1;                           // untiled layouts: every block may read a ghost
     }
+    h->xchg_arrivals = 0;
+    for (unsigned char r : role) h->xchg_arrivals += (r & 3) ? 1 : 0;
     int rc;
     if (!h->d_peer_slot && (rc = h->alloc(&h->d_peer_slot, ps.size() * sizeof(int2)))) return rc;
     if (!h->d_tile_role && (rc = h->alloc(&h->d_tile_role, role.size()))) return rc;
