@@ -149,6 +149,7 @@ struct ss_engine {
     std::vector<int32_t> halo_send_host[2], halo_recv_host[2];   // this shard's plane slots
     unsigned char *d_tile_role = nullptr;
     int2 *d_peer_slot = nullptr;
+    int *d_tile_order = nullptr;
     int xchg_arrivals = 0;         // CTAs that read ghosts or push (kernels.cuh xchg_finish)
     bool p2p_on = false;
     // CTA-resident small-scene kernel (resident.cuh): record image and launch shape
@@ -462,6 +463,7 @@ void xchg_params(const ss_engine *h, Params<T> &p) {
     }
     p.done_ctas = &mine->counter[0];
     p.xchg_arrivals = h->xchg_arrivals;
+    p.tile_order = h->d_tile_order;
     p.xchg_error = &mine->error;
 }
 
@@ -524,6 +526,8 @@ void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
     if (h->lean_lanes == 2)
         k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS, 6, 2> : tile_lean_kernel<1, GROUPS, 6, 2>;
+    else if (h->p2p_on)                                    // sharded: boundary tiles first
+        k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS, 6, 1, true> : tile_lean_kernel<1, GROUPS, 6, 1, true>;
     const int block = kTile * h->lean_lanes;
     if (h->pdl) launch_pdl(k, grid, block, h->lean_smem, h->stream, p);      // tile_f32.cuh
     else k<<<grid, block, h->lean_smem, h->stream>>>(p);
@@ -1021,7 +1025,9 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                 for (auto *kk : {tile_lean_kernel<0, false>, tile_lean_kernel<1, false>, tile_lean_kernel<0, true>,
                                  tile_lean_kernel<1, true>, tile_lean_kernel<0, false, 6, 2>,
                                  tile_lean_kernel<1, false, 6, 2>, tile_lean_kernel<0, true, 6, 2>,
-                                 tile_lean_kernel<1, true, 6, 2>})
+                                 tile_lean_kernel<1, true, 6, 2>, tile_lean_kernel<0, false, 6, 1, true>,
+                                 tile_lean_kernel<1, false, 6, 1, true>, tile_lean_kernel<0, true, 6, 1, true>,
+                                 tile_lean_kernel<1, true, 6, 1, true>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
@@ -2004,7 +2010,15 @@ int build_xchg(ss_engine *h) {
     }
     h->xchg_arrivals = 0;
     for (unsigned char r : role) h->xchg_arrivals += (r & 3) ? 1 : 0;
+    // fp32 lean kernel launch order: the tiles the neighbours wait on first
+    std::vector<int32_t> order;
+    order.reserve((size_t)nb);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int64_t b = 0; b < nb; ++b)
+            if (((role[b] & 3) != 0) == (pass == 0)) order.push_back((int32_t)b);
     int rc;
+    if (!h->d_tile_order && (rc = h->alloc(&h->d_tile_order, order.size() * sizeof(int32_t)))) return rc;
+    if ((rc = upload(h, h->d_tile_order, order.data(), order.size() * sizeof(int32_t)))) return rc;
     if (!h->d_peer_slot && (rc = h->alloc(&h->d_peer_slot, ps.size() * sizeof(int2)))) return rc;
     if (!h->d_tile_role && (rc = h->alloc(&h->d_tile_role, role.size()))) return rc;
     if ((rc = upload(h, h->d_peer_slot, ps.data(), ps.size() * sizeof(int2)))) return rc;

@@ -51,7 +51,8 @@ __device__ __forceinline__ float spring_c(float dx, float dy, float dz, float k,
 // check of device mass m (engine.py:273-328, 297-301, 375-381).
 template <int INTEG>
 __device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V3<float> sum, float4 x4,
-                                                float4 p4, float4 v4, float4 xp4, bool need_prev) {
+                                                float4 p4, float4 v4, float4 xp4, bool need_prev,
+                                                int tile = blockIdx.x) {
     const float mass = fabsf(x4.w);
     const bool fixed = signbit(x4.w);
     const V3<float> xa = {p4.x + x4.x, p4.y + x4.y, p4.z + x4.z};
@@ -76,7 +77,7 @@ __device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V
         for (int c = 0; c < 3; ++c) { xn[c] = x[c]; vn[c] = v[c]; un[c] = 0.f; }
     }
     const float4 xo = make_float4(xn[0], xn[1], xn[2], x4.w);
-    if (!xchg_store(p, m, xo)) return;                      // a ghost: its neighbour writes it
+    if (!xchg_store(p, m, xo, tile)) return;                // a ghost: its neighbour writes it
     p.Xout[m] = xo;
     p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
     if constexpr (INTEG == 1) p.U[m] = make_float4(un[0], un[1], un[2], 0.f);
@@ -168,12 +169,20 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
 // bootstrap, for friction, or to restore a fixed mass; P only for contact.
 template <int INTEG>
 __device__ __forceinline__ void tile_epilogue(const Params<float> &p, int m, const V3<float> &s, const float4 &x4,
-                                              const float4 &hist, bool need_prev) {
+                                              const float4 &hist, bool need_prev, int tile) {
     float4 v4 = need_prev ? make_float4(0.f, 0.f, 0.f, 0.f) : hist;
     if (need_prev && (p.n_planes > 0 || signbit(x4.w))) v4 = p.V[m];
     float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (p.n_planes > 0) p4 = p.P[m];
-    integrate_store<INTEG>(p, m, s, x4, p4, v4, hist, need_prev);
+    integrate_store<INTEG>(p, m, s, x4, p4, v4, hist, need_prev, tile);
+}
+
+// The tile of this CTA: sharded slabs run their boundary tiles first
+// (ORDERED, kernels.cuh xchg_*), so the neighbours' flags publish early.
+template <bool ORDERED>
+__device__ __forceinline__ int lean_tile(const Params<float> &p) {
+    if constexpr (ORDERED) return __ldg(p.tile_order + blockIdx.x);
+    else return (int)blockIdx.x;
 }
 
 // ------------------------------------------------------------------ lean
@@ -192,13 +201,14 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
 // mass l = t mod 256 with lane t / 256 taking every other incidence, and the
 // lanes' sums meet in shared memory in a fixed order -- twice the warps for
 // the same tiles, for scenes too small to fill the GPU.
-template <int INTEG, bool GROUPS, int LANES = 1>
+template <int INTEG, bool GROUPS, int LANES = 1, bool ORDERED = false>
 __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char *smem) {
     const Topology<float> &t = p.topo;
     const int tid = threadIdx.x;
     const int l = tid % kTile, lane = tid / kTile;
-    const int m = blockIdx.x * kTile + l;
-    const int n = (int)(__ldg(t.tsplit + blockIdx.x) >> 24) + 1;
+    const int tile = lean_tile<ORDERED>(p);
+    const int m = tile * kTile + l;
+    const int n = (int)(__ldg(t.tsplit + tile) >> 24) + 1;
     const bool active = l < n;
     const bool need_prev = INTEG == 1 && !p.bootstrap;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
@@ -215,7 +225,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     }
     __syncthreads();
     if (tid == 0) {
-        const int tb = p.debug == 2 ? 0 : blockIdx.x;       // debug 2: every CTA stages tile 0 (L2-resident)
+        const int tb = p.debug == 2 ? 0 : tile;             // debug 2: every CTA stages tile 0 (L2-resident)
         const unsigned long long g0 = t.toff[tb];
         const uint32_t bytes = (uint32_t)(t.toff[tb + 1] - g0);
         const uint32_t split = t.tsplit[tb] & 0xffffffu;
@@ -224,7 +234,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     }
     // everything below reads the previous substep's state
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    xchg_wait(p);
+    xchg_wait(p, tile);
     if (*p.div_step < p.step) return;                       // grid-uniform (an earlier step diverged)
     float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), hist = x4;
     if (active && lane == 0) {
@@ -289,15 +299,15 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
             flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt & 0xff, junk));
         }
     }
-    tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev);
+    tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev, tile);
 }
 
-template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1>
+template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1, bool ORDERED = false>
 __global__ void __launch_bounds__(kTile * LANES, LANES == 1 ? MINB : 3) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    lean_body<INTEG, GROUPS, LANES>(p, smem);
-    xchg_finish(p);
+    lean_body<INTEG, GROUPS, LANES, ORDERED>(p, smem);
+    xchg_finish(p, lean_tile<ORDERED>(p));
 }
 
 // Persistent cooperative variant for small scenes (kernels.cuh persist_step_kernel).
