@@ -147,11 +147,12 @@ class ShardGroup:
     multi-GPU transport (kernels.cuh xchg_*), linked without IPC."""
 
     def __init__(self, cells: int, shards: int, precision: str = "f64", layout: str = "auto",
-                 v_global: np.ndarray | None = None, device: int = 0, transport: str = "copy"):
+                 v_global: np.ndarray | None = None, device: int = 0, transport: str = "copy",
+                 integrator: str = "verlet"):
         nx = cells + 1
         self.slabs = [cube_slab(cells, *slab_planes(nx, shards, r), v_global=v_global)
                       for r in range(shards)]
-        self.engines = [Engine(s.scene, integrator="verlet", precision=precision, layout=layout,
+        self.engines = [Engine(s.scene, integrator=integrator, precision=precision, layout=layout,
                                device=device) for s in self.slabs]
         for e, s in zip(self.engines, self.slabs):
             attach_halo(e, s)

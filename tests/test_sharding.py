@@ -215,3 +215,23 @@ def test_peer_memory_shards_across_processes():
     v = np.concatenate([r[3] for r in res])
     assert x.tobytes() == ref_x.tobytes()
     assert v.tobytes() == ref_v.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_peer_memory_shards_euler(precision):
+    """The fused exchange under forward Euler (positions from the old
+    velocities): 3 shards, fp64 bitwise, fp32 to rounding."""
+    cells = 11
+    full = L.excite(L.block_scene(cells), seed=11)
+    v = excited_velocities(full.mass_count)
+    one = Engine(full, integrator="euler", precision=precision)
+    grp = ShardGroup(cells, 3, precision=precision, v_global=v, transport="p2p", integrator="euler")
+    one.step(29)
+    grp.step(29)
+    if precision == "f64":
+        assert grp.positions().tobytes() == one.x.tobytes()
+        assert grp.velocities().tobytes() == one.v.tobytes()
+    else:
+        disp = np.abs(one.x - full.x).max()
+        assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
