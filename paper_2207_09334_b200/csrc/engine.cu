@@ -521,6 +521,23 @@ void launch_pdl(void (*k)(P), int grid, int block, size_t smem, cudaStream_t str
     cudaLaunchKernelEx(&cfg, k, p);
 }
 
+// RK4 stage `stage` (1-4) of a fp32 compact-tile engine on the lean kernel
+// (tile_f32.cuh rk4_store), chained by programmatic dependent launch.
+template <bool GROUPS>
+void launch_rk4_lean(ss_engine *h, const Params<float> &p, int grid, int stage) {
+    const bool two = h->lean_lanes == 2;
+    void (*k)(Params<float>) = nullptr;
+    switch (stage) {
+        case 1: k = two ? tile_lean_kernel<2, GROUPS, 6, 2> : tile_lean_kernel<2, GROUPS>; break;
+        case 2: k = two ? tile_lean_kernel<3, GROUPS, 6, 2> : tile_lean_kernel<3, GROUPS>; break;
+        case 3: k = two ? tile_lean_kernel<4, GROUPS, 6, 2> : tile_lean_kernel<4, GROUPS>; break;
+        default: k = two ? tile_lean_kernel<5, GROUPS, 6, 2> : tile_lean_kernel<5, GROUPS>; break;
+    }
+    const int block = kTile * h->lean_lanes;
+    if (h->pdl) launch_pdl(k, grid, block, h->lean_smem, h->stream, p);
+    else k<<<grid, block, h->lean_smem, h->stream>>>(p);
+}
+
 template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
@@ -674,7 +691,15 @@ int launch_steps(ss_engine *h, int64_t count) {
             p.SA = reinterpret_cast<T4 *>(h->SA);
             // tiles: stages chained by programmatic dependent launch (the
             // kernel waits in stage_tile before its first state read)
+            int stage = 0;
             auto rk4_launch = [&](void (*k)(Params<T>)) {
+                ++stage;
+                if constexpr (F32 && LAYOUT >= 3) {
+                    if (h->lean_smem) {                      // fp32 compact tiles: the lean kernel
+                        launch_rk4_lean<LAYOUT == 3>(h, p, grid, stage);
+                        return;
+                    }
+                }
                 if (LAYOUT >= 3 && h->pdl) launch_pdl(k, grid, kBlock, smem, h->stream, p);
                 else k<<<grid, kBlock, smem, h->stream>>>(p);
             };
@@ -1005,7 +1030,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             // explicit format and RK4 use the kernels.cuh kernels.
             const char *kenv = getenv("SS_KERNEL");
             const std::string kname = kenv ? kenv : "lean";
-            if (kname != "step1" && h->integrator != SS_RK4 && !L.has_self && L.compact &&
+            if (kname != "step1" && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
                 // scenes with few tiles (at most 3 per SM) use two lanes per mass:
@@ -1027,7 +1052,14 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_lean_kernel<1, false, 6, 2>, tile_lean_kernel<0, true, 6, 2>,
                                  tile_lean_kernel<1, true, 6, 2>, tile_lean_kernel<0, false, 6, 1, true>,
                                  tile_lean_kernel<1, false, 6, 1, true>, tile_lean_kernel<0, true, 6, 1, true>,
-                                 tile_lean_kernel<1, true, 6, 1, true>})
+                                 tile_lean_kernel<1, true, 6, 1, true>, tile_lean_kernel<2, false>,
+                                 tile_lean_kernel<3, false>, tile_lean_kernel<4, false>, tile_lean_kernel<5, false>,
+                                 tile_lean_kernel<2, true>, tile_lean_kernel<3, true>, tile_lean_kernel<4, true>,
+                                 tile_lean_kernel<5, true>, tile_lean_kernel<2, false, 6, 2>,
+                                 tile_lean_kernel<3, false, 6, 2>, tile_lean_kernel<4, false, 6, 2>,
+                                 tile_lean_kernel<5, false, 6, 2>, tile_lean_kernel<2, true, 6, 2>,
+                                 tile_lean_kernel<3, true, 6, 2>, tile_lean_kernel<4, true, 6, 2>,
+                                 tile_lean_kernel<5, true, 6, 2>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }

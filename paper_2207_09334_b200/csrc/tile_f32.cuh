@@ -49,10 +49,78 @@ __device__ __forceinline__ float spring_c(float dx, float dy, float dz, float k,
 
 // External forces + Euler/Verlet update + restore fixed + store + finiteness
 // check of device mass m (engine.py:273-328, 297-301, 375-381).
+// RK4 stage STAGE (1-4) of device mass m at the trial state (x4, vs4):
+// kernels.cuh rk4_kernel's stage update (engine.py:330-354), on the lean
+// kernel's spring sum.  X0/V0 step start, SV/SA running sums.
+template <int STAGE>
+__device__ __forceinline__ void rk4_store(const Params<float> &p, int m, V3<float> sum, const float4 &x4,
+                                          const float4 &p4, const float4 &vs4) {
+    const float4 x04 = p.X0[m];
+    const float mass = fabsf(x04.w);
+    const bool fixed = signbit(x04.w);
+    const V3<float> xa = {p4.x + x4.x, p4.y + x4.y, p4.z + x4.z};
+    const V3<float> f = add_external<true>(p, m, sum, xa, vs4, mass);
+    const float a[3] = {f.x / mass, f.y / mass, f.z / mass};
+    const float4 v04 = p.V0[m];
+    const float x0[3] = {x04.x, x04.y, x04.z};
+    const float v0[3] = {v04.x, v04.y, v04.z};
+    const float vs[3] = {vs4.x, vs4.y, vs4.z};
+    float xn[3], vn[3], sv[3], sa[3];
+    if constexpr (STAGE == 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            xn[c] = x0[c] + p.half_dt * v0[c];
+            vn[c] = v0[c] + p.half_dt * a[c];
+            sa[c] = a[c];
+        }
+    } else if constexpr (STAGE == 2 || STAGE == 3) {
+        const float4 sv4 = p.SV[m], sa4 = p.SA[m];
+        const float h = (STAGE == 2) ? p.half_dt : p.dt;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            xn[c] = x0[c] + h * vs[c];
+            vn[c] = v0[c] + h * a[c];
+            const float svp = (STAGE == 2) ? v0[c] : (&sv4.x)[c];
+            sv[c] = svp + 2.0f * vs[c];
+            sa[c] = (&sa4.x)[c] + 2.0f * a[c];
+        }
+    } else {
+        const float4 sv4 = p.SV[m], sa4 = p.SA[m];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float svf = (&sv4.x)[c] + vs[c];
+            const float saf = (&sa4.x)[c] + a[c];
+            xn[c] = x0[c] + p.dt6 * svf;
+            vn[c] = v0[c] + p.dt6 * saf;
+            if (p.damped) vn[c] = vn[c] * p.one_minus_d;
+        }
+    }
+    if (fixed) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { xn[c] = x0[c]; vn[c] = v0[c]; }
+    }
+    p.Xout[m] = make_float4(xn[0], xn[1], xn[2], x04.w);
+    p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
+    if constexpr (STAGE == 1) {
+        p.SA[m] = make_float4(sa[0], sa[1], sa[2], 0.f);
+    } else if constexpr (STAGE < 4) {
+        p.SV[m] = make_float4(sv[0], sv[1], sv[2], 0.f);
+        p.SA[m] = make_float4(sa[0], sa[1], sa[2], 0.f);
+    } else {
+        if (!(finite3<true>(xn[0], xn[1], xn[2]) && finite3<true>(vn[0], vn[1], vn[2])))
+            flag_divergence<true>(p, m);
+    }
+}
+
+// INTEG: 0 Euler, 1 Verlet, 2-5 RK4 stages 1-4 (rk4_store).
 template <int INTEG>
 __device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V3<float> sum, float4 x4,
                                                 float4 p4, float4 v4, float4 xp4, bool need_prev,
                                                 int tile = blockIdx.x) {
+    if constexpr (INTEG >= 2) {
+        rk4_store<INTEG - 1>(p, m, sum, x4, p4, v4);
+        return;
+    }
     const float mass = fabsf(x4.w);
     const bool fixed = signbit(x4.w);
     const V3<float> xa = {p4.x + x4.x, p4.y + x4.y, p4.z + x4.z};
