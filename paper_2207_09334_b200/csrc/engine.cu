@@ -154,9 +154,10 @@ struct ss_engine {
     bool p2p_on = false;
     // CTA-resident small-scene kernel (resident.cuh): record image and launch shape
     void *res_image = nullptr;
-    unsigned res_image_bytes = 0, res_off[4] = {0, 0, 0, 0};
+    unsigned *res_segd = nullptr;                 // per-CTA segment offsets in the image (device)
+    unsigned res_dict_bytes = 0, res_off[3] = {0, 0, 0};   // smem offsets: dict, groups, segment
     size_t res_smem = 0;
-    int res_nnz = 0, res_n_dict = 0, res_g = 0, res_threads = 0;
+    int res_ctas = 0, res_pslots = 0, res_g = 0, res_threads = 0;
 
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
@@ -569,20 +570,19 @@ int launch_steps(ss_engine *h, int64_t count) {
     if (h->res_image && h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2) {
         // small scene: one CTA keeps the state on chip for the whole batch (resident.cuh)
         ResidentArgs a{};
-        a.image = reinterpret_cast<const uint4 *>(h->res_image);
-        a.image_bytes = h->res_image_bytes;
-        a.nnz = h->res_nnz;
-        a.n_dict = h->res_n_dict;
+        a.image = reinterpret_cast<const unsigned char *>(h->res_image);
+        a.seg = h->res_segd;
+        a.dict_bytes = h->res_dict_bytes;
         a.nd = (int)h->ND;
+        a.pslots = h->res_pslots;
         a.cur0 = h->cur;
         a.count = count;
         a.step0 = h->n;
         a.bootstrap0 = (h->integrator == SS_VERLET && !h->has_prev) ? 1 : 0;
         a.G = (int)G;
-        a.off_row = h->res_off[0];
-        a.off_inc = h->res_off[1];
-        a.off_dict = h->res_off[2];
-        a.off_grp = h->res_off[3];
+        a.off_dict = h->res_off[0];
+        a.off_grp = h->res_off[1];
+        a.off_seg = h->res_off[2];
         p.X = reinterpret_cast<const T4 *>(h->X[0]);
         p.Xout = reinterpret_cast<T4 *>(h->X[1]);
         p.V = reinterpret_cast<T4 *>(h->V);
@@ -596,8 +596,19 @@ int launch_steps(ss_engine *h, int64_t count) {
         const bool euler = h->integrator == SS_EULER;
         auto *k = h->res_g == 8 ? (euler ? resident_kernel<F32, 0, 8> : resident_kernel<F32, 1, 8>)
                                 : (euler ? resident_kernel<F32, 0, 4> : resident_kernel<F32, 1, 4>);
-        k<<<1, h->res_threads, h->res_smem, h->stream>>>(p, a);
-        CK(cudaGetLastError());
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)h->res_ctas);
+        cfg.blockDim = dim3((unsigned)h->res_threads);
+        cfg.dynamicSmemBytes = h->res_smem;
+        cfg.stream = h->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)h->res_ctas;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k, p, a));
         h->launches += 1;
         h->cur ^= (int)(count & 1);
         if (h->integrator == SS_VERLET) h->has_prev = true;
@@ -799,19 +810,24 @@ int up_vec(ss_engine *h, void **dst, const std::vector<T> &src) {
     return upload(h, *dst, src.data(), src.size() * sizeof(T));
 }
 
-// Record image of the CTA-resident kernel (resident.cuh) for scenes of at
-// most kResidentMaxSlots device slots whose image fits shared memory; every
+// Record image of the cluster-resident kernel (resident.cuh) for scenes of at
+// most kResidentMaxCtas tiles whose per-CTA image fits shared memory; every
 // mass's incidences in ascending spring id (the reference's summation order),
-// springs deduplicated into a dictionary.  SS_RESIDENT=0 disables it.
+// springs deduplicated into a dictionary, partners renumbered into the CTA's
+// own slots and its halo.  SS_RESIDENT=0 disables it.
 template <bool F32>
 int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     using T4 = typename Prec<F32>::T4;
-    if (h->integrator == SS_RK4 || h->ND > kResidentMaxSlots || (F32 && !h->rx0) ||
+    const int64_t ND = h->ND, S = h->S;
+    const int64_t n_ctas = (ND + kResidentSlots - 1) / kResidentSlots;
+    if (h->integrator == SS_RK4 || n_ctas > kResidentMaxCtas || (F32 && !h->rx0) ||
         h->groups.size() > (size_t)kResidentMaxGroups)
         return SS_OK;
-    if (const char *e = getenv("SS_RESIDENT"))
-        if (atoi(e) == 0) return SS_OK;
-    const int64_t ND = h->ND, S = h->S;
+    // fp32: clusters of up to kResidentMaxCtas CTAs (measured faster than a
+    // launch per step); fp64: one CTA only (its multi-CTA cluster was slower)
+    int max_ctas = F32 ? kResidentMaxCtas : 1;
+    if (const char *e = getenv("SS_RESIDENT")) max_ctas = std::min(max_ctas, atoi(e));  // 0: off
+    if (n_ctas > max_ctas) return SS_OK;
     std::vector<int64_t> dev(h->N);
     for (int64_t i = 0; i < h->N; ++i)
         dev[i] = h->tl.new_of.empty() || h->orig_of.empty() ? i : (int64_t)h->tl.new_of[i];
@@ -823,6 +839,7 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     for (int64_t i = 0; i < ND; ++i) row[i + 1] += row[i];
     const int64_t nnz = row[ND];
     std::vector<uint32_t> inc((size_t)nnz), fill(row.begin(), row.end() - 1);
+    std::vector<int32_t> partner((size_t)nnz);
     const bool has_g = d->group && !h->groups.empty();
     // dictionary: fp64 (k, l0, group) bit patterns; fp32 (k, k*l0, D, group) as tiles_f32.cpp
     std::map<std::array<uint64_t, 4>, uint32_t> dict;
@@ -864,25 +881,56 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
                 di = it->second;
             }
             const uint32_t owner = me < other ? 0x1000u : 0u;      // degenerate springs counted at the lower id
-            inc[fill[dev[me]]++] = (uint32_t)dev[other] | owner | (di << 13);
+            const int64_t q = fill[dev[me]]++;
+            inc[q] = owner | (di << 13);
+            partner[q] = (int32_t)dev[other];
         }
+    }
+    // per CTA: halo list (partners owned by other CTAs) and local partner slots
+    std::vector<std::vector<uint32_t>> halo((size_t)n_ctas);
+    size_t max_halo = 0;
+    for (int64_t r = 0; r < n_ctas; ++r) {
+        const int64_t lo = r * kResidentSlots, hi = std::min<int64_t>(ND, lo + kResidentSlots);
+        std::vector<uint32_t> &hl = halo[r];
+        for (uint32_t q = row[lo]; q < row[hi]; ++q)
+            if (partner[q] < lo || partner[q] >= hi) hl.push_back((uint32_t)partner[q]);
+        std::sort(hl.begin(), hl.end());
+        hl.erase(std::unique(hl.begin(), hl.end()), hl.end());
+        for (uint32_t q = row[lo]; q < row[hi]; ++q) {
+            const int64_t o = partner[q];
+            const uint32_t local = (o >= lo && o < hi)
+                                       ? (uint32_t)(o - lo)
+                                       : (uint32_t)(kResidentSlots +
+                                                    (std::lower_bound(hl.begin(), hl.end(), (uint32_t)o) - hl.begin()));
+            inc[q] |= local;
+        }
+        max_halo = std::max(max_halo, hl.size());
     }
     const int64_t nd = (int64_t)keys.size();
     auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
-    const size_t off_row = 2 * (size_t)ND * sizeof(T4);
-    const size_t off_inc = off_row + al16(((size_t)ND + 1) * 4);
-    const size_t off_dict = off_inc + al16((size_t)nnz * 4);
-    const size_t off_grp = off_dict + al16((size_t)nd * (F32 ? 32 : 16));
-    const size_t end = off_grp + (F32 ? 0 : al16((size_t)nd * 4));
+    const size_t pslots = (size_t)((kResidentSlots + max_halo + 31) / 32 * 32);
+    if (pslots > 4096) return SS_OK;                               // 12-bit partner slots
+    const size_t dict_bytes = al16((size_t)nd * (F32 ? 32 : 16));
+    const size_t grp_bytes = F32 ? 0 : al16((size_t)nd * 4);
+    std::vector<size_t> seg((size_t)n_ctas + 1);
+    seg[0] = dict_bytes + grp_bytes;
+    size_t max_seg = 0;
+    for (int64_t r = 0; r < n_ctas; ++r) {
+        const int64_t lo = r * kResidentSlots, hi = std::min<int64_t>(ND, lo + kResidentSlots);
+        const size_t bytes = 16 + 260 * 4 + ((halo[r].size() + 3) & ~(size_t)3) * 4 + al16((size_t)(row[hi] - row[lo]) * 4);
+        seg[r + 1] = seg[r] + al16(bytes);
+        max_seg = std::max(max_seg, al16(bytes));
+    }
+    const size_t off_dict = 2 * pslots * sizeof(T4);
+    const size_t off_seg = off_dict + dict_bytes + grp_bytes;
+    const size_t smem = off_seg + max_seg;
     int dev_max = 0;
     CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-    if (end + 64 > (size_t)dev_max) return SS_OK;                   // does not fit one SM
-    std::vector<unsigned char> img(end - off_row, 0);
-    std::memcpy(img.data(), row.data(), row.size() * 4);
-    std::memcpy(img.data() + (off_inc - off_row), inc.data(), inc.size() * 4);
+    if (smem + 1024 > (size_t)dev_max) return SS_OK;                // does not fit one SM
+    std::vector<unsigned char> img(seg[n_ctas], 0);
     for (int64_t q = 0; q < nd; ++q) {
         const auto &k = keys[q];
-        unsigned char *e = img.data() + (off_dict - off_row) + (size_t)q * (F32 ? 32 : 16);
+        unsigned char *e = img.data() + (size_t)q * (F32 ? 32 : 16);
         const int32_t g = (int32_t)((int64_t)k[3] - 1);
         if constexpr (F32) {
             const uint32_t b[6] = {(uint32_t)(k[0] >> 32), (uint32_t)k[0], (uint32_t)(k[1] >> 32), (uint32_t)k[1],
@@ -891,28 +939,65 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
         } else {
             std::memcpy(e, &k[0], 8);
             std::memcpy(e + 8, &k[1], 8);
-            std::memcpy(img.data() + (off_grp - off_row) + (size_t)q * 4, &g, 4);
+            std::memcpy(img.data() + dict_bytes + (size_t)q * 4, &g, 4);
         }
+    }
+    for (int64_t r = 0; r < n_ctas; ++r) {                         // header, rows, halo, incidences
+        const int64_t lo = r * kResidentSlots, hi = std::min<int64_t>(ND, lo + kResidentSlots);
+        uint32_t *w = reinterpret_cast<uint32_t *>(img.data() + seg[r]);
+        w[0] = (uint32_t)halo[r].size();
+        uint32_t *rw = w + 4;
+        for (int64_t i = 0; i <= kResidentSlots; ++i) rw[i] = row[std::min(lo + i, hi)] - row[lo];
+        uint32_t *hl = rw + 260;
+        std::copy(halo[r].begin(), halo[r].end(), hl);
+        uint32_t *iw = hl + ((halo[r].size() + 3) & ~(size_t)3);
+        std::memcpy(iw, inc.data() + row[lo], (size_t)(row[hi] - row[lo]) * 4);
     }
     int rc = h->alloc(&h->res_image, img.size());
     if (rc || (rc = upload(h, h->res_image, img.data(), img.size()))) return rc;
-    h->res_image_bytes = (unsigned)img.size();
-    h->res_off[0] = (unsigned)off_row;
-    h->res_off[1] = (unsigned)off_inc;
-    h->res_off[2] = (unsigned)off_dict;
-    h->res_off[3] = (unsigned)off_grp;
-    h->res_smem = end;
-    h->res_nnz = (int)nnz;
-    h->res_n_dict = (int)nd;
-    // lanes per mass slot; only slots up to the last real mass get threads
-    int64_t used = 0;
-    for (int64_t i = 0; i < ND; ++i)
-        if (h->src_of(i) >= 0) used = i + 1;
+    {
+        std::vector<unsigned> sg(seg.begin(), seg.end());
+        if ((rc = up_vec(h, reinterpret_cast<void **>(&h->res_segd), sg))) return rc;
+    }
+    h->res_dict_bytes = (unsigned)(dict_bytes + grp_bytes);
+    h->res_off[0] = (unsigned)off_dict;
+    h->res_off[1] = (unsigned)(off_dict + dict_bytes);
+    h->res_off[2] = (unsigned)off_seg;
+    h->res_pslots = (int)pslots;
+    h->res_smem = smem;
+    h->res_ctas = (int)n_ctas;
+    // lanes per mass slot; a lone CTA gets threads only up to its last real mass
+    int64_t used = kResidentSlots;
+    if (n_ctas == 1) {
+        used = 0;
+        for (int64_t i = 0; i < ND; ++i)
+            if (h->src_of(i) >= 0) used = i + 1;
+    }
     h->res_g = used * 8 <= 1024 ? 8 : 4;
     h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
     for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
                            (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>})
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)end));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (n_ctas > 1) {                                               // can the cluster be scheduled at all?
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)n_ctas);
+        cfg.blockDim = dim3((unsigned)h->res_threads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)n_ctas;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        const void *fn = h->integrator == SS_EULER ? (const void *)resident_kernel<F32, 0, 4>
+                                                   : (const void *)resident_kernel<F32, 1, 4>;
+        if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess || clusters < 1) {
+            cudaGetLastError();
+            h->res_image = nullptr;                                  // (freed with the engine)
+        }
+    }
     return SS_OK;
 }
 

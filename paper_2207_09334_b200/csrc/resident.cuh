@@ -18,12 +18,15 @@
 // d = D + (r_o - r_m) of tile_f32.cuh.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 #include "tile_f32.cuh"
 
 namespace ss {
 
-constexpr int kResidentMaxSlots = 256;      // one tile: beyond it the multi-CTA kernels win
+constexpr int kResidentSlots = 256;         // slots per CTA (one tile)
+constexpr int kResidentMaxCtas = 8;         // portable cluster size
 constexpr int kResidentMaxGroups = 64;      // actuation groups staged in shared memory
 
 // add_external (kernels.cuh) with f_ext from registers: same op order.
@@ -64,25 +67,28 @@ add_external_fe(const Params<typename Prec<F32>::T> &p, V3<typename Prec<F32>::T
     return a;
 }
 
-// incidence word: partner slot (bits 0-11) | counts a degenerate spring (bit
-// 12: this endpoint is the spring's lower caller id) | dictionary index << 13
-// Shared memory: positions [2][nd] T4, then an image of the records built by
-// the host (engine.cu build_resident), copied in verbatim:
-//   row   u32 [nd + 1]   offsets into inc (device slot order)
-//   inc   u32 [nnz]      incidence words, per mass in ascending spring id
-//   dict  fp64: double2 (k, l0) [n_dict]; fp32: float4 (k, k*l0, Dx, Dy),
-//         float4 (Dz, group bits, 0, 0) [n_dict]
-//   grp   fp64: int32 group per dictionary entry (-1 passive) [n_dict]
-// each section 16-byte aligned.
+// CTA r of the cluster owns device slots [256 r, 256 r + 256).  Incidence
+// word: partner (bits 0-11: a local position slot -- 0..255 own, 256 + k the
+// k-th entry of this CTA's halo) | counts a degenerate spring (bit 12: this
+// endpoint is the spring's lower caller id) | dictionary index << 13.
+// Record image (engine.cu setup_resident), copied to shared memory:
+//   shared part at 0: dict (fp64 double2 (k, l0); fp32 float4 (k, k*l0, Dx,
+//     Dy), float4 (Dz, group bits, 0, 0)) [n_dict], then fp64 int32 groups
+//   per CTA, at seg[r]: u32 n_halo, 3 x u32 pad, row u32 [257] (padded to
+//     16 B), halo u32 [n_halo] (global device slots, padded), inc u32 [...]
+// Shared memory of a CTA: positions T4 [2][pslots] (own 256, then halo) |
+// dict | its segment.
 struct ResidentArgs {
-    const uint4 *image;           // the record image (global memory)
-    unsigned image_bytes;         // multiple of 16
-    int nnz, n_dict, nd;
+    const unsigned char *image;   // the record image
+    const unsigned *seg;          // n_ctas + 1 segment byte offsets (multiples of 16)
+    unsigned dict_bytes;          // shared part (dict + groups), multiple of 16
+    int nd;                       // device slots
+    int pslots;                   // position slots per CTA and parity (256 + max halo)
     int cur0;                     // X buffer holding the positions at the start
     long long count, step0;
     int bootstrap0;               // Verlet without x_prev at the first step
     int G;                        // actuation groups (scale row stride)
-    unsigned off_row, off_inc, off_dict, off_grp;   // shared-memory byte offsets (positions first)
+    unsigned off_dict, off_grp, off_seg;   // shared-memory byte offsets
 };
 
 // Spring sum of mass m by a group of G lanes (lane j = 0..G-1 of the group):
@@ -93,12 +99,11 @@ struct ResidentArgs {
 // The sum is returned to every lane of the group.
 template <bool F32, int G>
 __device__ __forceinline__ V3<typename Prec<F32>::T>
-resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const typename Prec<F32>::T4 *xs, int m,
+resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint32_t *row, const uint32_t *inc,
+                    const typename Prec<F32>::T4 *xs, int m,   // m: local slot
                     const typename Prec<F32>::T4 &x4, const typename Prec<F32>::T *scale, int lane, unsigned gmask,
                     int leader, unsigned &deg) {
     using T = typename Prec<F32>::T;
-    const uint32_t *row = reinterpret_cast<const uint32_t *>(smem + a.off_row);
-    const uint32_t *inc = reinterpret_cast<const uint32_t *>(smem + a.off_inc);
     V3<T> s = {(T)0, (T)0, (T)0};
     const int q0 = (int)row[m], n = (int)row[m + 1] - q0;
     if constexpr (F32) {
@@ -179,27 +184,35 @@ template <bool F32, int INTEG, int G>
 __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<F32>::T> p, ResidentArgs a) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int diverged;
     __shared__ T sscale[2][kResidentMaxGroups];            // this and the next step's actuation scales
-    T4 *const xsb = reinterpret_cast<T4 *>(smem);          // positions: [c * nd + slot], c = step parity
+    T4 *const xsb = reinterpret_cast<T4 *>(smem);          // positions: [c * pslots + slot], c = step parity
+    const unsigned rank = cl.block_rank(), n_ctas = cl.num_blocks();
     const int tid = threadIdx.x, bs = blockDim.x;
-    const int m = tid / G, lane = tid % G;
+    const int l = tid / G, lane = tid % G;
+    const int m = (int)rank * kResidentSlots + l;           // device slot
     const int leader = (tid & 31) & ~(G - 1);               // group's first lane within the warp
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << leader;
-    // stage the record image (16-byte copies) and the start positions
+    // stage the shared dictionary and this CTA's segment (16-byte copies)
     {
-        uint4 *dst = reinterpret_cast<uint4 *>(smem + a.off_row);
-        const unsigned n16 = a.image_bytes / 16u;
-        for (unsigned i = tid; i < n16; i += bs) dst[i] = __ldg(a.image + i);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + a.off_dict);
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.image);
+        for (unsigned i = tid; i < a.dict_bytes / 16u; i += bs) dst[i] = __ldg(src + i);
+        const unsigned s0 = __ldg(a.seg + rank), s1 = __ldg(a.seg + rank + 1);
+        dst = reinterpret_cast<uint4 *>(smem + a.off_seg);
+        src = reinterpret_cast<const uint4 *>(a.image + s0);
+        for (unsigned i = tid; i < (s1 - s0) / 16u; i += bs) dst[i] = __ldg(src + i);
     }
     const T4 *X0 = a.cur0 ? p.Xout : p.X;                   // (host passes X[0] as X, X[1] as Xout)
-    const bool in = m < a.nd;
+    const bool in = l < kResidentSlots && m < a.nd;
     const bool act = in && (!p.orig_of || p.orig_of[m] >= 0);
     T4 x{}, v{}, hst{}, pb{};
     if (in) {
         x = X0[m];
-        if (lane == 0) xsb[m] = x;
+        if (lane == 0) xsb[l] = x;
     }
     if (act) {
         v = p.V[m];
@@ -215,11 +228,25 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
         fe[1] = f4.y;
         fe[2] = f4.z;
     }
-    __syncthreads();
+    if (n_ctas > 1) cl.sync();                              // every CTA's start positions and records staged
+    else __syncthreads();
+    const uint32_t *seg = reinterpret_cast<const uint32_t *>(smem + a.off_seg);
+    const uint32_t n_halo = seg[0];
+    const uint32_t *halo = seg + 4 + 260;                   // global device slots of this CTA's halo
+    const uint32_t *srow = seg + 4;                         // rows, then incidences after the halo list
+    const uint32_t *sinc = halo + ((n_halo + 3u) & ~3u);
     unsigned deg = 0;
     int c = 0;
     long long done = 0;
     for (long long s = 0; s < a.count; ++s) {
+        if (n_ctas > 1) {                                   // halo positions from their owners (DSMEM)
+            T4 *cur = xsb + (c ? a.pslots : 0);
+            for (uint32_t k = tid; k < n_halo; k += bs) {
+                const uint32_t g = halo[k];
+                cur[kResidentSlots + k] = *cl.map_shared_rank(cur + (g % kResidentSlots), g / kResidentSlots);
+            }
+            __syncthreads();
+        }
         const T *scale = a.G ? sscale[s & 1] : nullptr;
         // the next step's scales, fetched now and published by this step's barrier
         T next_scale = (T)0;
@@ -229,8 +256,8 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
             const T4 x4 = x;
             const T mass = F32 ? (T)fabsf((float)x4.w) : (T)fabs((double)x4.w);
             const bool fixed = signbit(x4.w);
-            const V3<T> sp = resident_spring_sum<F32, G>(a, smem, xsb + (c ? a.nd : 0), m, x4, scale, lane, gmask,
-                                                         leader, deg);
+            const V3<T> sp = resident_spring_sum<F32, G>(a, smem, srow, sinc, xsb + (c ? a.pslots : 0), l, x4, scale,
+                                                         lane, gmask, leader, deg);
             V3<T> xa = {x4.x, x4.y, x4.z};                  // absolute position (contact)
             if constexpr (F32) { xa.x = pb.x + xa.x; xa.y = pb.y + xa.y; xa.z = pb.z + xa.z; }
             const V3<T> f = add_external_fe<F32>(p, sp, xa, v, mass, fe);   // engine.py:273-288
@@ -294,19 +321,20 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
             v.y = vn[1];
             v.z = vn[2];
             if (lane == 0) {
-                xsb[(c ? 0 : a.nd) + m] = x;
+                xsb[(c ? 0 : a.pslots) + l] = x;
                 if (!(finite3<F32>(xn[0], xn[1], xn[2]) && finite3<F32>(vn[0], vn[1], vn[2]))) {
-                    diverged = 1;
+                    for (unsigned r = 0; r < n_ctas; ++r) *cl.map_shared_rank(&diverged, r) = 1;   // rare
                     atomicMin(p.div_mass, p.orig_of ? p.orig_of[m] : m);
                 }
             }
         }
         if (tid < a.G) sscale[(s + 1) & 1][tid] = next_scale;
-        __syncthreads();                                    // also orders next step's writes after this step's reads
+        if (n_ctas > 1) cl.sync();                          // this step's writes before the next step's reads
+        else __syncthreads();
         c ^= 1;
         done = s + 1;
         if (diverged) {                                     // committed; the reference raises here
-            if (tid == 0) atomicMin(p.div_step, a.step0 + s + 1);
+            if (tid == 0 && rank == 0) atomicMin(p.div_step, a.step0 + s + 1);
             break;
         }
     }

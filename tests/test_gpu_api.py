@@ -405,3 +405,33 @@ def test_engines_release_their_device_memory():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 8 << 20, (free0, free1)
+
+
+def test_cluster_resident_fp32_matches_per_step_launches(monkeypatch):
+    """fp32 scenes of 2-8 tiles run one thread-block cluster for a whole batch
+    (positions in shared memory, halos through distributed shared memory):
+    same physics as one launch per step to fp32 rounding, same divergence
+    step and mass."""
+    from paper_2207_09334_b200 import crawler_scene, lattice as L, replicate
+    for scene in (L.beam_lattice(length=4.0), replicate(crawler_scene(), 64, jitter=1e-6, seed=4)):
+        out = {}
+        for res in ("8", "0"):
+            monkeypatch.setenv("SS_RESIDENT", res)
+            eng = Engine(scene, integrator="verlet", precision="f32")
+            eng.step(3)
+            eng.step(2000)
+            out[res] = eng.x.copy()
+            eng.close()
+        assert np.abs(out["8"] - out["0"]).max() <= 1e-4 * np.abs(out["0"]).max()   # the fp32 tolerance
+    # divergence inside a cluster batch: the reference's step and lowest mass
+    blown = L.excite(L.block_scene(9), seed=11)
+    blown.dt = 0.05
+    got = {}
+    for res in ("8", "0"):
+        monkeypatch.setenv("SS_RESIDENT", res)
+        eng = Engine(blown, integrator="euler", precision="f32")
+        with pytest.raises(DivergenceError) as err:
+            eng.step(10000)
+        got[res] = (err.value.mass_id, err.value.step, eng.n)
+        eng.close()
+    assert got["8"][1:] == got["0"][1:]

@@ -10,15 +10,15 @@ scenes = {"crawler": crawler_scene, "crawler_x12": lambda: replicate(crawler_sce
 for name, mk in scenes.items():
     for prec in ("f64", "f32"):
         row = {"scene": name, "prec": prec}
-        for res in ("1", "0"):
+        for res in (os.environ.get("RES_ON", "1"), "0"):
             os.environ["SS_RESIDENT"] = res
             e = Engine(mk(), integrator="verlet", precision=prec)
             row["slots"] = e.info()["n_masses"]
             e.step(100)
             n = 20000
             t0 = time.perf_counter(); e.step(n); dt = time.perf_counter() - t0
-            row["us_per_step_resident" + res] = round(1e6 * dt / n, 3)
-            row["x_" + res] = e.x.copy()
+            row["us_per_step_resident" + ("0" if res == "0" else "1")] = round(1e6 * dt / n, 3)
+            row["x_" + ("0" if res == "0" else "1")] = e.x.copy()
             e.close()
         row["same"] = bool(row.pop("x_0").tobytes() == row.pop("x_1").tobytes())
         print(json.dumps(row), flush=True)
