@@ -1,15 +1,18 @@
-// CTA-resident kernel for small scenes ("small scenes").
+// Resident kernel for small scenes ("small scenes").
 //
-// A scene of at most kResidentMaxSlots device slots (the walker, the
-// cantilever, a few dozen robots) is stepped by ONE CTA for a whole batch:
-// positions live in shared memory (double-buffered by step parity), every
+// A scene of at most kResidentMaxCtas tiles (the walker, a few dozen
+// robots, the cantilever) is stepped by ONE CTA -- or, in fp32, one
+// thread-block cluster with one tile per CTA -- for a whole batch:
+// positions live in shared memory, double-buffered by step parity; every
 // mass's incidence list and a dictionary of distinct spring records are
-// staged into shared memory once per launch, and each thread keeps its
-// masses' velocity and history (x_prev / u) in registers.  A step is then a
-// pass over shared memory plus one __syncthreads -- no launch, no grid
-// barrier, no global-memory round trip -- which is what "many small-dt
-// substeps batched into a persistent kernel" (north_star) needs when the
-// whole scene is a few microseconds of work per launch.
+// staged once per launch; each lane group keeps its mass's velocity and
+// history (x_prev / u) in registers.  A step is: copy this CTA's halo
+// positions from their owner CTAs through distributed shared memory (one
+// read per halo mass), a pass over the CTA's own shared memory, and one
+// barrier (__syncthreads for a lone CTA, the cluster barrier otherwise) --
+// no launch, no grid barrier, no global-memory round trip: "many small-dt
+// substeps batched into a persistent kernel" (north_star) for scenes whose
+// step is a few microseconds of work.
 //
 // Arithmetic is that of the multi-CTA kernels: fp64 sums each mass's
 // springs in ascending spring id with the reference's op order
