@@ -926,7 +926,7 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     const size_t smem = off_seg + max_seg;
     int dev_max = 0;
     CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-    if (smem + 1024 > (size_t)dev_max) return SS_OK;                // does not fit one SM
+    if (smem + 2048 > (size_t)dev_max) return SS_OK;                // does not fit one SM (+ static smem)
     std::vector<unsigned char> img(seg[n_ctas], 0);
     for (int64_t q = 0; q < nd; ++q) {
         const auto &k = keys[q];
@@ -976,8 +976,14 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     h->res_g = used * 8 <= 1024 ? 8 : 4;
     h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
     for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
-                           (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>})
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                           (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>}) {
+        // per-function attributes are shared by every engine in the process:
+        // grant the device maximum, never this engine's size
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, fn));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max - (int)fa.sharedSizeBytes));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
     if (n_ctas > 1) {                                               // can the cluster be scheduled at all?
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)n_ctas);

@@ -29,7 +29,7 @@
 namespace ss {
 
 constexpr int kResidentSlots = 256;         // slots per CTA (one tile)
-constexpr int kResidentMaxCtas = 8;         // portable cluster size
+constexpr int kResidentMaxCtas = 16;        // cluster size (above 8: non-portable, B200 allows 16)
 constexpr int kResidentMaxGroups = 64;      // actuation groups staged in shared memory
 
 // add_external (kernels.cuh) with f_ext from registers: same op order.
