@@ -174,7 +174,8 @@ typedef struct ss_info {
     int64_t tile_blob_bytes;   /* TILE: bytes of records streamed per step */
     double  tile_halo_ratio;   /* TILE: mean (tile + halo masses) / tile masses */
     double  tile_foreign_frac; /* TILE: fraction of references whose owner is in another tile */
-    int32_t tile_kernel;       /* tile record format: fp32 1 explicit, 2 compact (0: step_kernel); fp64 0 explicit, 3 compact */
+    int32_t tile_kernel;       /* dominant kernel / record format: fp32 1 explicit, 2 compact (tile_lean_kernel; 0: step_kernel);
+                                  fp64 0 explicit, 3 compact (step_kernel), 4 compact (tile_f64_kernel) */
     int32_t kernel_smem;       /* its dynamic shared memory per CTA */
 } ss_info;
 int ss_get_info(ss_engine *h, ss_info *info);
@@ -268,6 +269,14 @@ int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256], co
                        int64_t n_slots);
 int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer);
 int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res);
+
+/* Diagnostics: the fp64 kernel's branch-free IEEE fast paths against the
+ * library operators on `n` operand pairs (device `device`).  out[4i..4i+3] =
+ * (fast sqrt(a), sqrt(a), fast b/a, b/a); ok[i] bit 0 / bit 1: the sqrt /
+ * division operands are inside the fast-path range (then the fast result
+ * must equal the library's bit for bit; tests/test_gpu_f64_kernel.py). */
+int ss_check_f64_fastpath(int32_t device, const double *a, const double *b, int64_t n,
+                          double *out, int32_t *ok);
 
 #ifdef __cplusplus
 }

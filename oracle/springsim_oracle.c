@@ -22,6 +22,8 @@
  *   Engine._step_euler/_verlet/_rk4  engine.py:303-354   -> step_*()
  *   Engine._restore_fixed       engine.py:297-301
  *   Engine.step/_check_finite   engine.py:366-381        -> oracle_step()
+ *   build_voxel_lattice (boxes) lattice.py:89-136        -> oracle_voxel_box()
+ *        (the workload builder of bench.py's reference arm, bench.py:83-89)
  * Built with -O2 -ffp-contract=off (no FMA contraction, like numba/numpy).
  */
 #include <math.h>
@@ -356,6 +358,91 @@ void oracle_set_params(oracle_engine *e, double damping, const double *g) {
 }
 
 void oracle_set_f_ext(oracle_engine *e, const double *f_ext) { e->f_ext = f_ext; }
+
+/* ------------------------------------------------------ workload builder
+ *
+ * build_voxel_lattice(box_mesh(lo, hi), LatticeSpec(dim=dim), Material(k0, l_ref))
+ * (lattice.py:89-136) for a box, restated so that the reference arm of
+ * bench.py can build its cube without the product library:
+ *   counts = floor((hi - lo)/dim + 1e-9) + 1                 lattice.py:104-107
+ *   every grid node is kept (a box contains all its grid nodes, mesh.py:75-132
+ *   counts on-surface points as inside); ids in (i,j,k) lexicographic order,
+ *   x = lo + idx*dim                                         lattice.py:109-119
+ *   the 28 corner pairs of every cell, each sorted, de-duplicated and listed in
+ *   (lower id, upper id) order                               lattice.py:121-134
+ *   -- here grouped by the lower endpoint a: the corners b > a of the cells that
+ *   contain a, sorted and de-duplicated (the same set and order as np.unique);
+ *   l0 = np.linalg.norm(x_b - x_a) (lattice.py:84), i.e. OpenBLAS ddot
+ *   = sqrt(fma(dz, dz, fma(dy, dy, dx*dx)));
+ *   k = (k0 * l_ref) / l0                                    model.py:87-92
+ * Call with x == NULL for the sizes only.  Returns the spring count. */
+static int cmp_i64(const void *a, const void *b) {
+    const int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+static int upper_partners(int64_t a, const int64_t c[3], int64_t *out) {
+    const int64_t nz = c[2], ny = c[1];
+    const int64_t i = a / (ny * nz), j = (a / nz) % ny, k = a % nz;
+    int64_t buf[64];
+    int n = 0;
+    for (int64_t ci = i - 1; ci <= i; ++ci)
+        for (int64_t cj = j - 1; cj <= j; ++cj)
+            for (int64_t ck = k - 1; ck <= k; ++ck) {
+                if (ci < 0 || cj < 0 || ck < 0 || ci > c[0] - 2 || cj > ny - 2 || ck > nz - 2) continue;
+                for (int q = 0; q < 8; ++q) {            /* corners of cell (ci, cj, ck) */
+                    const int64_t b = ((ci + (q >> 2)) * ny + (cj + ((q >> 1) & 1))) * nz + (ck + (q & 1));
+                    if (b > a) buf[n++] = b;
+                }
+            }
+    qsort(buf, (size_t)n, sizeof(int64_t), cmp_i64);
+    int u = 0;
+    for (int q = 0; q < n; ++q)
+        if (u == 0 || buf[q] != out[u - 1]) out[u++] = buf[q];
+    return u;
+}
+
+int64_t oracle_voxel_box(const double lo[3], const double hi[3], double dim, double k0, double l_ref,
+                         int64_t counts[3], int64_t *n_masses, double *x, int64_t *si, int64_t *sj,
+                         double *k, double *l0) {
+    int64_t c[3];
+    for (int d = 0; d < 3; ++d) c[d] = (int64_t)floor((hi[d] - lo[d]) / dim + 1e-9) + 1;
+    const int64_t n = c[0] * c[1] * c[2];
+    if (counts) { counts[0] = c[0]; counts[1] = c[1]; counts[2] = c[2]; }
+    if (n_masses) *n_masses = n;
+    int64_t *first = malloc(sizeof(int64_t) * (size_t)(n + 1));
+    first[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t a = 0; a < n; ++a) {
+        int64_t tmp[32];
+        first[a + 1] = upper_partners(a, c, tmp);
+    }
+    for (int64_t a = 0; a < n; ++a) first[a + 1] += first[a];
+    const int64_t s = first[n];
+    if (x) {
+#pragma omp parallel for schedule(static)
+        for (int64_t a = 0; a < n; ++a) {
+            const int64_t idx[3] = {a / (c[1] * c[2]), (a / c[2]) % c[1], a % c[2]};
+            for (int d = 0; d < 3; ++d) x[3 * a + d] = lo[d] + (double)idx[d] * dim;
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t a = 0; a < n; ++a) {
+            int64_t part[32];
+            const int u = upper_partners(a, c, part);
+            for (int q = 0; q < u; ++q) {
+                const int64_t w = first[a] + q, b = part[q];
+                const double dx = x[3 * b] - x[3 * a], dy = x[3 * b + 1] - x[3 * a + 1],
+                             dz = x[3 * b + 2] - x[3 * a + 2];
+                si[w] = a;
+                sj[w] = b;
+                l0[w] = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
+                k[w] = (k0 * l_ref) / l0[w];
+            }
+        }
+    }
+    free(first);
+    return s;
+}
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP

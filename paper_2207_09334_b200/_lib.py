@@ -103,6 +103,7 @@ SIGNATURES = {
     "ss_lattice_box": (C.c_int, [_dp, _dp, C.c_double, C.c_double, C.c_double,
                                  C.c_int64, C.c_int64, _i64p, _i64p, _i64p,
                                  _dp, _i64p, _i64p, _dp, _dp, _i64p]),
+    "ss_check_f64_fastpath": (C.c_int, [C.c_int32, _dp, _dp, C.c_int64, _dp, _i32p]),
 }
 
 _lib = None

@@ -24,6 +24,7 @@
 #include "common.h"
 #include "kernels.cuh"
 #include "tile_f32.cuh"
+#include "tile_f64.cuh"
 #include "sampling.cuh"
 #include "layout.h"
 #include "springsim_b200.h"
@@ -121,6 +122,8 @@ struct ss_engine {
     uint32_t blob_smem = 0, max_halo = 0;
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
+    size_t f64_smem = 0;           // fp64 Euler/Verlet compact-format tile kernel (tile_f64.cuh), 0 = off
+    int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3)
     int lean_lanes = 1;            // threads per mass of that kernel (2: scenes with few tiles)
     int persist_max_grid = 0;      // co-resident CTAs of the persistent kernel (0: never persistent)
     bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
@@ -551,6 +554,20 @@ void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     else k<<<grid, block, h->lean_smem, h->stream>>>(p);
 }
 
+// fp64 Euler/Verlet step on compact tiles: tile_f64_kernel (tile_f64.cuh).
+template <bool GROUPS>
+void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
+    const bool euler = h->integrator == SS_EULER;
+    void (*k)(Params<double>) = nullptr;
+    switch (h->f64_variant) {
+        case 1: k = euler ? tile_f64_kernel<0, GROUPS, 1, 4> : tile_f64_kernel<1, GROUPS, 1, 4>; break;
+        case 2: k = euler ? tile_f64_kernel<0, GROUPS, 2, 3> : tile_f64_kernel<1, GROUPS, 2, 3>; break;
+        default: k = euler ? tile_f64_kernel<0, GROUPS, 2, 4> : tile_f64_kernel<1, GROUPS, 2, 4>; break;
+    }
+    if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
+    else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
@@ -677,6 +694,13 @@ int launch_steps(ss_engine *h, int64_t count) {
                 if (h->lean_smem) {
                     constexpr bool GROUPS = LAYOUT == 3;
                     launch_tile_f32<GROUPS>(h, p, grid);
+                    goto launched;
+                }
+            }
+            if constexpr (!F32 && LAYOUT >= 3) {
+                if (h->f64_smem) {
+                    if (G) launch_tile_f64<true>(h, p, grid);
+                    else launch_tile_f64<false>(h, p, grid);
                     goto launched;
                 }
             }
@@ -1152,6 +1176,26 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_lean_kernel<3, true, 6, 2>, tile_lean_kernel<4, true, 6, 2>,
                                  tile_lean_kernel<5, true, 6, 2>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            }
+        }
+        if constexpr (!F32) {
+            // fp64 Euler/Verlet on compact tiles: tile_f64_kernel (split
+            // staging planes, 24 B per slot) unless SS_F64_KERNEL=step asks
+            // for kernels.cuh's step_kernel
+            const char *kenv = getenv("SS_F64_KERNEL");
+            const std::string kname = kenv ? kenv : "tile";
+            const size_t f64s = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * 24;
+            if (kname != "step" && d->integrator != SS_RK4 && L.compact && !L.has_self &&
+                (int64_t)f64s <= dev_max) {
+                h->f64_smem = f64s;
+                if (const char *e = getenv("SS_F64_VARIANT")) h->f64_variant = atoi(e);
+                for (auto *kk : {tile_f64_kernel<0, false, 2, 4>, tile_f64_kernel<1, false, 2, 4>,
+                                 tile_f64_kernel<0, true, 2, 4>, tile_f64_kernel<1, true, 2, 4>,
+                                 tile_f64_kernel<0, false, 1, 4>, tile_f64_kernel<1, false, 1, 4>,
+                                 tile_f64_kernel<0, true, 1, 4>, tile_f64_kernel<1, true, 1, 4>,
+                                 tile_f64_kernel<0, false, 2, 3>, tile_f64_kernel<1, false, 2, 3>,
+                                 tile_f64_kernel<0, true, 2, 3>, tile_f64_kernel<1, true, 2, 3>})
+                    CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max));
             }
         }
         h->lay.canonical = L.canonical;
@@ -1939,8 +1983,9 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
-        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1) : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
-        info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->smem_bytes);
+        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1)
+                          : h->f64_smem ? 4 : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
+        info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->f64_smem ? h->f64_smem : h->smem_bytes);
     } else {
         info->ell_width_own = h->lay.W;
         info->ell_width_ref = h->lay.Wr;
@@ -2324,3 +2369,32 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
     for (int k = 0; k < n; ++k) hs[k]->stream = saved[k];
     return first_err;
 }
+
+extern "C" int ss_check_f64_fastpath(int32_t device, const double *a, const double *b, int64_t n, double *out,
+                                     int32_t *ok) {
+    if (!a || !b || !out || !ok || n < 0 || n > (1ll << 28)) return ss::fail(SS_EINVAL, "ss_check_f64_fastpath: bad arguments");
+    if (n == 0) return SS_OK;
+    CK(cudaSetDevice(device));
+    double *da = nullptr, *db = nullptr, *dout = nullptr;
+    int *dok = nullptr;
+    const size_t nb = (size_t)n * sizeof(double);
+    cudaError_t e = cudaMalloc(&da, nb);
+    if (e == cudaSuccess) e = cudaMalloc(&db, nb);
+    if (e == cudaSuccess) e = cudaMalloc(&dout, 4 * nb);
+    if (e == cudaSuccess) e = cudaMalloc(&dok, (size_t)n * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(da, a, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(db, b, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        f64_fastpath_check<<<(unsigned)((n + 255) / 256), 256>>>(da, db, (int)n, dout, dok);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, 4 * nb, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(ok, dok, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dout);
+    cudaFree(dok);
+    if (e != cudaSuccess) return ss::fail(SS_ECUDA, "ss_check_f64_fastpath: %s", cudaGetErrorString(e));
+    return SS_OK;
+}
+

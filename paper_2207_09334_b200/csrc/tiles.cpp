@@ -141,7 +141,9 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
     for (int64_t s = 0; s < S; ++s)
         if (in.si[s] == in.sj[s]) return SS_EAGAIN_DICT;
     L = TileLayout{};
-    tile_order(in, L.orig_of);
+    std::vector<int32_t> zcell;
+    tile_order(in, L.orig_of, &zcell);
+    const bool bank_aware = !zcell.empty();
     const int64_t D = (int64_t)L.orig_of.size();
     L.new_of.assign(N, -1);
     for (int64_t i = 0; i < D; ++i)
@@ -188,7 +190,30 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
         }
         std::sort(halo.begin(), halo.end());
         halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
-        if (W > 255 || halo.size() > 768) {
+        // bank-aware halo slots (as tiles_f32.cpp): a halo mass sits at
+        // 8 * (its rank among the halo masses of its z class) + (z mod 8), so
+        // the partners of 8 consecutive z (one warp phase of a 16-byte
+        // gather) land in 8 distinct bank groups; holes hold id -1
+        std::vector<int32_t> halo_ids;
+        std::vector<uint32_t> halo_slot(halo.size());
+        uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, maxc = 0;
+        std::vector<uint32_t> cls(halo.size());
+        if (bank_aware) {
+            for (size_t i = 0; i < halo.size(); ++i) cls[i] = cnt[zcell[L.orig_of[halo[i]]] & 7]++;
+            for (int r = 0; r < 8; ++r) maxc = std::max(maxc, cnt[r]);
+        }
+        if (bank_aware && 8 * maxc <= 768) {          // (else: dense slots, the tile still fits)
+            halo_ids.assign((size_t)8 * maxc, -1);
+            for (size_t i = 0; i < halo.size(); ++i) {
+                const uint32_t sl = 8 * cls[i] + ((uint32_t)zcell[L.orig_of[halo[i]]] & 7u);
+                halo_ids[sl] = halo[i];
+                halo_slot[i] = (uint32_t)kTile + sl;
+            }
+        } else {
+            halo_ids = halo;
+            for (size_t i = 0; i < halo.size(); ++i) halo_slot[i] = (uint32_t)(kTile + i);
+        }
+        if (W > 255 || halo_ids.size() > 768) {
 #pragma omp atomic write
             err = 3;
             continue;
@@ -213,8 +238,7 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
                 }
                 const uint32_t slot = (o >= base && o < base + n)
                                           ? (uint32_t)(o - base)
-                                          : (uint32_t)(kTile + (std::lower_bound(halo.begin(), halo.end(), o) -
-                                                                halo.begin()));
+                                          : halo_slot[std::lower_bound(halo.begin(), halo.end(), o) - halo.begin()];
                 incs[(size_t)(q - ptr[m]) * kTile + l] = (uint16_t)(slot | (di << 10));
             }
         }
@@ -225,12 +249,12 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
         }
         const uint32_t nd = (uint32_t)keys.size();
         TileHdr h{};
-        h.n = n; h.W = W; h.Wr = W; h.n_halo = (uint32_t)halo.size();
+        h.n = n; h.W = W; h.Wr = W; h.n_halo = (uint32_t)halo_ids.size();
         h.canonical = 1u | 2u;                 // bit 1: compact format
         h.slice_log2 = 8;
         h.n_dict = nd;
         uint32_t off = align16(sizeof(TileHdr));
-        h.off_halo = off; off = align16(off + (uint32_t)halo.size() * 4);
+        h.off_halo = off; off = align16(off + (uint32_t)halo_ids.size() * 4);
         h.off_cnt = off;  off = align16(off + kTile * 2);
         h.off_oo = off;   off = align16(off + W * kTile * 2);
         h.off_okl = off;  off = align16(off + nd * 16);
@@ -241,7 +265,7 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
         std::vector<uint8_t> &blob = parts[t];
         blob.assign(off, 0);
         std::memcpy(blob.data(), &h, sizeof h);
-        std::memcpy(blob.data() + h.off_halo, halo.data(), halo.size() * 4);
+        std::memcpy(blob.data() + h.off_halo, halo_ids.data(), halo_ids.size() * 4);
         for (int l = 0; l < n; ++l)
             put<uint16_t>(blob, h.off_cnt + 2 * l, (uint16_t)((ptr[base + l + 1] - ptr[base + l]) << 8));
         std::memcpy(blob.data() + h.off_oo, incs.data(), incs.size() * 2);
@@ -251,7 +275,7 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
             std::memcpy(blob.data() + h.off_okl + 16 * d + 8, &lb, 8);
             if (has_g) put<int8_t>(blob, h.off_og + d, (int8_t)std::get<2>(keys[d]));
         }
-        tW[t] = W; tH[t] = (uint32_t)halo.size(); tN[t] = n;
+        tW[t] = W; tH[t] = (uint32_t)halo_ids.size(); tN[t] = n;
         tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);
         tRatio[t] = (double)(n + halo.size()) / n;
     }

@@ -272,6 +272,12 @@ class Engine:
         except Exception:
             pass
 
+    def __enter__(self) -> "Engine":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
     @property
     def handle(self):
         return self._h

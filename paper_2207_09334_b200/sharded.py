@@ -16,7 +16,6 @@ same-device shards (``ShardGroup``).
 from __future__ import annotations
 
 import ctypes as C
-import json
 import os
 import time
 from dataclasses import dataclass
@@ -190,109 +189,96 @@ class ShardGroup:
 
 # ------------------------------------------------------------------ bench
 
-def bench_main(args) -> None:
-    """bench.py under torchrun with N>1 ranks: the 400M-spring cube
-    (BASELINE.json configs[4], block_scene(313)) split into N x-slabs, one
-    per GPU, halo exchange every substep over peer memory (attach_peers;
-    SS_HALO=nccl: NCCL send/recv).  Strong scaling (fixed lattice)."""
+def bench_slabs(cells: int, precision: str, steps: int, warmup: int, sub: int, layout: str = "auto",
+                rank: int = 0, world: int = 1, dist=None, device: int = 0, clk=None) -> dict:
+    """Time ``block_scene(cells)`` split into ``world`` x-slabs, this rank's
+    slab on ``device``; halo exchange fused into every substep over peer
+    memory (``attach_peers``; SS_HALO=nccl: NCCL send/recv).  ``dist`` is
+    torch.distributed when world > 1.  Returns the job's numbers (the time
+    is the max over ranks): springs, masses, ms, launches, e2e wall, ..."""
+    import sys
+
     import torch
-    import torch.distributed as dist
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    # SS_BENCH_SAME_DEVICE=1 (testing the N>1 path on a one-GPU box): every
-    # rank on cuda:0, host coordination over gloo (NCCL refuses duplicate GPUs)
-    same_device = os.environ.get("SS_BENCH_SAME_DEVICE") == "1"
-    if same_device:
-        local = 0
-    torch.cuda.set_device(local)
-    if same_device:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    red_dev = "cpu" if same_device else "cuda"
-
-    def reduce(value, op):
-        t = torch.tensor([value], device=red_dev)
-        dist.all_reduce(t, op=op)
+    def reduce_max(value):
+        if dist is None:
+            return value
+        t = torch.tensor([value], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
-    cells = args.cells or 313
+
     nx = cells + 1
     n_masses = nx ** 3
     i_lo, i_hi = slab_planes(nx, world, rank)
-    import sys
     t0 = time.perf_counter()
     v_global = excited_velocities(n_masses)
     slab = cube_slab(cells, i_lo, i_hi, v_global=v_global)
     del v_global
     t1 = time.perf_counter()
-    eng = Engine(slab.scene, integrator="verlet", precision=args.precision, layout=args.layout,
-                 device=local)
+    eng = Engine(slab.scene, integrator="verlet", precision=precision, layout=layout, device=device)
     print(f"[rank {rank}] planes [{i_lo},{i_hi}) {slab.scene.spring_count} springs: "
-          f"slab build {t1 - t0:.1f} s, engine {time.perf_counter() - t1:.1f} s", file=sys.stderr,
-          flush=True)
+          f"slab build {t1 - t0:.1f} s, engine {time.perf_counter() - t1:.1f} s", file=sys.stderr, flush=True)
     attach_halo(eng, slab)
-    transport = os.environ.get("SS_HALO", "p2p")
-    if transport == "p2p":
-        ok = 1
-        try:
-            attach_peers(eng, rank, world)
-        except Exception as exc:            # no peer access / IPC: fall back to NCCL everywhere
-            print(f"[rank {rank}] peer-memory halo unavailable ({exc}); using NCCL", file=sys.stderr)
-            ok = 0
-        if not int(reduce(ok, dist.ReduceOp.MIN)):
-            transport = "nccl"
-            if ok:                          # this rank linked, another did not: rebuild without links
-                eng.close()
-                eng = Engine(slab.scene, integrator="verlet", precision=args.precision, layout=args.layout,
-                             device=local)
-                attach_halo(eng, slab)
-    if transport == "nccl":
-        uid = C.create_string_buffer(128)
-        if rank == 0:
-            _lib.check(_lib.lib().ss_nccl_unique_id(uid), "ss_nccl_unique_id")
-        obj = [bytes(uid.raw)]
-        dist.broadcast_object_list(obj, src=0)
-        _lib.check(_lib.lib().ss_halo_nccl(eng.handle, obj[0], world, rank,
-                                           rank - 1 if rank > 0 else -1,
-                                           rank + 1 if rank + 1 < world else -1), "ss_halo_nccl")
+    transport = "none"
+    if world > 1:
+        transport = os.environ.get("SS_HALO", "p2p")
+        if transport == "p2p":
+            ok = 1
+            try:
+                attach_peers(eng, rank, world)
+            except Exception as exc:        # no peer access / IPC: fall back to NCCL everywhere
+                print(f"[rank {rank}] peer-memory halo unavailable ({exc}); using NCCL", file=sys.stderr)
+                ok = 0
+            t = torch.tensor([ok], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            if not int(t.item()):
+                transport = "nccl"
+                if ok:                      # this rank linked, another did not: rebuild without links
+                    eng.close()
+                    eng = Engine(slab.scene, integrator="verlet", precision=precision, layout=layout,
+                                 device=device)
+                    attach_halo(eng, slab)
+        if transport == "nccl":
+            uid = C.create_string_buffer(128)
+            if rank == 0:
+                _lib.check(_lib.lib().ss_nccl_unique_id(uid), "ss_nccl_unique_id")
+            obj = [bytes(uid.raw)]
+            dist.broadcast_object_list(obj, src=0)
+            _lib.check(_lib.lib().ss_halo_nccl(eng.handle, obj[0], world, rank,
+                                               rank - 1 if rank > 0 else -1,
+                                               rank + 1 if rank + 1 < world else -1), "ss_halo_nccl")
     build_s = time.perf_counter() - t0
     info = eng.info()
-    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", local))
-    sub = args.substeps
-    for _ in range(max(args.warmup, 3)):
+    stream = torch.cuda.ExternalStream(eng.stream_ptr, device=torch.device("cuda", device))
+    for _ in range(max(warmup, 3)):
         eng.step_async(sub)
     eng.synchronize()
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     launches0 = eng.launch_count
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.start()
     a.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         eng.step_async(sub)
     b.record(stream)
     b.synchronize()
+    if clk:
+        clk.stop()
     eng.synchronize()
-    ms = float(reduce(a.elapsed_time(b), dist.ReduceOp.MAX))
+    ms = float(reduce_max(a.elapsed_time(b)))
     torch.cuda.synchronize()
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     launches = eng.launch_count - launches0
-    S = slab.springs_global
-    value = S * sub * args.steps / (ms / 1e3)
-    # per-GPU algorithmic bytes of the whole job / time, against N x peak
-    peak = 6550.4
-    pk = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        peak = float(json.load(open(pk))["hbm_gbs"])
-    algo_job = (16 if args.precision == "f32" else 24) * S + (64 if args.precision == "f32" else 128) * n_masses
-    per_sub = ms / 1e3 / (args.steps * sub)
-    achieved = algo_job / per_sub / 1e9 / world
     # e2e through the public API: host state in, positions out (per rank, max over ranks)
     x_h, v_h, xp_h = eng.x.copy(), eng.v.copy(), eng.x_prev.copy()
     e2e_steps = 2
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     w0 = time.perf_counter()
     for _ in range(e2e_steps):
         eng.x = x_h
@@ -300,34 +286,14 @@ def bench_main(args) -> None:
         eng.x_prev = xp_h
         eng.step(sub)
         _ = eng.x
-    ew = float(reduce(time.perf_counter() - w0, dist.ReduceOp.MAX))
+    ew = float(reduce_max(time.perf_counter() - w0))
     n_local = slab.scene.mass_count
-    vec = 16 if args.precision == "f32" else 32
-    if rank == 0:
-        print(json.dumps({
-            "metric": "spring updates/sec (springs x steps / s)", "value": value,
-            "unit": "spring-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": f"cube_n{cells}_sharded_x_slabs_verlet", "cells": cells,
-                       "springs": S, "masses": n_masses, "substeps_per_step": sub,
-                       "integrator": "verlet", "precision": args.precision,
-                       "layout": {1: "csr", 2: "ell", 3: "tile"}[info["layout"]],
-                       "parallelism": (f"x-slab x{world}, halo exchange per substep over "
-                                       + ("peer memory (NVLink P2P stores + device flags)" if transport == "p2p"
-                                          else "NCCL send/recv")) if world > 1
-                                      else "single GPU through the sharded path (no neighbours, no exchange)",
-                       "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
-                       "build_s_rank0": round(build_s, 1),
-                       "l2": "inputs larger than L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": "measured",
-                         "note": "per GPU: whole-job algorithmic bytes / time / N"},
-            "cpu_baseline": None,
-            "e2e": {"value": S * sub * e2e_steps / ew, "unit": "spring-updates/s",
-                    "h2d_bytes_per_step": 3 * n_local * vec * world,
-                    "d2h_bytes_per_step": n_local * vec * world},
-            "gpu_launches": launches,
-        }), flush=True)
+    vec = 16 if precision == "f32" else 32
+    out = {"cells": cells, "springs": slab.springs_global, "masses": n_masses, "ms": ms, "steps": steps,
+           "substeps": sub, "launches": launches, "e2e_wall_s": ew, "e2e_steps": e2e_steps,
+           "h2d_bytes_per_step": 3 * n_local * vec * world, "d2h_bytes_per_step": n_local * vec * world,
+           "transport": transport, "build_s": build_s, "tile_kernel": info["tile_kernel"],
+           "layout": info["layout"], "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
+           "records_bytes": info["tile_blob_bytes"]}
     eng.close()
-    dist.destroy_process_group()
+    return out

@@ -87,7 +87,8 @@ def test_random_scene_fp64_bitwise(seed, n, long_range, lattice, layout, fmt, in
     scene = random_scene(seed, n, long_range=long_range, lattice=lattice)
     eng = Engine(scene, integrator=integrator, precision="f64", layout=layout)
     if fmt is not None and integrator != "rk4":
-        assert eng.info()["tile_kernel"] == fmt
+        # compact fp64 tiles step on tile_f64_kernel (4), explicit ones on step_kernel (0)
+        assert eng.info()["tile_kernel"] == (4 if fmt == 3 else fmt)
     ref = orc.OracleEngine(scene_arrays(scene), integrator=integrator)
     steps = (17, 40) if integrator == "rk4" else (37, 120)
     for count in steps:

@@ -63,3 +63,43 @@ def test_oracle_parallel_det_is_thread_count_invariant():
         eng.step(10)
         outs.append(eng.x.tobytes())
     assert outs[0] == outs[1] == outs[2] == d["x_10"].tobytes()
+
+
+def _digest(a) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for arr in (a.x, a.m, a.si, a.sj, a.k, a.l0):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 20, 42, 91])
+def test_oracle_lattice_builder_matches_reference(n):
+    """oracle_voxel_box (the reference arm's workload builder, a restatement
+    of lattice.py:89-136) against the reference's block_scene digests."""
+    import json
+    import os
+    from conftest import GOLDEN
+    topo = json.load(open(os.path.join(GOLDEN, "topology.json")))
+    a = orc.block_arrays(n)
+    assert _digest(a) == topo[f"block_{n}"]
+
+
+def test_oracle_excite_matches_reference_stream():
+    import hashlib
+    import json
+    import os
+    from conftest import GOLDEN
+    topo = json.load(open(os.path.join(GOLDEN, "topology.json")))
+    a = orc.excite(orc.block_arrays(91), seed=11)
+    assert hashlib.sha256(np.ascontiguousarray(a.v).tobytes()).hexdigest() == topo["excited91_v_sha256"]
+
+
+def test_oracle_box_with_inexact_extent():
+    import json
+    import os
+    from conftest import GOLDEN
+    topo = json.load(open(os.path.join(GOLDEN, "topology.json")))
+    _, x, si, sj, k, l0 = orc.voxel_box((0, 0, 0), (0.3, 0.2, 0.1), 0.1)
+    a = orc.Arrays(x, si, sj, k, l0)
+    assert _digest(a) == topo["box_0.3x0.2x0.1"]
