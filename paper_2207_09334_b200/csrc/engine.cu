@@ -123,7 +123,7 @@ struct ss_engine {
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
     size_t f64_smem = 0;           // fp64 Euler/Verlet compact-format tile kernel (tile_f64.cuh), 0 = off
-    int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3)
+    int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3), 3 (3,3)
     int lean_lanes = 1;            // threads per mass of that kernel (2: scenes with few tiles)
     int persist_max_grid = 0;      // co-resident CTAs of the persistent kernel (0: never persistent)
     bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
@@ -562,6 +562,7 @@ void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
     switch (h->f64_variant) {
         case 1: k = euler ? tile_f64_kernel<0, GROUPS, 1, 4> : tile_f64_kernel<1, GROUPS, 1, 4>; break;
         case 2: k = euler ? tile_f64_kernel<0, GROUPS, 2, 3> : tile_f64_kernel<1, GROUPS, 2, 3>; break;
+        case 3: k = euler ? tile_f64_kernel<0, GROUPS, 3, 3> : tile_f64_kernel<1, GROUPS, 3, 3>; break;
         default: k = euler ? tile_f64_kernel<0, GROUPS, 2, 4> : tile_f64_kernel<1, GROUPS, 2, 4>; break;
     }
     if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
@@ -1194,7 +1195,9 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_f64_kernel<0, false, 1, 4>, tile_f64_kernel<1, false, 1, 4>,
                                  tile_f64_kernel<0, true, 1, 4>, tile_f64_kernel<1, true, 1, 4>,
                                  tile_f64_kernel<0, false, 2, 3>, tile_f64_kernel<1, false, 2, 3>,
-                                 tile_f64_kernel<0, true, 2, 3>, tile_f64_kernel<1, true, 2, 3>})
+                                 tile_f64_kernel<0, true, 2, 3>, tile_f64_kernel<1, true, 2, 3>,
+                                 tile_f64_kernel<0, false, 3, 3>, tile_f64_kernel<1, false, 3, 3>,
+                                 tile_f64_kernel<0, true, 3, 3>, tile_f64_kernel<1, true, 3, 3>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max));
             }
         }

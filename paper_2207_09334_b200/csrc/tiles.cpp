@@ -143,7 +143,8 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
     L = TileLayout{};
     std::vector<int32_t> zcell;
     tile_order(in, L.orig_of, &zcell);
-    const bool bank_aware = !zcell.empty();
+    const char *bank_env = getenv("SS_TILE_BANK");           // 0: dense halo slots (A/B experiments)
+    const bool bank_aware = !zcell.empty() && !(bank_env && atoi(bank_env) == 0);
     const int64_t D = (int64_t)L.orig_of.size();
     L.new_of.assign(N, -1);
     for (int64_t i = 0; i < D; ++i)
