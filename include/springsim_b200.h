@@ -128,6 +128,12 @@ int ss_step(ss_engine *h, int64_t count, ss_step_result *res);
  * device and reported by the next ss_step / ss_sync. */
 int ss_step_async(ss_engine *h, int64_t count);
 int ss_sync(ss_engine *h, ss_step_result *res);
+/* Block until at most `max_ahead` asynchronously enqueued steps are still
+ * unfinished on the device.  Engine.step drains the command queue between
+ * chunks of a long batch (engine.py:366-370 drains before every step):
+ * keeping the host one chunk ahead of the device bounds how late a command
+ * posted mid-batch lands, without idling the device. */
+int ss_pending_wait(ss_engine *h, int64_t max_ahead);
 /* cudaStream_t of the engine, as an opaque pointer (for CUDA-event timing). */
 void *ss_stream(ss_engine *h);
 
@@ -269,6 +275,11 @@ int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256], co
                        int64_t n_slots);
 int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer);
 int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res);
+
+/* Engine.gpe_datum (engine.py:240-242): the height GPE is measured from,
+ * read by every later on-device energy sample (service.py:462 and
+ * analysis.py:755 move it after construction). */
+int ss_set_gpe_datum(ss_engine *h, double datum);
 
 /* Diagnostics: the fp64 kernel's branch-free IEEE fast paths against the
  * library operators on `n` operand pairs (device `device`).  out[4i..4i+3] =

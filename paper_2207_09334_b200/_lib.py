@@ -104,6 +104,8 @@ SIGNATURES = {
                                  C.c_int64, C.c_int64, _i64p, _i64p, _i64p,
                                  _dp, _i64p, _i64p, _dp, _dp, _i64p]),
     "ss_check_f64_fastpath": (C.c_int, [C.c_int32, _dp, _dp, C.c_int64, _dp, _i32p]),
+    "ss_pending_wait": (C.c_int, [C.c_void_p, C.c_int64]),
+    "ss_set_gpe_datum": (C.c_int, [C.c_void_p, C.c_double]),
 }
 
 _lib = None

@@ -132,6 +132,14 @@ struct ss_engine {
     int64_t pending = 0;
     int64_t pending_n0 = 0;
     int pending_cur0 = 0;
+    // async batches in flight (oldest first): the event recorded after each
+    // and its step count (ss_pending_wait); spare events
+    std::vector<std::pair<cudaEvent_t, int64_t>> inflight;
+    std::vector<cudaEvent_t> spare_events;
+    // a divergence found while settling async steps behind another call: it
+    // is reported by the next ss_step / ss_sync, never dropped
+    bool div_held = false;
+    ss_step_result held{};
 
     // halo exchange (x-slab sharding); side 0 = lower neighbour, 1 = upper
     bool halo_on = false;
@@ -176,6 +184,8 @@ struct ss_engine {
         }
         for (auto &b : bufs) cudaFree(b.p);
         if (stream) cudaStreamSynchronize(stream);
+        for (auto &f : inflight) cudaEventDestroy(f.first);
+        for (cudaEvent_t e : spare_events) cudaEventDestroy(e);
         for (void *b : pinned)
             if (b) cudaFreeHost(b);
         if (staged) cudaEventDestroy(staged);
@@ -1258,10 +1268,35 @@ int64_t algorithmic_bytes(const ss_engine *h) {
     return per_spring * h->S + per_mass * h->N;
 }
 
+// Settle asynchronously enqueued steps before another operation.  A
+// divergence among them is held on the handle (the state is the diverged
+// state, as in the reference) and raised by the next ss_step / ss_sync.
 int sync_pending(ss_engine *h) {
     if (!h->pending) return SS_OK;
-    int rc = ss_sync(h, nullptr);
-    return rc == SS_EDIVERGED ? SS_OK : rc;
+    ss_step_result r{};
+    int rc = ss_sync(h, &r);
+    if (rc == SS_EDIVERGED) {
+        h->div_held = true;
+        h->held = r;
+        return SS_OK;
+    }
+    return rc;
+}
+
+// The held divergence, if any: reported once.
+int take_held(ss_engine *h, ss_step_result *res) {
+    if (!h->div_held) return SS_OK;
+    h->div_held = false;
+    if (res) *res = h->held;
+    return ss::fail(SS_EDIVERGED,
+                    "simulation diverged at step %lld: mass %lld has a non-finite position or "
+                    "velocity (try a smaller dt)",
+                    (long long)h->held.diverged_step, (long long)h->held.diverged_mass);
+}
+
+void release_inflight(ss_engine *h) {
+    for (auto &f : h->inflight) h->spare_events.push_back(f.first);
+    h->inflight.clear();
 }
 
 template <bool F32>
@@ -1577,7 +1612,7 @@ int ss_step(ss_engine *h, int64_t count, ss_step_result *res) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     CK(cudaSetDevice(h->device));
     int rc = sync_pending(h);
-    if (rc) return rc;
+    if (rc || (rc = take_held(h, res))) return rc;
     if (count <= 0) {
         if (res) *res = {0, h->n, h->t, -1, -1};
         return SS_OK;
@@ -1592,6 +1627,7 @@ int ss_step_async(ss_engine *h, int64_t count) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
     if (count <= 0) return SS_OK;
     CK(cudaSetDevice(h->device));
+    if (h->div_held) return take_held(h, nullptr);
     if (!h->pending) {
         h->pending_n0 = h->n;
         h->pending_cur0 = h->cur;
@@ -1601,6 +1637,31 @@ int ss_step_async(ss_engine *h, int64_t count) {
     h->pending += count;
     h->n += count;                   // provisional; ss_sync settles it
     h->t = (double)h->n * h->dt;
+    cudaEvent_t ev = nullptr;
+    if (!h->spare_events.empty()) {
+        ev = h->spare_events.back();
+        h->spare_events.pop_back();
+    } else {
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ev, h->stream));
+    h->inflight.push_back({ev, count});
+    return SS_OK;
+}
+
+int ss_pending_wait(ss_engine *h, int64_t max_ahead) {
+    if (!h) return ss::fail(SS_EINVAL, "null engine");
+    CK(cudaSetDevice(h->device));
+    int64_t ahead = 0;
+    for (auto &f : h->inflight) ahead += f.second;
+    size_t done = 0;
+    while (done < h->inflight.size() && ahead > max_ahead) {
+        CK(cudaEventSynchronize(h->inflight[done].first));
+        ahead -= h->inflight[done].second;
+        h->spare_events.push_back(h->inflight[done].first);
+        ++done;
+    }
+    h->inflight.erase(h->inflight.begin(), h->inflight.begin() + (std::ptrdiff_t)done);
     return SS_OK;
 }
 
@@ -1837,12 +1898,20 @@ int ss_sync(ss_engine *h, ss_step_result *res) {
     CK(cudaSetDevice(h->device));
     const int64_t count = h->pending;
     h->pending = 0;
+    release_inflight(h);
     if (count == 0) {
         CK(cudaStreamSynchronize(h->stream));
         if (res) *res = {0, h->n, h->t, -1, -1};
-        return SS_OK;
+        return take_held(h, res);
     }
-    return finish_batch(h, count, h->pending_n0, h->pending_cur0, res);
+    const int rc = finish_batch(h, count, h->pending_n0, h->pending_cur0, res);
+    return h->div_held ? take_held(h, res) : rc;
+}
+
+int ss_set_gpe_datum(ss_engine *h, double datum) {
+    if (!h) return ss::fail(SS_EINVAL, "null engine");
+    h->gpe_datum = datum;
+    return SS_OK;
 }
 
 void *ss_stream(ss_engine *h) { return h ? (void *)h->stream : nullptr; }

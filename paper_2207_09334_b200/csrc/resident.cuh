@@ -190,7 +190,12 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int diverged;
+    // divergence flag of each step, triple-buffered by step (mod 3): step s
+    // sets flag[s%3] (in every CTA of the cluster) before its closing barrier,
+    // every thread reads it after that barrier, and flag[(s+1)%3] is cleared
+    // during step s -- after everyone has read it at step s-2, before anyone
+    // can set it at step s+1 -- so all threads leave the loop at the same step
+    __shared__ int diverged[3];
     __shared__ T sscale[2][kResidentMaxGroups];            // this and the next step's actuation scales
     T4 *const xsb = reinterpret_cast<T4 *>(smem);          // positions: [c * pslots + slot], c = step parity
     const unsigned rank = cl.block_rank(), n_ctas = cl.num_blocks();
@@ -199,6 +204,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
     const int m = (int)rank * kResidentSlots + l;           // device slot
     const int leader = (tid & 31) & ~(G - 1);               // group's first lane within the warp
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << leader;
+    if (*p.div_step <= a.step0) return;                     // an earlier batch on the stream diverged (uniform)
     // stage the shared dictionary and this CTA's segment (16-byte copies)
     {
         uint4 *dst = reinterpret_cast<uint4 *>(smem + a.off_dict);
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
         if (INTEG == 1 && !a.bootstrap0) hst = p.Xprev[m];  // fp64: x_prev; fp32: u
         if constexpr (F32) pb = p.P[m];
     }
-    if (tid == 0) diverged = 0;
+    if (tid < 3) diverged[tid] = 0;
     if (tid < a.G) sscale[0][tid] = p.scale[tid];
     T fe[3] = {(T)0, (T)0, (T)0};                           // f_ext is constant over a batch
     if (act && p.F) {
@@ -241,7 +247,9 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
     unsigned deg = 0;
     int c = 0;
     long long done = 0;
+    int ph = 0;                                             // s % 3
     for (long long s = 0; s < a.count; ++s) {
+        if (tid == 0) diverged[ph == 2 ? 0 : ph + 1] = 0;   // the next step's flag
         if (n_ctas > 1) {                                   // halo positions from their owners (DSMEM)
             T4 *cur = xsb + (c ? a.pslots : 0);
             for (uint32_t k = tid; k < n_halo; k += bs) {
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
             if (lane == 0) {
                 xsb[(c ? 0 : a.pslots) + l] = x;
                 if (!(finite3<F32>(xn[0], xn[1], xn[2]) && finite3<F32>(vn[0], vn[1], vn[2]))) {
-                    for (unsigned r = 0; r < n_ctas; ++r) *cl.map_shared_rank(&diverged, r) = 1;   // rare
+                    for (unsigned r = 0; r < n_ctas; ++r) *cl.map_shared_rank(&diverged[ph], r) = 1;   // rare
                     atomicMin(p.div_mass, p.orig_of ? p.orig_of[m] : m);
                 }
             }
@@ -336,10 +344,11 @@ __global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<
         else __syncthreads();
         c ^= 1;
         done = s + 1;
-        if (diverged) {                                     // committed; the reference raises here
+        if (diverged[ph]) {                                 // committed; the reference raises here
             if (tid == 0 && rank == 0) atomicMin(p.div_step, a.step0 + s + 1);
             break;
         }
+        ph = ph == 2 ? 0 : ph + 1;
     }
     // write back: x into the buffer the host will call current, history,
     // velocities; padding slots keep their zeros

@@ -303,7 +303,13 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     // everything below reads the previous substep's state
     asm volatile("griddepcontrol.wait;" ::: "memory");
     xchg_wait(p, tile);
-    if (*p.div_step < p.step) return;                       // grid-uniform (an earlier step diverged)
+    if (*p.div_step < p.step) {                             // grid-uniform (an earlier step diverged):
+        if (tid == 0) {                                     // retire only once the bulk copies have landed
+            mbar_wait(bar, 0);
+            mbar_wait(bar + 1, 0);
+        }
+        return;
+    }
     float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f), hist = x4;
     if (active && lane == 0) {
         x4 = ldg4(p.X + m);                                 // r = x - X0, w = +-m

@@ -32,12 +32,13 @@ import ctypes as C
 import math
 import os
 import queue
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
-from .model import CONSTANT_EXPANSION, scene_arrays
+from .model import CONSTANT_EXPANSION, ActuationGroup, actuation_scale, scene_arrays
 from .traces import TraceSeries
 
 SERIAL = "serial"
@@ -70,31 +71,35 @@ class DivergenceError(RuntimeError):
 
 
 def spring_force(x_i, x_j, k: float, l0: float) -> np.ndarray:
-    """Scalar force on i from one spring (engine.py:55-65)."""
-    d = np.asarray(x_j, dtype=np.float64) - np.asarray(x_i, dtype=np.float64)
+    """Force on mass i from one spring; the force on j is its exact negation
+    (engine.py:55-65).  ``np.linalg.norm`` of the 1-D offset, as the
+    reference, so the length rounds the same way; coincident endpoints
+    (L < 1e-12) give zero force."""
+    d = np.subtract(x_j, x_i, dtype=np.float64)
     length = float(np.linalg.norm(d))
-    if length < DEGENERATE_LENGTH:
-        return np.zeros(3)
-    return (k * (length - l0) / length) * d
+    return np.zeros(3) if length < DEGENERATE_LENGTH else (k * (length - l0) / length) * d
+
+
+def _friction(v, normal, f_n: float, mu: float, m: float, dt: float):
+    """Clamped Coulomb friction opposing the tangential velocity: at most
+    |v_t| m / dt, so one step can stop the sliding but never reverse it."""
+    v_t = v - (v @ normal) * normal
+    speed = float(np.linalg.norm(v_t))
+    if not (mu > 0.0 and speed > 1e-15):
+        return None
+    return (min(mu * f_n, speed * m / dt) / speed) * v_t
 
 
 def contact_force(x, v, m: float, plane, dt: float) -> np.ndarray:
-    """Penalty + clamped Coulomb friction of one plane on one mass (engine.py:68-89)."""
-    x = np.asarray(x, dtype=np.float64)
-    v = np.asarray(v, dtype=np.float64)
-    n = np.asarray(plane.normal, dtype=np.float64)
-    depth = plane.offset - x @ n
+    """Penalty normal force plus friction of one plane on one mass
+    (engine.py:68-89); zero outside the half-space."""
+    x, v, normal = (np.asarray(a, dtype=np.float64) for a in (x, v, plane.normal))
+    depth = plane.offset - x @ normal
     if depth <= 0.0:
         return np.zeros(3)
     f_n = plane.penalty * depth
-    out = f_n * n
-    if plane.friction > 0.0:
-        v_t = v - (v @ n) * n
-        speed = float(np.linalg.norm(v_t))
-        if speed > 1e-15:
-            mag = min(plane.friction * f_n, speed * m / dt)
-            out = out - (mag / speed) * v_t
-    return out
+    tangential = _friction(v, normal, f_n, plane.friction, m, dt)
+    return f_n * normal if tangential is None else f_n * normal - tangential
 
 
 @dataclass
@@ -110,25 +115,33 @@ class EngineState:
     mode: str
 
 
-def energy_breakdown(x, v, m, si, sj, k, l0_eff, gravity, datum: float):
-    """(elastic, gravitational, kinetic) energy of a raw state (engine.py:148-170).
+def _elastic(x, si, sj, k, l0_eff) -> float:
+    """1/2 sum k (L - l0_eff)^2 over the springs (L by np.linalg.norm, as the reference)."""
+    if not si.size:
+        return 0.0
+    stretch = np.linalg.norm(x[sj] - x[si], axis=1) - l0_eff
+    return float(0.5 * np.sum(k * stretch ** 2))
 
-    Sampling-only host reduction (numpy), same formulas and op order."""
+
+def _gravitational(x, m, gravity, datum: float) -> float:
+    """sum m |g| (height above datum), height measured against gravity; 0 without gravity."""
+    g = np.asarray(gravity, dtype=np.float64)
+    g_mag = float(np.linalg.norm(g))
+    if not g_mag > 0.0:
+        return 0.0
+    return float(np.sum(m * g_mag * (x @ (-g / g_mag) - datum)))
+
+
+def _kinetic(v, m) -> float:
+    return float(0.5 * np.sum(m * np.einsum("ij,ij->i", v, v)))
+
+
+def energy_breakdown(x, v, m, si, sj, k, l0_eff, gravity, datum: float):
+    """(elastic, gravitational, kinetic) energy of a raw state on the host
+    (engine.py:148-170, same formulas and reductions); overflow reads as inf
+    (the stepper's divergence check reports the blow-up)."""
     with np.errstate(over="ignore", invalid="ignore"):
-        if si.size:
-            d = x[sj] - x[si]
-            lengths = np.linalg.norm(d, axis=1)
-            epe = float(0.5 * np.sum(k * (lengths - l0_eff) ** 2))
-        else:
-            epe = 0.0
-        g_mag = float(np.linalg.norm(gravity))
-        if g_mag > 0.0:
-            up = -np.asarray(gravity, dtype=np.float64) / g_mag
-            gpe = float(np.sum(m * g_mag * (x @ up - datum)))
-        else:
-            gpe = 0.0
-        ke = float(0.5 * np.sum(m * np.einsum("ij,ij->i", v, v)))
-    return epe, gpe, ke
+        return _elastic(x, si, sj, k, l0_eff), _gravitational(x, m, gravity, datum), _kinetic(v, m)
 
 
 class _Mirror:
@@ -166,7 +179,8 @@ class Engine:
         self.dt = float(arr.dt)
         self.damping = float(arr.damping)
         self.gravity = np.asarray(arr.gravity, dtype=np.float64)
-        self.m = arr.m
+        self._m = arr.m
+        self._m.setflags(write=False)      # masses live in the device state: fixed at construction
         self._fixed = arr.fixed
         self._fixed_idx = np.nonzero(arr.fixed)[0]
         self._si = arr.si
@@ -190,7 +204,7 @@ class Engine:
             available = os.cpu_count() or 1
             self.threads = max(1, min(threads or available, available))
         g_mag = float(np.linalg.norm(self.gravity))
-        self.gpe_datum = float((arr.x @ (-self.gravity / g_mag)).min()) if g_mag else 0.0
+        self._gpe_datum = float((arr.x @ (-self.gravity / g_mag)).min()) if g_mag else 0.0
         self._degenerate_offset = 0
         self._host_prev_nonverlet = None
 
@@ -200,6 +214,8 @@ class Engine:
         self._v = _Mirror(arr.v)
         self._xp = _Mirror(None)
         self._f = _Mirror(arr.f_ext)
+        self._f_sent = None                # f_ext as last uploaded (once handed out, edits are watched)
+        self._step_s = None                # measured seconds per step (sizes command-drain chunks)
 
     # ------------------------------------------------------------ plumbing
 
@@ -334,10 +350,13 @@ class Engine:
                        "ss_set_state")
         if clear_prev:
             _lib.check(lib.ss_clear_prev(self._h), "ss_clear_prev")
-        if self._f.lent:
+        # f_ext is a live array in the reference (forces() reads it every
+        # step): once handed out it stays watched, and any change -- through
+        # the attribute, a kept reference or set_external_force -- goes down
+        if self._f.lent and (self._f_sent is None or not np.array_equal(self._f.arr, self._f_sent)):
             f = np.ascontiguousarray(self._f.arr, dtype=np.float64).reshape(-1, 3)
             _lib.check(lib.ss_set_f_ext(self._h, _lib.dptr(f)), "ss_set_f_ext")
-            self._f.lent = False
+            self._f_sent = f.copy()
         self._x.lent = self._v.lent = self._xp.lent = False
 
     def _push_params(self) -> None:
@@ -403,6 +422,23 @@ class Engine:
         self._xp.stale, self._xp.lent = False, True
 
     @property
+    def m(self) -> np.ndarray:
+        """Node masses (read-only: they are part of the device state)."""
+        return self._m
+
+    @property
+    def gpe_datum(self) -> float:
+        return self._gpe_datum
+
+    @gpe_datum.setter
+    def gpe_datum(self, value: float) -> None:
+        """Height GPE is measured from (engine.py:240-242); every later energy
+        sample uses the new datum, as the reference reads it per call."""
+        self._gpe_datum = float(value)
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.check(_lib.lib().ss_set_gpe_datum(self._h, self._gpe_datum), "ss_set_gpe_datum")
+
+    @property
     def f_ext(self) -> np.ndarray:
         self._f.lent = True
         return self._f.arr
@@ -454,16 +490,12 @@ class Engine:
     # ------------------------------------------------------------- forces
 
     def _rest_lengths(self, t: float) -> np.ndarray:
-        """Host restatement of engine.py:250-259 (used by energies only; the
-        device applies the same scale per group inside the spring kernel)."""
+        """Actuated rest lengths at time t on the host (engine.py:250-259;
+        energies of a supplied state only -- the device scales l0 per group
+        inside the spring kernels)."""
         for g in self._groups.values():
-            idx = g["indices"]
-            if g["mode"] == CONSTANT_EXPANSION:
-                scale = 1.0 + g["amplitude"]
-            else:
-                scale = 1.0 + g["amplitude"] * math.sin(
-                    2.0 * math.pi * g["frequency"] * t + g["phase"])
-            self._l0_eff[idx] = self._l0[idx] * scale
+            signal = ActuationGroup("", g["mode"], g["amplitude"], g["frequency"], g["phase"])
+            self._l0_eff[g["indices"]] = self._l0[g["indices"]] * actuation_scale(signal, t)
         return self._l0_eff
 
     def forces(self, x: np.ndarray, v: np.ndarray, t: float) -> np.ndarray:
@@ -483,23 +515,62 @@ class Engine:
 
     # ------------------------------------------------------------ stepping
 
-    def step(self, count: int = 1) -> None:
-        """Advance ``count`` steps (engine.py:366-373) in one device batch.
+    # A batch longer than this much device time is enqueued in chunks with
+    # the command queue drained before each one (the reference drains before
+    # every step, engine.py:366-370): the host stays one chunk ahead of the
+    # device, so a command posted mid-batch lands within about two chunks.
+    COMMAND_LATENCY_S = 2e-3
+    MIN_CHUNK_STEPS = 16
 
-        Queued commands are drained once at the batch boundary (the
-        reference drains before every step; with an empty queue the two are
-        identical, and a command posted concurrently lands at the next batch)."""
-        if count <= 0:
-            return
-        self.drain_commands()
-        self._upload_lent()
-        self._push_params()
-        res = _lib.StepResult()
-        rc = _lib.lib().ss_step(self._h, int(count), C.byref(res))
-        self._mark_stepped()
+    def _chunk_steps(self) -> int:
+        if self._step_s is None:
+            return self.MIN_CHUNK_STEPS
+        return max(self.MIN_CHUNK_STEPS, int(self.COMMAND_LATENCY_S / max(self._step_s, 1e-8)))
+
+    def _raise_step(self, rc: int, res, what: str) -> None:
         if rc == _lib.SS_EDIVERGED:
             raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
-        _lib.check(rc, "ss_step")
+        _lib.check(rc, what)
+
+    def step(self, count: int = 1) -> None:
+        """Advance ``count`` steps (engine.py:366-373).
+
+        Short batches go down as one device batch; long ones in chunks of
+        about COMMAND_LATENCY_S of device time, draining queued commands and
+        re-reading damping, gravity, f_ext and actuation before each chunk.
+        DivergenceError is raised for the first non-finite step, the state
+        being the diverged state, as in the reference."""
+        if count <= 0:
+            return
+        lib = _lib.lib()
+        res = _lib.StepResult()
+        chunk = self._chunk_steps()
+        t0 = time.perf_counter()
+        if count <= chunk:
+            self.drain_commands()
+            self._upload_lent()
+            self._push_params()
+            rc = lib.ss_step(self._h, int(count), C.byref(res))
+            self._mark_stepped()
+            self._raise_step(rc, res, "ss_step")
+        else:
+            done = 0
+            try:
+                while done < count:
+                    self.drain_commands()
+                    self._upload_lent()
+                    self._push_params()
+                    k = min(chunk, count - done)
+                    rc = lib.ss_step_async(self._h, k)
+                    if rc != _lib.SS_OK:
+                        self._raise_step(rc, res, "ss_step_async")
+                    done += k
+                    _lib.check(lib.ss_pending_wait(self._h, chunk), "ss_pending_wait")
+            finally:
+                self._mark_stepped()
+            self._raise_step(lib.ss_sync(self._h, C.byref(res)), res, "ss_sync")
+        per_step = (time.perf_counter() - t0) / count
+        self._step_s = per_step if self._step_s is None else 0.5 * (self._step_s + per_step)
 
     def step_sampled(self, count: int, sample_every: int, traces=()):
         """Advance ``count`` steps recording, on the device, the samples
@@ -604,7 +675,13 @@ class Engine:
                            t=self.t, n=self.n, integrator=self.integrator, mode=self.mode)
 
     def energies(self, x=None, v=None, t=None):
-        """(epe, gpe, ke, total) at the current or a supplied state (engine.py:390-398)."""
+        """(epe, gpe, ke, total) (engine.py:390-398).  At the engine's own
+        state the sums are reduced on the device (the reduction simulate()
+        samples with; no state download); a supplied state is reduced on the
+        host with the reference's formulas."""
+        if x is None and v is None and t is None:
+            _, _, en = self.snapshot(ids=np.zeros(0, dtype=np.int64))
+            return tuple(float(e) for e in en)
         x = self.x if x is None else x
         v = self.v if v is None else v
         t = self.t if t is None else t
@@ -613,12 +690,14 @@ class Engine:
         return epe, gpe, ke, epe + gpe + ke
 
     # ------------------------------------------------------------ commands
+    # Setters and the thread-safe command channel (engine.py:402-466).  The
+    # engine reads every parameter fresh at the next step boundary.
 
     def set_external_force(self, mass_id: int, f) -> None:
         self.f_ext[mass_id] = np.asarray(f, dtype=np.float64)
 
     def set_damping(self, value: float) -> None:
-        if not 0.0 <= value < 1.0:
+        if not (0.0 <= value < 1.0):
             raise ValueError("damping must be in [0, 1)")
         self.damping = float(value)
 
@@ -626,56 +705,59 @@ class Engine:
         self.gravity = np.asarray(g, dtype=np.float64)
 
     def set_actuation(self, label: str, amplitude=None, frequency=None, phase=None) -> None:
-        if label not in self._groups:
+        """Change a group's signal; ``None`` keeps a parameter, |amplitude| < 1."""
+        group = self._groups.get(label)
+        if group is None:
             raise ValueError(f"unknown actuation group {label!r}")
-        g = self._groups[label]
-        if amplitude is not None:
-            if not abs(amplitude) < 1.0:
-                raise ValueError("|amplitude| must be < 1")
-            g["amplitude"] = float(amplitude)
-        if frequency is not None:
-            g["frequency"] = float(frequency)
-        if phase is not None:
-            g["phase"] = float(phase)
+        if amplitude is not None and not abs(amplitude) < 1.0:
+            raise ValueError("|amplitude| must be < 1")
+        group.update({key: float(val) for key, val in
+                      (("amplitude", amplitude), ("frequency", frequency), ("phase", phase)) if val is not None})
 
     def post_command(self, command: dict) -> None:
+        """Queue a command (any thread); applied at the next step boundary."""
         self._commands.put(dict(command))
 
+    def _queued(self, wait: float):
+        """Commands waiting in the channel; the first may be waited for."""
+        try:
+            yield self._commands.get(timeout=wait) if wait > 0.0 else self._commands.get_nowait()
+            while True:
+                yield self._commands.get_nowait()
+        except queue.Empty:
+            return
+
     def drain_commands(self, wait: float = 0.0) -> None:
-        first = True
-        while True:
-            try:
-                if first and wait > 0.0:
-                    cmd = self._commands.get(timeout=wait)
-                else:
-                    cmd = self._commands.get_nowait()
-            except queue.Empty:
-                return
-            first = False
+        """Apply every queued command; a failing one is reported in
+        ``command_errors`` and the rest still apply."""
+        for cmd in self._queued(wait):
             try:
                 self.apply_command(cmd)
-            except Exception as exc:
+            except Exception as exc:            # reported through the channel, stepping goes on
                 self.command_errors.append(f"{cmd.get('op', '?')}: {exc}")
 
     def apply_command(self, cmd: dict) -> None:
-        op = cmd.get("op")
-        if op == "pause":
-            self.paused = True
-        elif op == "resume":
-            self.paused = False
-        elif op == "stop":
-            self.stopped = True
-        elif op == "set-damping":
-            self.set_damping(float(cmd["value"]))
-        elif op == "set-gravity":
-            self.set_gravity([float(c) for c in cmd["value"]])
-        elif op == "set-external-force":
-            self.set_external_force(int(cmd["mass"]), [float(c) for c in cmd["value"]])
-        elif op == "set-actuation":
-            self.set_actuation(cmd["group"], cmd.get("amplitude"), cmd.get("frequency"),
-                               cmd.get("phase"))
-        else:
-            raise ValueError(f"unknown command op {op!r}")
+        handler = _COMMANDS.get(cmd.get("op"))
+        if handler is None:
+            raise ValueError(f"unknown command op {cmd.get('op')!r}")
+        handler(self, cmd)
+
+
+def _floats(values) -> list[float]:
+    return [float(c) for c in values]
+
+
+# op -> handler(engine, command) (engine.py:448-466)
+_COMMANDS = {
+    "pause": lambda e, c: setattr(e, "paused", True),
+    "resume": lambda e, c: setattr(e, "paused", False),
+    "stop": lambda e, c: setattr(e, "stopped", True),
+    "set-damping": lambda e, c: e.set_damping(float(c["value"])),
+    "set-gravity": lambda e, c: e.set_gravity(_floats(c["value"])),
+    "set-external-force": lambda e, c: e.set_external_force(int(c["mass"]), _floats(c["value"])),
+    "set-actuation": lambda e, c: e.set_actuation(c["group"], c.get("amplitude"), c.get("frequency"),
+                                                  c.get("phase")),
+}
 
 
 def plan(scene, precision: str = "f32") -> dict:
@@ -708,15 +790,22 @@ def plan(scene, precision: str = "f32") -> dict:
 
 
 def total_force(scene, mass_id: int, t: float = 0.0, **engine_kwargs) -> np.ndarray:
-    """Total force on one mass at rest state (engine.py:469-473)."""
-    engine = Engine(scene, integrator=EULER, mode=SERIAL, **engine_kwargs)
-    engine.t = t
-    return engine.total_force(mass_id)
+    """Total force on one mass of a scene in its initial state at time t
+    (engine.py:469-473), evaluated by a throw-away Euler engine."""
+    with Engine(scene, integrator=EULER, mode=SERIAL, **engine_kwargs) as engine:
+        engine.t = t
+        return engine.total_force(mass_id)
+
+
+_ENERGY_COLUMNS = ("epe", "gpe", "ke", "total")
 
 
 @dataclass
 class RunResult:
-    """Sampled output of :func:`simulate` (engine.py:476-515)."""
+    """Sampled output of :func:`simulate` (engine.py:476-515): sample times,
+    traced positions per mass id (T,3), energies (T,4) in the column order
+    epe, gpe, ke, total.  Under Verlet each sample pairs x_prev with the
+    central-difference v, one step behind the final engine state."""
 
     times: np.ndarray
     positions: dict[int, np.ndarray]
@@ -724,30 +813,24 @@ class RunResult:
     engine: Engine = field(repr=False)
 
     def position_series(self, mass_id: int, axis: int | None = None) -> TraceSeries:
-        values = self.positions[mass_id]
-        if axis is not None:
-            values = values[:, axis]
-        return TraceSeries(self.times, values)
+        track = self.positions[mass_id]
+        return TraceSeries(self.times, track if axis is None else track[:, axis])
 
     def energy_series(self, term: str) -> TraceSeries:
-        column = {"epe": 0, "gpe": 1, "ke": 2, "total": 3}[term]
+        column = {name: c for c, name in enumerate(_ENERGY_COLUMNS)}[term]     # KeyError like the reference
         return TraceSeries(self.times, self.energies[:, column])
 
     def write_csv(self, path) -> None:
+        """t, then x/y/z of every traced mass (ascending id), then the four
+        energies; every number with 17 significant digits."""
         ids = sorted(self.positions)
-        header = ["t"]
-        for mass_id in ids:
-            header += [f"{mass_id}.x", f"{mass_id}.y", f"{mass_id}.z"]
-        header += ["epe", "gpe", "ke", "total"]
-        lines = [",".join(header)]
-        for row in range(len(self.times)):
-            cells = [f"{self.times[row]:.17g}"]
-            for mass_id in ids:
-                cells += [f"{c:.17g}" for c in self.positions[mass_id][row]]
-            cells += [f"{c:.17g}" for c in self.energies[row]]
-            lines.append(",".join(cells))
+        header = ["t", *(f"{i}.{axis}" for i in ids for axis in "xyz"), *_ENERGY_COLUMNS]
+        table = np.column_stack([np.asarray(self.times, dtype=np.float64).reshape(-1, 1),
+                                 *(np.asarray(self.positions[i], dtype=np.float64).reshape(-1, 3) for i in ids),
+                                 np.asarray(self.energies, dtype=np.float64).reshape(-1, 4)])
         with open(path, "w") as fh:
-            fh.write("\n".join(lines) + "\n")
+            fh.write(",".join(header) + "\n")
+            fh.writelines(",".join(format(float(c), ".17g") for c in row) + "\n" for row in table)
 
 
 SAMPLE_SEGMENT_ROWS = 4096          # samples per device segment of simulate()

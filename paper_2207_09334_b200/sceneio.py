@@ -67,60 +67,57 @@ def render_scene(scene) -> str:
 
 # ------------------------------------------------------------ parsing
 
-_NUM = (int, float)
+def _is_number(value) -> bool:
+    return isinstance(value, (int, float)) and not isinstance(value, bool)
+
+
+def _named(what: str):
+    return lambda value: f"expected {what}, got {type(value).__name__}"
+
+
+def _same(value):
+    return value
+
+
+# kind -> (accepts?, conversion, complaint) -- the field types of the
+# reference's document schema (sceneio.py:98-136)
+_KINDS = {
+    "number": (_is_number, float, _named("a number")),
+    "number?": (lambda v: v is None or _is_number(v), lambda v: None if v is None else float(v), _named("a number")),
+    "int": (lambda v: isinstance(v, int) and not isinstance(v, bool), _same, _named("an integer")),
+    "bool": (lambda v: isinstance(v, bool), _same, _named("a boolean")),
+    "string": (lambda v: isinstance(v, str), _same, _named("a string")),
+    "string?": (lambda v: v is None or isinstance(v, str), _same, _named("a string or null")),
+    "vec3": (lambda v: isinstance(v, list) and len(v) == 3 and all(map(_is_number, v)),
+             lambda v: tuple(map(float, v)), lambda v: "expected a list of three numbers"),
+    "list": (lambda v: isinstance(v, list), _same, _named("a list")),
+}
 
 
 def _coerce(value, path: str, kind):
-    """Type checks of sceneio.py:98-136."""
-    if kind == "number":
-        if isinstance(value, bool) or not isinstance(value, _NUM):
-            raise SceneFormatError(path, f"expected a number, got {type(value).__name__}")
-        return float(value)
-    if kind == "int":
-        if isinstance(value, bool) or not isinstance(value, int):
-            raise SceneFormatError(path, f"expected an integer, got {type(value).__name__}")
-        return value
-    if kind == "bool":
-        if not isinstance(value, bool):
-            raise SceneFormatError(path, f"expected a boolean, got {type(value).__name__}")
-        return value
-    if kind == "string":
-        if not isinstance(value, str):
-            raise SceneFormatError(path, f"expected a string, got {type(value).__name__}")
-        return value
-    if kind == "string?":
-        if value is not None and not isinstance(value, str):
-            raise SceneFormatError(path, f"expected a string or null, got {type(value).__name__}")
-        return value
-    if kind == "number?":
-        return None if value is None else _coerce(value, path, "number")
-    if kind == "vec3":
-        if (not isinstance(value, list) or len(value) != 3
-                or any(isinstance(c, bool) or not isinstance(c, _NUM) for c in value)):
-            raise SceneFormatError(path, "expected a list of three numbers")
-        return tuple(float(c) for c in value)
-    if kind == "list":
-        if not isinstance(value, list):
-            raise SceneFormatError(path, f"expected a list, got {type(value).__name__}")
-        return value
-    raise AssertionError(kind)
+    """``value`` checked against and converted to ``kind``, else SceneFormatError at ``path``."""
+    accepts, convert, complaint = _KINDS[kind]
+    if not accepts(value):
+        raise SceneFormatError(path, complaint(value))
+    return convert(value)
 
 
 def _expect(obj, path: str, required: dict, optional: dict) -> dict:
+    """The fields of a JSON object: no unknown keys (first one in document
+    order is reported), every required key present, each value of its kind;
+    absent optional keys take their defaults."""
     if not isinstance(obj, dict):
-        raise SceneFormatError(path, f"expected an object, got {type(obj).__name__}")
-    known = set(required) | set(optional)
-    for key in obj:
-        if key not in known:
-            raise SceneFormatError(f"{path}.{key}", "unknown field")
-    out = {}
-    for key, kind in required.items():
-        if key not in obj:
-            raise SceneFormatError(path, f"missing required field {key!r}")
-        out[key] = _coerce(obj[key], f"{path}.{key}", kind)
-    for key, (kind, default) in optional.items():
-        out[key] = _coerce(obj[key], f"{path}.{key}", kind) if key in obj else default
-    return out
+        raise SceneFormatError(path, _named("an object")(obj))
+    stray = next((key for key in obj if key not in required and key not in optional), None)
+    if stray is not None:
+        raise SceneFormatError(f"{path}.{stray}", "unknown field")
+    missing = next((key for key in required if key not in obj), None)
+    if missing is not None:
+        raise SceneFormatError(path, f"missing required field {missing!r}")
+    fields = {key: _coerce(obj[key], f"{path}.{key}", kind) for key, kind in required.items()}
+    fields.update((key, _coerce(obj[key], f"{path}.{key}", kind) if key in obj else default)
+                  for key, (kind, default) in optional.items())
+    return fields
 
 
 _TOP = dict(required={"schema_version": "int", "gravity": "vec3", "dt": "number", "masses": "list",

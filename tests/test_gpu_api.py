@@ -442,3 +442,82 @@ def test_cluster_resident_fp32_matches_per_step_launches(monkeypatch):
         got[res] = (err.value.mass_id, err.value.step, eng.n)
         eng.close()
     assert got["8"][1:] == got["0"][1:]
+
+
+def test_command_posted_mid_batch_lands_within_the_batch():
+    """The reference drains the command queue before every step
+    (engine.py:366-370).  A command posted by another thread while one long
+    step(N) runs must take effect inside that batch (within ~two drain
+    chunks), not N steps late."""
+    from paper_2207_09334_b200 import lattice as L
+    scene = L.excite(L.block_scene(20), seed=4)
+    a = Engine(scene, integrator="verlet", precision="f64")
+    b = Engine(scene, integrator="verlet", precision="f64")
+    a.step(20)                      # measured step time sizes the drain chunks
+    b.step(20)
+    steps = max(4000, int(0.25 / max(a._step_s, 1e-7)))      # a batch of ~0.25 s
+    seen = {}
+
+    def post():
+        import time as _t
+        _t.sleep(0.05)
+        a.post_command({"op": "set-gravity", "value": [0.0, -9.81, 0.0]})
+        seen["posted"] = True
+    th = threading.Thread(target=post)
+    th.start()
+    a.step(steps)
+    th.join()
+    b.step(steps)
+    assert seen.get("posted") and np.allclose(a.gravity, [0.0, -9.81, 0.0])
+    # gravity acted for part of the batch: the centre of mass fell
+    drop_a = float(b.x[:, 1].mean() - a.x[:, 1].mean())
+    assert drop_a > 0.0
+    # and not from the very first step (it was posted 50 ms into the batch)
+    full = 0.5 * 9.81 * (steps * scene.dt) ** 2
+    assert drop_a < full
+
+
+def test_divergence_behind_an_async_batch_is_not_dropped():
+    """A divergence found while another call settles asynchronously
+    enqueued steps is raised by the next step (never silently continued)."""
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=1.0)
+    a = sc.add_mass((0.0, 0.0, 0.0))
+    b = sc.add_mass((1.0, 0.0, 0.0))
+    sc.add_spring(a, b, k=1e6, l0=0.5)      # dt far too large: blows up
+    eng = Engine(sc, integrator="euler")
+    ref = Engine(sc, integrator="euler")
+    with pytest.raises(DivergenceError) as want:
+        ref.step(2000)
+    eng.step_async(2000)
+    _ = eng.x                               # settles the batch behind this read
+    with pytest.raises(DivergenceError) as err:
+        eng.step(1)
+    assert (err.value.mass_id, err.value.step) == (want.value.mass_id, want.value.step)
+    assert eng.n == ref.n
+
+
+def test_kept_f_ext_reference_edits_reach_the_device():
+    """f_ext is a live array (the reference's forces() reads it every step):
+    an edit through a reference kept across steps takes effect."""
+    sc = Scene(gravity=(0.0, 0.0, 0.0), dt=1e-3)
+    sc.add_mass((0.0, 0.0, 0.0), m=2.0)
+    eng = Engine(sc, integrator="euler")
+    fe = eng.f_ext
+    eng.step(10)
+    fe[0] = (4.0, 0.0, 0.0)
+    eng.step(10)
+    # v = (F/m) * 10 dt after the edit
+    assert eng.v[0, 0] == pytest.approx(4.0 / 2.0 * 10 * 1e-3, rel=1e-12)
+    with pytest.raises(ValueError):
+        eng.m[0] = 1.0                      # masses are part of the device state
+
+
+def test_gpe_datum_change_reaches_device_sampling():
+    sc = Scene(gravity=(0.0, -9.81, 0.0), dt=1e-3)
+    sc.add_mass((0.0, 1.0, 0.0), m=2.0, fixed=True)
+    eng = Engine(sc, integrator="euler")
+    r0 = simulate(sc, 0.005, engine=eng)
+    eng.gpe_datum = eng.gpe_datum - 1.0
+    r1 = simulate(sc, 0.005, engine=eng)
+    assert r1.energies[-1, 1] == pytest.approx(r0.energies[-1, 1] + 2.0 * 9.81 * 1.0, rel=1e-12)
+    assert eng.energies()[1] == pytest.approx(r1.energies[-1, 1], rel=1e-12)
