@@ -215,7 +215,9 @@ class Engine:
         self._xp = _Mirror(None)
         self._f = _Mirror(arr.f_ext)
         self._f_sent = None                # f_ext as last uploaded (once handed out, edits are watched)
-        self._step_s = None                # measured seconds per step (sizes command-drain chunks)
+        # seconds per step: sizes the command-drain chunks of long batches;
+        # measured after every step() call, first guessed from the size
+        self._step_s = 2e-6 + 1e-11 * arr.si.shape[0]
 
     # ------------------------------------------------------------ plumbing
 
@@ -523,8 +525,6 @@ class Engine:
     MIN_CHUNK_STEPS = 16
 
     def _chunk_steps(self) -> int:
-        if self._step_s is None:
-            return self.MIN_CHUNK_STEPS
         return max(self.MIN_CHUNK_STEPS, int(self.COMMAND_LATENCY_S / max(self._step_s, 1e-8)))
 
     def _raise_step(self, rc: int, res, what: str) -> None:
@@ -569,8 +569,7 @@ class Engine:
             finally:
                 self._mark_stepped()
             self._raise_step(lib.ss_sync(self._h, C.byref(res)), res, "ss_sync")
-        per_step = (time.perf_counter() - t0) / count
-        self._step_s = per_step if self._step_s is None else 0.5 * (self._step_s + per_step)
+        self._step_s = 0.5 * (self._step_s + (time.perf_counter() - t0) / count)
 
     def step_sampled(self, count: int, sample_every: int, traces=()):
         """Advance ``count`` steps recording, on the device, the samples

@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from .engine import Engine, _lib as _englib  # noqa: F401
 from .lattice import PITCH, voxel_arrays
-from .model import ArrayScene
+from .model import ArrayScene, ContactPlane, scene_arrays
 
 
 def slab_planes(nx: int, nranks: int, rank: int) -> tuple[int, int]:
@@ -57,6 +57,82 @@ class Slab:
     i_lo: int
     i_hi: int
     nx: int
+    global_ids: np.ndarray | None = None   # local -> global mass id (generic slabs; cube slabs: first_global + local)
+
+
+# ------------------------------------------------------- any x-major scene
+
+def plane_starts(scene) -> np.ndarray:
+    """First mass id of every x-plane of a scene whose ids are x-major (the
+    voxel builder numbers masses (i, j, k)-lexicographically,
+    lattice.py:116-119, so every box, beam and multi-material lattice is);
+    ValueError otherwise."""
+    x0 = np.asarray(scene.x, dtype=np.float64)[:, 0]
+    if x0.size and np.any(np.diff(x0) < 0):
+        raise ValueError("mass ids are not ordered by x: the scene cannot be split into x-slabs")
+    return np.concatenate([[0], np.flatnonzero(np.diff(x0) > 0) + 1]).astype(np.int64)
+
+
+def slab_ranges(scene, shards: int) -> list[tuple[int, int]]:
+    """Contiguous mass-id ranges of whole x-planes, balanced by mass count."""
+    starts = plane_starts(scene)
+    n = scene.mass_count
+    if shards > starts.size:
+        raise ValueError(f"{starts.size} x-planes cannot make {shards} slabs")
+    cuts = [0]
+    for r in range(1, shards):
+        want = n * r / shards
+        q = int(np.clip(np.searchsorted(starts, want), cuts[-1] + 1, starts.size - (shards - r)))
+        cuts.append(q)
+    bounds = [int(starts[c]) for c in cuts] + [n]
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def scene_slab(scene, ranges: list[tuple[int, int]], rank: int) -> Slab:
+    """Rank ``rank``'s slab of an x-major scene split at ``ranges``: its
+    owned masses, the neighbours' masses its springs reach (ghosts, fixed
+    locally, overwritten every substep by the owner's push), and every
+    spring touching an owned mass in global id order -- so each owned mass
+    sums its springs in the single-device order and fp64 results are
+    bitwise those of one engine.  Springs may only join adjacent slabs."""
+    a = scene_arrays(scene)
+    lo, hi = ranges[rank]
+    touch = ((a.si >= lo) & (a.si < hi)) | ((a.sj >= lo) & (a.sj < hi))
+    si, sj = a.si[touch], a.sj[touch]
+    partner = np.where((si >= lo) & (si < hi), sj, si)
+    ghosts = np.unique(partner[(partner < lo) | (partner >= hi)])
+    below = ranges[rank - 1][0] if rank > 0 else lo
+    above = ranges[rank + 1][1] if rank + 1 < len(ranges) else hi
+    if ghosts.size and (ghosts[0] < below or ghosts[-1] >= above):
+        raise ValueError("a spring joins non-adjacent slabs: split into fewer shards")
+    gids = np.concatenate([ghosts[ghosts < lo], np.arange(lo, hi, dtype=np.int64), ghosts[ghosts >= hi]])
+    local = np.searchsorted(gids, np.stack([si, sj]))
+    n_lo = int((ghosts < lo).sum())
+    fixed = a.fixed[gids].copy()
+    fixed[:n_lo] = True
+    fixed[n_lo + (hi - lo):] = True
+    groups = {label: scene.groups[label] for label, *_ in a.group_params}
+    sub = ArrayScene(x=a.x[gids], m=a.m[gids], si=local[0], sj=local[1], k=a.k[touch], l0=a.l0[touch],
+                     v=a.v[gids], f_ext=a.f_ext[gids], fixed=fixed, gravity=tuple(a.gravity), dt=a.dt,
+                     damping=a.damping, groups=groups,
+                     group=a.group[touch] if (a.group >= 0).any() else None,
+                     planes=[ContactPlane(tuple(nrm), off, pen, fr) for nrm, off, pen, fr in a.planes],
+                     materials=list(getattr(scene, "materials", [])))
+
+    def facing(other):                     # owned masses that are ghosts of slab `other`
+        if not 0 <= other < len(ranges):
+            return np.zeros(0, dtype=np.int64)
+        o_lo, o_hi = ranges[other]
+        o_touch = ((a.si >= o_lo) & (a.si < o_hi)) | ((a.sj >= o_lo) & (a.sj < o_hi))
+        ends = np.concatenate([a.si[o_touch], a.sj[o_touch]])
+        mine = np.unique(ends[(ends >= lo) & (ends < hi)])
+        return np.searchsorted(gids, mine)
+
+    ids = np.arange(gids.size, dtype=np.int64)
+    return Slab(scene=sub, first_global=int(gids[0]), n_owned=hi - lo, owned=slice(n_lo, n_lo + hi - lo),
+                send_lo=facing(rank - 1), recv_lo=ids[:n_lo], send_hi=facing(rank + 1),
+                recv_hi=ids[n_lo + hi - lo:], springs_global=int(a.si.size), masses_global=int(a.x.shape[0]),
+                i_lo=lo, i_hi=hi, nx=len(ranges), global_ids=gids)
 
 
 def cube_slab(cells: int, i_lo: int, i_hi: int, v_global: np.ndarray | None = None) -> Slab:
@@ -151,6 +227,21 @@ class ShardGroup:
         nx = cells + 1
         self.slabs = [cube_slab(cells, *slab_planes(nx, shards, r), v_global=v_global)
                       for r in range(shards)]
+        self._link(precision, layout, device, transport, integrator)
+
+    @classmethod
+    def from_scene(cls, scene, shards: int, precision: str = "f64", layout: str = "auto", device: int = 0,
+                   transport: str = "copy", integrator: str = "verlet") -> "ShardGroup":
+        """x-slab shards of any x-major scene (a voxel box, beam or
+        multi-material lattice: the builder's ids are (i, j, k)-lexicographic,
+        lattice.py:116-119), stepped in lockstep on one device."""
+        self = cls.__new__(cls)
+        ranges = slab_ranges(scene, shards)
+        self.slabs = [scene_slab(scene, ranges, r) for r in range(shards)]
+        self._link(precision, layout, device, transport, integrator)
+        return self
+
+    def _link(self, precision, layout, device, transport, integrator) -> None:
         self.engines = [Engine(s.scene, integrator=integrator, precision=precision, layout=layout,
                                device=device) for s in self.slabs]
         for e, s in zip(self.engines, self.slabs):

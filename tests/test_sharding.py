@@ -235,3 +235,172 @@ def test_peer_memory_shards_euler(precision):
     else:
         disp = np.abs(one.x - full.x).max()
         assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
+
+
+# ------------------------------------------------ any x-major voxel lattice
+
+def _loaded_beam():
+    """The 40x4x4 cantilever of configs[0]: fixed root layer, gravity, a tip
+    load (f_ext) and damping (reference analysis.py:435-476)."""
+    b = L.beam_lattice(length=4.0, gravity=(0.0, -9.81, 0.0))
+    f = np.zeros((b.mass_count, 3))
+    f[b.x[:, 0] > 3.95, 1] = -0.02
+    b.f_ext = f
+    b.damping = 1e-4
+    return b
+
+
+@pytest.mark.parametrize("shards", [2, 3, 5])
+def test_scene_slabs_of_a_beam_cover_it_once(shards):
+    from paper_2207_09334_b200.sharded import scene_slab, slab_ranges
+    b = _loaded_beam()
+    ranges = slab_ranges(b, shards)
+    assert ranges[0][0] == 0 and ranges[-1][1] == b.mass_count
+    owned_springs = 0
+    for r in range(shards):
+        s = scene_slab(b, ranges, r)
+        g = s.global_ids
+        lo, hi = ranges[r]
+        touch = ((b.si >= lo) & (b.si < hi)) | ((b.sj >= lo) & (b.sj < hi))
+        assert np.array_equal(g[s.scene.si], b.si[touch]) and np.array_equal(g[s.scene.sj], b.sj[touch])
+        assert s.scene.k.tobytes() == b.k[touch].tobytes() and s.scene.l0.tobytes() == b.l0[touch].tobytes()
+        assert s.scene.f_ext[s.owned].tobytes() == b.f_ext[lo:hi].tobytes()
+        assert np.array_equal(s.scene.fixed[s.owned], b.fixed[lo:hi])
+        assert s.scene.fixed[s.recv_lo].all() and s.scene.fixed[s.recv_hi].all()
+        owned_springs += int(((g[s.scene.si] >= lo) & (g[s.scene.si] < hi)).sum())
+        if r + 1 < shards:
+            t = scene_slab(b, ranges, r + 1)
+            assert np.array_equal(g[s.send_hi], t.global_ids[t.recv_lo])
+            assert np.array_equal(t.global_ids[t.send_lo], g[s.recv_hi])
+    assert owned_springs == b.spring_count
+
+
+def test_scene_slabs_reject_non_x_major_and_long_springs():
+    from paper_2207_09334_b200.sharded import scene_slab, slab_ranges
+    c = L.block_scene(4)
+    rev = L.block_scene(4)
+    rev.x = rev.x[::-1].copy()
+    with pytest.raises(ValueError, match="not ordered by x"):
+        slab_ranges(rev, 2)
+    ranges = slab_ranges(c, 3)
+    c.si = np.append(c.si, 0)
+    c.sj = np.append(c.sj, c.mass_count - 1)           # a spring across the whole cube
+    c.k = np.append(c.k, 1.0)
+    c.l0 = np.append(c.l0, 1.0)
+    with pytest.raises(ValueError, match="non-adjacent"):
+        scene_slab(c, ranges, 0)
+
+
+def _gloo_beam_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2207_09334_b200.sharded import scene_slab, slab_ranges
+        b = _loaded_beam()
+        s = scene_slab(b, slab_ranges(b, world), rank)
+        g = s.global_ids
+        got = [None] * world
+        dist.all_gather_object(got, {"send_hi": g[s.send_hi].tolist(), "recv_lo": g[s.recv_lo].tolist(),
+                                     "send_lo": g[s.send_lo].tolist(), "recv_hi": g[s.recv_hi].tolist(),
+                                     "owned": s.n_owned})
+        ok = all(got[r]["send_hi"] == got[r + 1]["recv_lo"] and got[r + 1]["send_lo"] == got[r]["recv_hi"]
+                 for r in range(world - 1))
+        ok &= sum(x["owned"] for x in got) == b.mass_count
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_beam_halo_lists_agree_across_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 2000) + 3
+    procs = [ctx.Process(target=_gloo_beam_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+def _assemble(grp):
+    return (np.concatenate([e.x[s.owned] for e, s in zip(grp.engines, grp.slabs)]),
+            np.concatenate([e.v[s.owned] for e, s in zip(grp.engines, grp.slabs)]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["copy", "p2p"])
+@pytest.mark.parametrize("shards", [2, 3])
+@pytest.mark.parametrize("integrator", ["verlet", "euler"])
+def test_sharded_beam_bitwise(transport, shards, integrator):
+    """configs[0]'s loaded cantilever split into x-slabs (fixed root,
+    gravity, tip load, damping): fp64 bitwise equal to one engine."""
+    from paper_2207_09334_b200.sharded import ShardGroup
+    b = _loaded_beam()
+    one = Engine(b, integrator=integrator, precision="f64")
+    grp = ShardGroup.from_scene(b, shards, precision="f64", transport=transport, integrator=integrator)
+    for n in (13, 50):
+        one.step(n)
+        grp.step(n)
+        x, v = _assemble(grp)
+        assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
+
+
+@pytest.mark.gpu
+def test_sharded_multi_material_cube_bitwise():
+    """configs[1]'s multi-material stretched cube (n=14) in 3 slabs, p2p."""
+    from paper_2207_09334_b200.sharded import ShardGroup
+    c = L.multi_material_cube(14)
+    one = Engine(c, precision="f64")
+    grp = ShardGroup.from_scene(c, 3, precision="f64", transport="p2p")
+    one.step(60)
+    grp.step(60)
+    x, v = _assemble(grp)
+    assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
+
+
+def _ipc_beam_worker(rank, world, port, steps, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2207_09334_b200.sharded import attach_halo, attach_peers, scene_slab, slab_ranges
+        b = _loaded_beam()
+        s = scene_slab(b, slab_ranges(b, world), rank)
+        eng = Engine(s.scene, integrator="verlet", precision="f64", device=0)
+        attach_halo(eng, s)
+        attach_peers(eng, rank, world)
+        eng.step(steps)
+        q.put((rank, s.i_lo, eng.x[s.owned].copy(), eng.v[s.owned].copy(), None))
+        eng.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, -1, None, None, repr(exc)))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_sharded_beam_across_processes():
+    """The loaded beam in two processes (one slab each, CUDA-IPC mapped
+    peer buffers, device-side flags): bitwise the single engine."""
+    steps, world = 40, 2
+    one = Engine(_loaded_beam(), precision="f64")
+    one.step(steps)
+    ref_x, ref_v = one.x.copy(), one.v.copy()
+    one.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 2000) + 11
+    procs = [ctx.Process(target=_ipc_beam_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=500) for _ in procs], key=lambda t: t[1])
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r[4] for r in res if r[4]]
+    assert not errs, errs
+    assert np.concatenate([r[2] for r in res]).tobytes() == ref_x.tobytes()
+    assert np.concatenate([r[3] for r in res]).tobytes() == ref_v.tobytes()
