@@ -94,6 +94,13 @@ struct ss_engine {
     size_t scale_cap = 0;
     unsigned long long *d_degenerate = nullptr;
     void *pinned[3] = {nullptr, nullptr, nullptr};   // page-locked staging for state transfers
+    // fp64 state transfers in the caller's layout ((N,3) f64, 24 B per mass):
+    // two pinned chunk buffers (host memcpy into one overlaps the DMA out of
+    // the other), a device staging array, and the +-m word of every slot
+    void *chunk_buf[2] = {nullptr, nullptr};
+    cudaEvent_t chunk_done[2] = {nullptr, nullptr};
+    double *d_raw = nullptr;
+    double *d_w = nullptr;
     size_t pinned_bytes[3] = {0, 0, 0};
     cudaEvent_t staged = nullptr;              // recorded after asynchronous uploads from `pinned`
     cudaEvent_t chunk_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // chunked downloads
@@ -188,6 +195,10 @@ struct ss_engine {
         for (cudaEvent_t e : spare_events) cudaEventDestroy(e);
         for (void *b : pinned)
             if (b) cudaFreeHost(b);
+        for (void *b : chunk_buf)
+            if (b) cudaFreeHost(b);
+        for (cudaEvent_t e : chunk_done)
+            if (e) cudaEventDestroy(e);
         if (staged) cudaEventDestroy(staged);
         for (cudaEvent_t e : chunk_ev)
             if (e) cudaEventDestroy(e);
@@ -1353,12 +1364,146 @@ int staging(ss_engine *h, T4 **out, int which = 0) {
     return SS_OK;
 }
 
+// ---------------------------------------------- fp64 caller-layout transfers
+// The caller's (N,3) f64 arrays cross the bus as they are (24 B per mass,
+// not the 32 B device vectors) and are permuted into / out of the device
+// order by these kernels, so the host does a plain parallel memcpy into
+// pinned memory instead of a permuting gather.
+
+__global__ void raw_to_device_kernel(const double *__restrict__ raw, const int *__restrict__ orig_of, int64_t nd,
+                                     const double *__restrict__ w, double4 *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int64_t s = orig_of ? orig_of[i] : i;
+    double4 o = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (s >= 0) {
+        o.x = raw[3 * s];
+        o.y = raw[3 * s + 1];
+        o.z = raw[3 * s + 2];
+        o.w = w ? w[i] : 0.0;                             // +-m for positions, 0 for velocities
+    }
+    out[i] = o;
+}
+
+__global__ void device_to_raw_kernel(const double4 *__restrict__ in, const int *__restrict__ orig_of, int64_t nd,
+                                     double *__restrict__ raw) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int64_t s = orig_of ? orig_of[i] : i;
+    if (s < 0) return;
+    const double4 o = in[i];
+    raw[3 * s] = o.x;
+    raw[3 * s + 1] = o.y;
+    raw[3 * s + 2] = o.z;
+}
+
+constexpr size_t kChunkBytes = 4u << 20;
+
+int chunk_setup(ss_engine *h) {
+    if (h->chunk_buf[0]) return SS_OK;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaHostAlloc(&h->chunk_buf[b], kChunkBytes, cudaHostAllocDefault));
+        CK(cudaEventCreateWithFlags(&h->chunk_done[b], cudaEventDisableTiming));
+    }
+    if (!h->d_raw) {
+        int rc = h->alloc(&h->d_raw, (size_t)h->N * 3 * sizeof(double));
+        if (rc) return rc;
+    }
+    if (!h->d_w) {
+        std::vector<double> w((size_t)h->ND, 0.0);
+        for (int64_t i = 0; i < h->ND; ++i) {
+            const int64_t s = h->src_of(i);
+            if (s >= 0) w[i] = h->fixed[s] ? -h->m[s] : h->m[s];
+        }
+        int rc = up_vec(h, reinterpret_cast<void **>(&h->d_w), w);
+        if (rc) return rc;
+    }
+    return SS_OK;
+}
+
+void par_copy(void *dst, const void *src, size_t bytes) {
+    constexpr size_t kPiece = 256u << 10;
+    const int64_t n = (int64_t)((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < n; ++k) {
+        const size_t o = (size_t)k * kPiece;
+        std::memcpy(static_cast<char *>(dst) + o, static_cast<const char *>(src) + o, std::min(kPiece, bytes - o));
+    }
+}
+
+// pageable host -> device: chunk k is copied into pinned buffer k%2 while
+// the DMA of chunk k-1 runs
+int h2d_chunked(ss_engine *h, void *dst, const void *src, size_t bytes) {
+    for (size_t o = 0, k = 0; o < bytes; o += kChunkBytes, ++k) {
+        const int b = (int)(k & 1);
+        const size_t n = std::min(kChunkBytes, bytes - o);
+        CK(cudaEventSynchronize(h->chunk_done[b]));               // its previous DMA (any call) has finished
+        par_copy(h->chunk_buf[b], static_cast<const char *>(src) + o, n);
+        CK(cudaMemcpyAsync(static_cast<char *>(dst) + o, h->chunk_buf[b], n, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaEventRecord(h->chunk_done[b], h->stream));
+    }
+    return SS_OK;
+}
+
+// device -> pageable host: the DMA of chunk k+1 runs while chunk k is
+// copied out of its pinned buffer
+int d2h_chunked(ss_engine *h, void *dst, const void *src, size_t bytes) {
+    const size_t nk = (bytes + kChunkBytes - 1) / kChunkBytes;
+    auto issue = [&](size_t k) -> int {
+        const size_t o = k * kChunkBytes, n = std::min(kChunkBytes, bytes - o);
+        CK(cudaMemcpyAsync(h->chunk_buf[k & 1], static_cast<const char *>(src) + o, n, cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaEventRecord(h->chunk_done[k & 1], h->stream));
+        return SS_OK;
+    };
+    int rc;
+    if (nk && (rc = issue(0))) return rc;
+    for (size_t k = 0; k < nk; ++k) {
+        if (k + 1 < nk && (rc = issue(k + 1))) return rc;
+        CK(cudaEventSynchronize(h->chunk_done[k & 1]));
+        const size_t o = k * kChunkBytes;
+        par_copy(static_cast<char *>(dst) + o, h->chunk_buf[k & 1], std::min(kChunkBytes, bytes - o));
+    }
+    return SS_OK;
+}
+
+int raw_upload(ss_engine *h, const double *src, void *dst_vec, bool position) {
+    const size_t bytes = (size_t)h->N * 3 * sizeof(double);
+    int rc = h2d_chunked(h, h->d_raw, src, bytes);
+    if (rc) return rc;
+    const unsigned grid = (unsigned)((h->ND + 255) / 256);
+    raw_to_device_kernel<<<grid, 256, 0, h->stream>>>(h->d_raw, h->d_orig_of, h->ND, position ? h->d_w : nullptr,
+                                                      reinterpret_cast<double4 *>(dst_vec));
+    CK(cudaGetLastError());
+    return SS_OK;
+}
+
+int raw_download(ss_engine *h, const void *src_vec, double *dst) {
+    const unsigned grid = (unsigned)((h->ND + 255) / 256);
+    device_to_raw_kernel<<<grid, 256, 0, h->stream>>>(reinterpret_cast<const double4 *>(src_vec), h->d_orig_of,
+                                                      h->ND, h->d_raw);
+    CK(cudaGetLastError());
+    return d2h_chunked(h, dst, h->d_raw, (size_t)h->N * 3 * sizeof(double));
+}
+
 template <bool F32>
 int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
+    int rc;
+    if constexpr (!F32) {                         // caller layout over the bus, permuted on the device
+        if ((rc = chunk_setup(h))) return rc;
+        if (h->staged_pending) {
+            CK(cudaEventSynchronize(h->staged));
+            h->staged_pending = false;
+        }
+        if (x && (rc = raw_download(h, h->X[h->cur], x))) return rc;
+        if (v && (rc = raw_download(h, h->V, v))) return rc;
+        if (x_prev && h->has_prev && (rc = raw_download(h, h->X[h->cur ^ 1], x_prev))) return rc;
+        return SS_OK;
+    }
     T4 *tmp;
-    int rc = staging<T4>(h, &tmp);
+    rc = staging<T4>(h, &tmp);
     if (rc) return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);
     if (x) {
@@ -1412,11 +1557,21 @@ int set_state_impl(ss_engine *h, const double *x, const double *v, const double 
         if (r0) return r0;
         x_prev = keep_prev.data();
     }
+    int rc;
+    if constexpr (!F32) {                         // caller layout over the bus, permuted on the device
+        if ((rc = chunk_setup(h))) return rc;
+        if (x && (rc = raw_upload(h, x, h->X[h->cur], true))) return rc;
+        if (v && (rc = raw_upload(h, v, h->V, false))) return rc;
+        if (x_prev) {
+            if ((rc = raw_upload(h, x_prev, h->X[h->cur ^ 1], true))) return rc;
+            h->has_prev = true;
+        }
+        return SS_OK;
+    }
     // each vector is packed into its own staging buffer and its upload is
     // queued at once, so packing the next vector overlaps the DMA of the
     // previous one; the stream orders the uploads before the next step
     T4 *bx, *bv, *tmp;
-    int rc;
     if ((rc = staging<T4>(h, &bx, 0)) || (rc = staging<T4>(h, &bv, 1)) || (rc = staging<T4>(h, &tmp, 2)))
         return rc;
     const size_t bytes = (size_t)h->ND * sizeof(T4);

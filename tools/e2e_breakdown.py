@@ -7,7 +7,7 @@ from paper_2207_09334_b200 import _lib
 import ctypes as C
 
 sc = L.excite(L.block_scene(int(os.environ.get("CELLS", "91"))), seed=11)
-eng = Engine(sc, integrator="verlet", precision="f32")
+eng = Engine(sc, integrator="verlet", precision=os.environ.get("PREC", "f64"))
 eng.step(100)
 x, v, xp = eng.x.copy(), eng.v.copy(), eng.x_prev.copy()
 lib = _lib.lib()
