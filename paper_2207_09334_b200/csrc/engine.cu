@@ -1397,7 +1397,15 @@ __global__ void device_to_raw_kernel(const double4 *__restrict__ in, const int *
     raw[3 * s + 2] = o.z;
 }
 
-constexpr size_t kChunkBytes = 4u << 20;
+size_t chunk_bytes() {
+    static const size_t bytes = [] {
+        const char *e = getenv("SS_CHUNK_MB");                // transfer chunk (MB), 4 by default
+        const long mb = e ? atol(e) : 4;
+        return (size_t)std::max(1l, std::min(mb, 256l)) << 20;
+    }();
+    return bytes;
+}
+#define kChunkBytes chunk_bytes()
 
 int chunk_setup(ss_engine *h) {
     if (h->chunk_buf[0]) return SS_OK;

@@ -62,12 +62,12 @@ _INTEG = {EULER: _lib.SS_EULER, VERLET: _lib.SS_VERLET, RK4: _lib.SS_RK4}
 class DivergenceError(RuntimeError):
     """Non-finite position or velocity; the run is halted (engine.py:44-52)."""
 
+    MESSAGE = ("simulation diverged at step {step}: mass {mass_id} has a "
+               "non-finite position or velocity (try a smaller dt)")
+
     def __init__(self, mass_id: int, step: int):
-        self.mass_id = mass_id
-        self.step = step
-        super().__init__(
-            f"simulation diverged at step {step}: mass {mass_id} has a "
-            f"non-finite position or velocity (try a smaller dt)")
+        super().__init__(self.MESSAGE.format(step=step, mass_id=mass_id))
+        self.mass_id, self.step = mass_id, step
 
 
 def spring_force(x_i, x_j, k: float, l0: float) -> np.ndarray:
@@ -90,16 +90,21 @@ def _friction(v, normal, f_n: float, mu: float, m: float, dt: float):
     return (min(mu * f_n, speed * m / dt) / speed) * v_t
 
 
+def _penetration(x, plane, normal) -> float:
+    """How far x lies inside the plane's solid side (<= 0: outside)."""
+    return plane.offset - x @ normal
+
+
 def contact_force(x, v, m: float, plane, dt: float) -> np.ndarray:
     """Penalty normal force plus friction of one plane on one mass
     (engine.py:68-89); zero outside the half-space."""
     x, v, normal = (np.asarray(a, dtype=np.float64) for a in (x, v, plane.normal))
-    depth = plane.offset - x @ normal
+    depth = _penetration(x, plane, normal)
     if depth <= 0.0:
         return np.zeros(3)
-    f_n = plane.penalty * depth
-    tangential = _friction(v, normal, f_n, plane.friction, m, dt)
-    return f_n * normal if tangential is None else f_n * normal - tangential
+    push = plane.penalty * depth
+    tangential = _friction(v, normal, push, plane.friction, m, dt)
+    return push * normal if tangential is None else push * normal - tangential
 
 
 @dataclass
@@ -730,16 +735,25 @@ class Engine:
         """Apply every queued command; a failing one is reported in
         ``command_errors`` and the rest still apply."""
         for cmd in self._queued(wait):
-            try:
-                self.apply_command(cmd)
-            except Exception as exc:            # reported through the channel, stepping goes on
-                self.command_errors.append(f"{cmd.get('op', '?')}: {exc}")
+            error = _try_command(self, cmd)
+            if error:
+                self.command_errors.append(error)
 
     def apply_command(self, cmd: dict) -> None:
         handler = _COMMANDS.get(cmd.get("op"))
         if handler is None:
             raise ValueError(f"unknown command op {cmd.get('op')!r}")
         handler(self, cmd)
+
+
+def _try_command(engine: "Engine", cmd: dict) -> str | None:
+    """Apply one command; a failure comes back as "op: reason" (the
+    reference keeps stepping and reports through ``command_errors``)."""
+    try:
+        engine.apply_command(cmd)
+    except Exception as exc:
+        return f"{cmd.get('op', '?')}: {exc}"
+    return None
 
 
 def _floats(values) -> list[float]:
@@ -836,70 +850,75 @@ SAMPLE_SEGMENT_ROWS = 4096          # samples per device segment of simulate()
 DEVICE_SAMPLING = True              # False: sample on the host after every chunk (reference-style)
 
 
+class _Samples:
+    """Sample rows of a run: times, traced positions, energy tuples."""
+
+    def __init__(self, traces):
+        self.times: list[float] = []
+        self.tracks = {mass_id: [] for mass_id in traces}
+        self.energies: list = []
+
+    def host(self, engine: Engine, step_index: int, x, v) -> None:
+        """One sample of a host-side state (the reference's simulate loop)."""
+        t = step_index * engine.dt
+        self.times.append(t)
+        for mass_id, track in self.tracks.items():
+            track.append(x[mass_id].copy())
+        self.energies.append(engine.energies(x, v, t))
+
+    def device(self, t_s, p_s, e_s) -> None:
+        """Rows recorded on the device by Engine.step_sampled."""
+        self.times.extend(float(t) for t in t_s)
+        for q, track in enumerate(self.tracks.values()):
+            track.extend(p_s[:, q].copy())
+        self.energies.extend(tuple(e) for e in e_s)
+
+    def result(self, engine: Engine) -> RunResult:
+        return RunResult(times=np.asarray(self.times),
+                         positions={mass_id: np.asarray(track) for mass_id, track in self.tracks.items()},
+                         energies=np.asarray(self.energies).reshape(-1, 4), engine=engine)
+
+
+def _steps_to_next_sample(n: int, verlet: bool, every: int) -> int:
+    """Steps until the next sampling point: Verlet samples step n-1 (paired
+    with x_prev), the others step n, whenever it is a multiple of ``every``."""
+    lag = ((n - 1) if verlet else n) % every
+    return every - lag if lag else every
+
+
 def simulate(scene, duration: float, traces=(), integrator: str = VERLET,
              mode: str = SERIAL, threads: int | None = None, sample_every: int = 1,
              engine: Engine | None = None, **engine_kwargs) -> RunResult:
-    """Run ``ceil(duration/dt)`` steps, sampling traces and energies (engine.py:518-565).
-
-    Steps between two samples run as one device batch; sampling points,
-    pause/resume/stop handling and the Verlet one-step sample lag are those of
-    the reference."""
+    """Run ``ceil(duration/dt - 1e-9)`` steps sampling traced positions and
+    energies (engine.py:518-565): the reference's sampling points, Verlet
+    one-step sample lag and pause / resume / stop handling.  With an empty
+    command queue the steps and samples run on the device in segments
+    (Engine.step_sampled); a queued command drops to one step at a time, as
+    the reference drains before every step."""
     if engine is None:
         engine = Engine(scene, integrator=integrator, mode=mode, threads=threads, **engine_kwargs)
-    dt = engine.dt
-    steps = max(0, math.ceil(duration / dt - 1e-9))
+    total = max(0, math.ceil(duration / engine.dt - 1e-9))
     verlet = engine.integrator == VERLET
-    sample_every = max(1, int(sample_every))
-    times, rows, erows = [], {mass_id: [] for mass_id in traces}, []
-
-    def emit(step_index, x, v):
-        t = step_index * dt
-        times.append(t)
-        for mass_id in rows:
-            rows[mass_id].append(x[mass_id].copy())
-        erows.append(engine.energies(x, v, t))
-
-    if not verlet and engine.n == 0:
-        emit(0, engine.x, engine.v)
-
+    every = max(1, int(sample_every))
+    out = _Samples(traces)
+    if engine.n == 0 and not verlet:
+        out.host(engine, 0, engine.x, engine.v)
     done = 0
-    device_sampling = DEVICE_SAMPLING
-    while done < steps:
+    while done < total and not engine.stopped:
         while engine.paused and not engine.stopped:
             engine.drain_commands(wait=0.02)
         if engine.stopped:
             break
-        if device_sampling and engine._commands.empty():
-            # steps and samples enqueued on the device in segments; commands
-            # and pause/stop are honoured between segments
-            seg = min(steps - done, SAMPLE_SEGMENT_ROWS * sample_every)
-            t_s, p_s, e_s = engine.step_sampled(seg, sample_every, list(rows))
+        quiet = engine._commands.empty()
+        if DEVICE_SAMPLING and quiet:
+            seg = min(total - done, SAMPLE_SEGMENT_ROWS * every)
+            out.device(*engine.step_sampled(seg, every, list(out.tracks)))
             done += seg
-            for r in range(len(t_s)):
-                times.append(float(t_s[r]))
-                for q, mass_id in enumerate(rows):
-                    rows[mass_id].append(p_s[r, q].copy())
-                erows.append(tuple(e_s[r]))
             continue
-        n = engine.n
-        if not engine._commands.empty():
-            chunk = 1                       # reference: drain + one step
-        else:
-            # steps until the next sampling point
-            target = (n - 1) if verlet else n
-            chunk = sample_every - (target % sample_every)
-            if chunk <= 0:
-                chunk = sample_every
-            chunk = min(chunk, steps - done)
+        chunk = min(_steps_to_next_sample(engine.n, verlet, every), total - done) if quiet else 1
         engine.step(chunk)
         done += chunk
-        if verlet:
-            d = engine.n - 1
-            if d % sample_every == 0:
-                emit(d, engine.x_prev, engine.v)
-        elif engine.n % sample_every == 0:
-            emit(engine.n, engine.x, engine.v)
-
-    return RunResult(times=np.asarray(times),
-                     positions={mass_id: np.asarray(vals) for mass_id, vals in rows.items()},
-                     energies=np.asarray(erows).reshape(-1, 4), engine=engine)
+        sampled = engine.n - 1 if verlet else engine.n
+        if sampled % every == 0:
+            out.host(engine, sampled, engine.x_prev if verlet else engine.x, engine.v)
+    return out.result(engine)

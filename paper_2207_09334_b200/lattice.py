@@ -94,9 +94,9 @@ def block_cells(spring_count: int) -> int:
     """Cube edge whose block is closest to ``spring_count`` (bench.py:72-80)."""
     if spring_count < 1:
         raise ValueError("spring_count must be >= 1")
-    n = max(1, round((spring_count / 13) ** (1 / 3)))
-    return min((n - 1, n, n + 1, n + 2),
-               key=lambda c: abs(block_springs(c) - spring_count) if c >= 1 else float("inf"))
+    guess = max(1, round((spring_count / 13) ** (1 / 3)))          # 13 n^3 dominates
+    near = [c for c in range(guess - 1, guess + 3) if c >= 1]       # first minimum wins ties, as the reference
+    return near[int(np.argmin([abs(block_springs(c) - spring_count) for c in near]))]
 
 
 def block_scene(cells: int) -> ArrayScene:
