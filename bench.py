@@ -409,9 +409,13 @@ def engine_leg(scene, precision: str, args, clk, workload: str, e2e_steps: int, 
     e2e = None
     if e2e_steps:
         wall = time_e2e(eng, e2e_steps, sub)
-        vec = 16 if precision == "f32" else 32
+        # the caller's (N, 3) f64 arrays: x, v, x_prev in, x out.  fp64 moves
+        # exactly these over the bus (permuted on the device); fp32 packs them
+        # on the host into 16-byte device slots first
+        vec = 3 * 8
         e2e = {"value": S * sub * e2e_steps / wall, "unit": UNIT, "steps": e2e_steps,
-               "h2d_bytes_per_step": 3 * N * vec, "d2h_bytes_per_step": N * vec}
+               "h2d_bytes_per_step": 3 * N * vec, "d2h_bytes_per_step": N * vec,
+               "bus_bytes_per_mass_vector": 24 if precision == "f64" else 16}
     eng.close()
     return {"value": value, "ms_per_step": ms / args.steps, "launches": launches, "roofline": roof,
             "e2e": e2e, "dtype": precision, "label": label,

@@ -109,7 +109,10 @@ struct ss_engine {
     int *d_ssi = nullptr, *d_ssj = nullptr, *d_sgrp = nullptr;
     double *d_sk = nullptr, *d_sl0 = nullptr, *d_smass = nullptr, *d_sx0 = nullptr;
     int64_t energy_springs = -1;               // -1: ss_energy_setup not called
-    DevBuf d_sids, d_srows, d_serows, d_sscale, d_spartial;
+    DevBuf d_sids, d_srows, d_serows, d_sscale;
+    int *d_sdev_of = nullptr;                  // caller mass id -> device slot
+    PwPlanDev pw_springs{}, pw_masses{};       // numpy pairwise-sum plans (sampling.cuh)
+    double *d_pwv[3] = {nullptr, nullptr, nullptr};   // their node values: EPE; GPE, KE
     long long *d_div_step = nullptr;
     int *d_div_mass = nullptr;
     int *d_orig_of = nullptr;
@@ -590,6 +593,21 @@ void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
     else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
 }
 
+// RK4 stage `stage` (1-4) of a fp64 compact-tile engine on tile_f64_kernel
+// (tile_f64.cuh f64_rk4_epilogue), chained by programmatic dependent launch.
+template <bool GROUPS>
+void launch_rk4_f64(ss_engine *h, const Params<double> &p, int grid, int stage) {
+    void (*k)(Params<double>) = nullptr;
+    switch (stage) {
+        case 1: k = tile_f64_kernel<2, GROUPS, 2, 4>; break;
+        case 2: k = tile_f64_kernel<3, GROUPS, 2, 4>; break;
+        case 3: k = tile_f64_kernel<4, GROUPS, 2, 4>; break;
+        default: k = tile_f64_kernel<5, GROUPS, 2, 4>; break;
+    }
+    if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
+    else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
@@ -606,7 +624,9 @@ int launch_steps(ss_engine *h, int64_t count) {
     const size_t smem = LAYOUT >= 3 ? h->smem_bytes : 0;
     Params<T> p = base_params<T>(h);
     const T *scale = reinterpret_cast<const T *>(h->scale);
-    if (h->res_image && h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2) {
+    if (h->res_image && h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 1) {
+        // (every batch size, one step included: fp32 results must not depend on
+        // how the steps are batched, and the resident kernel sums in its own order)
         // small scene: one CTA keeps the state on chip for the whole batch (resident.cuh)
         ResidentArgs a{};
         a.image = reinterpret_cast<const unsigned char *>(h->res_image);
@@ -653,7 +673,7 @@ int launch_steps(ss_engine *h, int64_t count) {
         if (h->integrator == SS_VERLET) h->has_prev = true;
         return SS_OK;
     }
-    if (h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 2 && h->persist_max_grid >= grid) {
+    if (h->integrator != SS_RK4 && !h->nccl && !h->p2p_on && count >= 1 && h->persist_max_grid >= grid) {
         // small scene: one cooperative launch steps the whole batch
         // (kernels.cuh persist_step_kernel / tile_f32.cuh persist_lean_kernel)
         PersistArgs<T> a{};
@@ -754,6 +774,13 @@ int launch_steps(ss_engine *h, int64_t count) {
                 if constexpr (F32 && LAYOUT >= 3) {
                     if (h->lean_smem) {                      // fp32 compact tiles: the lean kernel
                         launch_rk4_lean<LAYOUT == 3>(h, p, grid, stage);
+                        return;
+                    }
+                }
+                if constexpr (!F32 && LAYOUT >= 3) {
+                    if (h->f64_smem) {                       // fp64 compact tiles: tile_f64_kernel
+                        if (G) launch_rk4_f64<true>(h, p, grid, stage);
+                        else launch_rk4_f64<false>(h, p, grid, stage);
                         return;
                     }
                 }
@@ -1207,7 +1234,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             const char *kenv = getenv("SS_F64_KERNEL");
             const std::string kname = kenv ? kenv : "tile";
             const size_t f64s = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * 24;
-            if (kname != "step" && d->integrator != SS_RK4 && L.compact && !L.has_self &&
+            if (kname != "step" && L.compact && !L.has_self &&
                 (int64_t)f64s <= dev_max) {
                 h->f64_smem = f64s;
                 if (const char *e = getenv("SS_F64_VARIANT")) h->f64_variant = atoi(e);
@@ -1218,7 +1245,11 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_f64_kernel<0, false, 2, 3>, tile_f64_kernel<1, false, 2, 3>,
                                  tile_f64_kernel<0, true, 2, 3>, tile_f64_kernel<1, true, 2, 3>,
                                  tile_f64_kernel<0, false, 3, 3>, tile_f64_kernel<1, false, 3, 3>,
-                                 tile_f64_kernel<0, true, 3, 3>, tile_f64_kernel<1, true, 3, 3>})
+                                 tile_f64_kernel<0, true, 3, 3>, tile_f64_kernel<1, true, 3, 3>,
+                                 tile_f64_kernel<2, false, 2, 4>, tile_f64_kernel<3, false, 2, 4>,
+                                 tile_f64_kernel<4, false, 2, 4>, tile_f64_kernel<5, false, 2, 4>,
+                                 tile_f64_kernel<2, true, 2, 4>, tile_f64_kernel<3, true, 2, 4>,
+                                 tile_f64_kernel<4, true, 2, 4>, tile_f64_kernel<5, true, 2, 4>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max));
             }
         }
@@ -1846,9 +1877,77 @@ int ensure(ss_engine *h, DevBuf &b, size_t bytes) {
     return SS_OK;
 }
 
+// numpy's pairwise-summation recursion over n elements (sampling.cuh):
+// leaves in order, internal nodes grouped by height, uploaded once.
+int build_pw_plan(ss_engine *h, long long n, PwPlanDev &pl, double **vals, int nvals) {
+    pl = PwPlanDev{};
+    if (n <= 0) return SS_OK;
+    std::vector<long long> off;
+    std::vector<int> len;
+    struct Inner { int l, r, height; };
+    std::vector<Inner> inner;                    // child ids: >= 0 leaf, < 0 inner -(k + 1)
+    struct Rec {
+        std::vector<long long> &off; std::vector<int> &len; std::vector<Inner> &inner;
+        int go(long long lo, long long m, int &height) {
+            if (m <= 128) {
+                off.push_back(lo);
+                len.push_back((int)m);
+                height = 0;
+                return (int)off.size() - 1;
+            }
+            long long m2 = m / 2;
+            m2 -= m2 % 8;
+            int hl, hr;
+            const int l = go(lo, m2, hl);
+            const int r = go(lo + m2, m - m2, hr);
+            height = std::max(hl, hr) + 1;
+            inner.push_back({l, r, height});
+            return -(int)inner.size();
+        }
+    } rec{off, len, inner};
+    int top_h = 0;
+    const int top = rec.go(0, n, top_h);
+    const int L = (int)off.size();
+    auto id = [&](int t) { return t >= 0 ? t : L + (-t - 1); };
+    std::vector<int> order(inner.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return inner[a].height < inner[b].height; });
+    std::vector<int4> nodes;
+    std::vector<int> level_start;
+    int cur_h = 0;
+    for (int k : order) {
+        while (cur_h < inner[k].height) {
+            level_start.push_back((int)nodes.size());
+            ++cur_h;
+        }
+        nodes.push_back(make_int4(id(inner[k].l), id(inner[k].r), L + k, 0));
+    }
+    level_start.push_back((int)nodes.size());
+    int rc;
+    void *p;
+    if ((rc = up_vec(h, &p, off))) return rc;
+    pl.leaf_off = reinterpret_cast<const long long *>(p);
+    if ((rc = up_vec(h, &p, len))) return rc;
+    pl.leaf_len = reinterpret_cast<const int *>(p);
+    if (!nodes.empty()) {
+        if ((rc = up_vec(h, &p, nodes))) return rc;
+        pl.nodes = reinterpret_cast<const int4 *>(p);
+        if ((rc = up_vec(h, &p, level_start))) return rc;
+        pl.level_start = reinterpret_cast<const int *>(p);
+    }
+    pl.n_leaves = L;
+    pl.n_levels = nodes.empty() ? 0 : (int)level_start.size() - 1;
+    pl.root = id(top);
+    for (int v = 0; v < nvals; ++v)
+        if ((rc = h->alloc(&vals[v], (size_t)(L + inner.size()) * sizeof(double)))) return rc;
+    return SS_OK;
+}
+
 // Launch the sample kernels for one row at the current device state
-// (Verlet: x_prev buffer, others: x), scales row `scale_row`.
-int launch_sample(ss_engine *h, int64_t row, int n_ids, int use_prev, int grid) {
+// (Verlet: x_prev buffer, others: x), scales row `scale_row`: traced
+// positions, then EPE over the springs and GPE/KE over the masses, each a
+// numpy pairwise sum in caller order (sampling.cuh).
+int launch_sample(ss_engine *h, int64_t row, int n_ids, int use_prev) {
     SampleArgs a{};
     a.X = h->X[use_prev && !h->U ? (h->cur ^ 1) : h->cur];
     a.Usub = use_prev && h->U ? h->U : nullptr;          // fp32 Verlet: x_prev = x - u
@@ -1864,20 +1963,46 @@ int launch_sample(ss_engine *h, int64_t row, int n_ids, int use_prev, int grid) 
     a.sgrp = h->groups.empty() ? nullptr : h->d_sgrp;
     a.scale = reinterpret_cast<const double *>(h->d_sscale.p) + (size_t)row * std::max<size_t>(h->groups.size(), 1);
     a.n_springs = h->energy_springs;
-    const double g2 = h->gravity[0] * h->gravity[0] + h->gravity[1] * h->gravity[1] + h->gravity[2] * h->gravity[2];
-    a.g_mag = std::sqrt(g2);
-    for (int c = 0; c < 3; ++c) a.up[c] = a.g_mag > 0.0 ? -h->gravity[c] / a.g_mag : 0.0;
+    a.n_masses = h->N;
+    a.dev_of = h->d_sdev_of;
+    // |g| = np.linalg.norm(gravity): BLAS ddot, fma(g2, g2, fma(g1, g1, g0 g0)) (as lattice.cpp's l0)
+    const double *g = h->gravity;
+    a.g_mag = std::sqrt(std::fma(g[2], g[2], std::fma(g[1], g[1], g[0] * g[0])));
+    for (int c = 0; c < 3; ++c) a.up[c] = a.g_mag > 0.0 ? -g[c] / a.g_mag : 0.0;
     a.datum = h->gpe_datum;
     a.ids = reinterpret_cast<const int *>(h->d_sids.p);
     a.n_ids = n_ids;
     a.pos_row = reinterpret_cast<double *>(h->d_srows.p) + (size_t)row * n_ids * 3;
-    a.partial = reinterpret_cast<double *>(h->d_spartial.p);
     a.energy_row = reinterpret_cast<double *>(h->d_serows.p) + (size_t)row * 4;
-    if (h->precision == SS_F32) sample_partial_kernel<true><<<grid, kSampleThreads, 0, h->stream>>>(a);
-    else sample_partial_kernel<false><<<grid, kSampleThreads, 0, h->stream>>>(a);
-    sample_final_kernel<<<1, kSampleThreads, 0, h->stream>>>(a.partial, grid, a.energy_row);
+    const bool f32 = h->precision == SS_F32;
+    int launched = 0;
+    if (n_ids) {
+        const int gi = (n_ids + kSampleThreads - 1) / kSampleThreads;
+        if (f32) sample_ids_kernel<true><<<gi, kSampleThreads, 0, h->stream>>>(a);
+        else sample_ids_kernel<false><<<gi, kSampleThreads, 0, h->stream>>>(a);
+        ++launched;
+    }
+    auto leaves = [&](const PwPlanDev &pl, auto kernel, double *v0, double *v1) {
+        const unsigned gl = (unsigned)((8LL * pl.n_leaves + kSampleThreads - 1) / kSampleThreads);
+        kernel<<<gl, kSampleThreads, 0, h->stream>>>(a, pl, v0, v1);
+        ++launched;
+        if (pl.n_levels) {
+            pw_combine_kernel<<<1, 1024, 0, h->stream>>>(pl, v0, v1);
+            ++launched;
+        }
+    };
+    const bool springs = h->energy_springs > 0;
+    if (springs) {
+        if (f32) leaves(h->pw_springs, pw_leaf_kernel<true, true>, h->d_pwv[0], nullptr);
+        else leaves(h->pw_springs, pw_leaf_kernel<false, true>, h->d_pwv[0], nullptr);
+    }
+    if (f32) leaves(h->pw_masses, pw_leaf_kernel<true, false>, h->d_pwv[1], h->d_pwv[2]);
+    else leaves(h->pw_masses, pw_leaf_kernel<false, false>, h->d_pwv[1], h->d_pwv[2]);
+    pw_final_kernel<<<1, 1, 0, h->stream>>>(h->d_pwv[0], h->pw_springs.root, h->d_pwv[1], h->d_pwv[2],
+                                            h->pw_masses.root, springs, a.g_mag, a.energy_row);
+    ++launched;
     CK(cudaGetLastError());
-    h->launches += 2;
+    h->launches += launched;
     return SS_OK;
 }
 
@@ -1910,6 +2035,14 @@ int ss_energy_setup(ss_engine *h, int64_t n_springs, const int64_t *si, const in
             if ((rc = h->alloc(&h->d_sx0, h->x0.size() * sizeof(double)))) return rc;
             if ((rc = upload(h, h->d_sx0, h->x0.data(), h->x0.size() * sizeof(double)))) return rc;
         }
+        std::vector<int> dv((size_t)h->N);
+        for (int64_t c = 0; c < h->N; ++c) dv[c] = (int)dev_of(h, c);
+        void *p;
+        if ((rc = up_vec(h, &p, dv))) return rc;
+        h->d_sdev_of = reinterpret_cast<int *>(p);
+        if ((rc = build_pw_plan(h, n_springs, h->pw_springs, h->d_pwv, 1)) ||
+            (rc = build_pw_plan(h, h->N, h->pw_masses, h->d_pwv + 1, 2)))
+            return rc;
     } else if (n_springs != h->energy_springs) {
         return ss::fail(SS_EINVAL, "ss_energy_setup: spring count changed");
     }
@@ -1976,14 +2109,10 @@ int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every, const int
                 ++r;
             }
     }
-    int sms = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    const int grid = std::max(1, std::min(4 * sms, (int)((std::max<int64_t>(h->energy_springs, h->ND) + 255) / 256)));
     if ((rc = ensure(h, h->d_sids, dids.size() * sizeof(int))) ||
         (rc = ensure(h, h->d_srows, (size_t)std::max<int64_t>(rows, 1) * std::max<int64_t>(n_ids, 1) * 3 * sizeof(double))) ||
         (rc = ensure(h, h->d_serows, (size_t)std::max<int64_t>(rows, 1) * 4 * sizeof(double))) ||
-        (rc = ensure(h, h->d_sscale, sc.size() * sizeof(double))) ||
-        (rc = ensure(h, h->d_spartial, (size_t)grid * 3 * sizeof(double))))
+        (rc = ensure(h, h->d_sscale, sc.size() * sizeof(double))))
         return rc;
     if ((rc = upload(h, h->d_sids.p, dids.data(), dids.size() * sizeof(int))) ||
         (rc = upload(h, h->d_sscale.p, sc.data(), sc.size() * sizeof(double))))
@@ -2000,7 +2129,7 @@ int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every, const int
         total += chunks[c];
         if (sample_d[c] >= 0) {
             if (times_out) times_out[r] = (double)sample_d[c] * h->dt;
-            if ((rc = launch_sample(h, r, (int)n_ids, verlet ? 1 : 0, grid))) return rc;
+            if ((rc = launch_sample(h, r, (int)n_ids, verlet ? 1 : 0))) return rc;
             ++r;
         }
     }
@@ -2034,20 +2163,16 @@ int ss_snapshot(ss_engine *h, const int64_t *ids, int64_t n_ids, double gpe_datu
     if (!h->groups.empty()) scales_at(h, h->t, sc.data());
     std::vector<int> dids((size_t)std::max<int64_t>(n_ids, 1), 0);
     for (int64_t i = 0; i < n_ids; ++i) dids[i] = (int)dev_of(h, ids[i]);
-    int sms = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    const int grid = std::max(1, std::min(4 * sms, (int)((std::max<int64_t>(h->energy_springs, h->ND) + 255) / 256)));
     if ((rc = ensure(h, h->d_sids, dids.size() * sizeof(int))) ||
         (rc = ensure(h, h->d_srows, (size_t)std::max<int64_t>(n_ids, 1) * 3 * sizeof(double))) ||
-        (rc = ensure(h, h->d_serows, 4 * sizeof(double))) || (rc = ensure(h, h->d_sscale, G * sizeof(double))) ||
-        (rc = ensure(h, h->d_spartial, (size_t)grid * 3 * sizeof(double))))
+        (rc = ensure(h, h->d_serows, 4 * sizeof(double))) || (rc = ensure(h, h->d_sscale, G * sizeof(double))))
         return rc;
     if ((rc = upload(h, h->d_sids.p, dids.data(), dids.size() * sizeof(int))) ||
         (rc = upload(h, h->d_sscale.p, sc.data(), G * sizeof(double))))
         return rc;
     const double datum = h->gpe_datum;
     h->gpe_datum = gpe_datum;
-    rc = launch_sample(h, 0, (int)n_ids, 0, grid);
+    rc = launch_sample(h, 0, (int)n_ids, 0);
     h->gpe_datum = datum;
     if (rc) return rc;
     CK(cudaStreamSynchronize(h->stream));

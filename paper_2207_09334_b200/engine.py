@@ -163,6 +163,8 @@ class _Mirror:
 class Engine:
     """GPU engine, call-compatible with reference engine.py:173-466."""
 
+    _divergence_error = DivergenceError      # (reference_backend raises the host package's class)
+
     def __init__(self, scene, integrator: str = VERLET, mode: str = SERIAL,
                  threads: int | None = None, *, precision: str = "f64",
                  layout: str = "auto", device: int = 0):
@@ -534,7 +536,7 @@ class Engine:
 
     def _raise_step(self, rc: int, res, what: str) -> None:
         if rc == _lib.SS_EDIVERGED:
-            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+            raise self._divergence_error(int(res.diverged_mass), int(res.diverged_step))
         _lib.check(rc, what)
 
     def step(self, count: int = 1) -> None:
@@ -604,7 +606,7 @@ class Engine:
                                  C.byref(rows), C.byref(res))
         self._mark_stepped()
         if rc == _lib.SS_EDIVERGED:
-            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+            raise self._divergence_error(int(res.diverged_mass), int(res.diverged_step))
         _lib.check(rc, "ss_step_sampled")
         r = int(rows.value)
         return times[:r], pos[:r, :ids.size], en[:r]
@@ -660,7 +662,7 @@ class Engine:
         res = _lib.StepResult()
         rc = _lib.lib().ss_sync(self._h, C.byref(res))
         if rc == _lib.SS_EDIVERGED:
-            raise DivergenceError(int(res.diverged_mass), int(res.diverged_step))
+            raise self._divergence_error(int(res.diverged_mass), int(res.diverged_step))
         _lib.check(rc, "ss_sync")
 
     @property

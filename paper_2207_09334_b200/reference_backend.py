@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import importlib
 
+from .engine import DivergenceError as _GpuDivergenceError
 from .engine import Engine as _GpuEngine
 
 _MODULES = ("springsim", "springsim.engine", "springsim.bench", "springsim.analysis", "springsim.service")
@@ -24,7 +25,17 @@ def enable(precision: str = "f64"):
     """Make ``springsim.Engine`` (and every module's imported copy) this engine."""
     ref_engine = importlib.import_module("springsim.engine")
 
+    class DivergenceError(ref_engine.DivergenceError, _GpuDivergenceError):
+        """Caught as either package's DivergenceError (the reference's
+        analysis and tests catch springsim.engine.DivergenceError)."""
+
+        def __init__(self, mass_id: int, step: int):
+            RuntimeError.__init__(self, _GpuDivergenceError.MESSAGE.format(step=step, mass_id=mass_id))
+            self.mass_id, self.step = mass_id, step
+
     class Engine(_GpuEngine):
+        _divergence_error = DivergenceError
+
         def __init__(self, scene, integrator=ref_engine.VERLET, mode=ref_engine.SERIAL, threads=None):
             super().__init__(scene, integrator=integrator, mode=mode, threads=threads, precision=precision)
 

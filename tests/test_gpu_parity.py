@@ -60,12 +60,12 @@ def test_fp64_explicit_tile_format_bitwise(case, monkeypatch):
 
 
 def test_fp64_compact_format_is_the_default():
-    """Compact fp64 tiles, stepped by tile_f64_kernel (4) for Euler/Verlet
-    and by kernels.cuh's rk4_kernel (3) for RK4."""
+    """Compact fp64 tiles, stepped by tile_f64_kernel (4) for Euler, Verlet
+    and the four RK4 stages."""
     d, eng = run_engine("block9_excited_verlet", "tile")
     assert eng.info()["tile_kernel"] == 4
     rk = Engine(L.block_scene(9), integrator="rk4", precision="f64", layout="tile")
-    assert rk.info()["tile_kernel"] == 3
+    assert rk.info()["tile_kernel"] == 4
 
 
 @pytest.mark.parametrize("integrator", ["verlet", "euler", "rk4"])
@@ -78,7 +78,7 @@ def test_fp64_compact_equals_explicit_on_a_crawler_batch(integrator, monkeypatch
     for fmt in ("1", "0"):
         monkeypatch.setenv("SS_TILE_DICT", fmt)
         eng = Engine(batch, integrator=integrator, precision="f64", layout="tile")
-        assert eng.info()["tile_kernel"] == ((3 if integrator == "rk4" else 4) if fmt == "1" else 0)
+        assert eng.info()["tile_kernel"] == (4 if fmt == "1" else 0)
         eng.set_damping(1e-4)
         eng.step(600)
         runs.append((eng.x.copy(), eng.v.copy(), eng.degenerate_springs))

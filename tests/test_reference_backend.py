@@ -43,3 +43,21 @@ def test_enable_routes_every_engine_user(springsim):
     finally:
         reference_backend.disable()
     assert reng.Engine is original and rbench.Engine is original
+
+
+def test_divergence_is_the_reference_exception(springsim):
+    """The routed engine raises a DivergenceError that the reference's own
+    callers catch (springsim.engine.DivergenceError, analysis.py re-raises it
+    as a time-step RuntimeError) and that this package's callers catch too,
+    with the reference's message and attributes."""
+    import springsim.engine as reng
+    from paper_2207_09334_b200 import reference_backend
+    from paper_2207_09334_b200.engine import DivergenceError as Ours
+    Engine = reference_backend.enable()
+    try:
+        err = Engine._divergence_error(7, 41)
+        assert isinstance(err, reng.DivergenceError) and isinstance(err, Ours)
+        assert (err.mass_id, err.step) == (7, 41)
+        assert str(err) == str(reng.DivergenceError(7, 41))
+    finally:
+        reference_backend.disable()
