@@ -133,7 +133,7 @@ struct ss_engine {
     size_t smem_bytes = 0;
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
     size_t f64_smem = 0;           // fp64 Euler/Verlet compact-format tile kernel (tile_f64.cuh), 0 = off
-    int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3), 3 (3,3)
+    int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3), 3 (3,3), 4 (1,5), 5 (2,5)
     int lean_lanes = 1;            // threads per mass of that kernel (2: scenes with few tiles)
     int persist_max_grid = 0;      // co-resident CTAs of the persistent kernel (0: never persistent)
     bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
@@ -587,6 +587,8 @@ void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
         case 1: k = euler ? tile_f64_kernel<0, GROUPS, 1, 4> : tile_f64_kernel<1, GROUPS, 1, 4>; break;
         case 2: k = euler ? tile_f64_kernel<0, GROUPS, 2, 3> : tile_f64_kernel<1, GROUPS, 2, 3>; break;
         case 3: k = euler ? tile_f64_kernel<0, GROUPS, 3, 3> : tile_f64_kernel<1, GROUPS, 3, 3>; break;
+        case 4: k = euler ? tile_f64_kernel<0, GROUPS, 1, 5> : tile_f64_kernel<1, GROUPS, 1, 5>; break;
+        case 5: k = euler ? tile_f64_kernel<0, GROUPS, 2, 5> : tile_f64_kernel<1, GROUPS, 2, 5>; break;
         default: k = euler ? tile_f64_kernel<0, GROUPS, 2, 4> : tile_f64_kernel<1, GROUPS, 2, 4>; break;
     }
     if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
@@ -1246,6 +1248,10 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_f64_kernel<0, true, 2, 3>, tile_f64_kernel<1, true, 2, 3>,
                                  tile_f64_kernel<0, false, 3, 3>, tile_f64_kernel<1, false, 3, 3>,
                                  tile_f64_kernel<0, true, 3, 3>, tile_f64_kernel<1, true, 3, 3>,
+                                 tile_f64_kernel<0, false, 1, 5>, tile_f64_kernel<1, false, 1, 5>,
+                                 tile_f64_kernel<0, true, 1, 5>, tile_f64_kernel<1, true, 1, 5>,
+                                 tile_f64_kernel<0, false, 2, 5>, tile_f64_kernel<1, false, 2, 5>,
+                                 tile_f64_kernel<0, true, 2, 5>, tile_f64_kernel<1, true, 2, 5>,
                                  tile_f64_kernel<2, false, 2, 4>, tile_f64_kernel<3, false, 2, 4>,
                                  tile_f64_kernel<4, false, 2, 4>, tile_f64_kernel<5, false, 2, 4>,
                                  tile_f64_kernel<2, true, 2, 4>, tile_f64_kernel<3, true, 2, 4>,
