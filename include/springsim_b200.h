@@ -112,6 +112,14 @@ int         ss_abi_version(void);
 const char *ss_last_error(void);
 int         ss_device_count(int *count);
 
+/* Page-locked host buffers (cudaHostAlloc).  State arrays passed to
+ * ss_set_state / ss_get_state that live in page-locked memory (these, or
+ * torch pin_memory tensors) cross the bus in one DMA, without the pageable
+ * staging copy.  No reference counterpart: the reference keeps its state in
+ * numpy arrays (engine.py:196-208); this is the transfer path behind them. */
+int ss_pinned_alloc(size_t bytes, void **out);
+int ss_pinned_free(void *p);
+
 /* Engine.__init__ (engine.py:182-246). */
 int ss_create(const ss_scene_desc *desc, ss_engine **out);
 int ss_destroy(ss_engine *h);

@@ -54,6 +54,7 @@ from .model import (
 )
 from .traces import TraceSeries
 from .batch import per_instance, replicate
+from ._lib import pinned_copy, pinned_empty
 from .sceneio import SceneFormatError, load_scene, parse_scene, render_scene, save_scene
 
 __version__ = "0.1.0"

@@ -149,6 +149,21 @@ def energy_breakdown(x, v, m, si, sj, k, l0_eff, gravity, datum: float):
         return _elastic(x, si, sj, k, l0_eff), _gravitational(x, m, gravity, datum), _kinetic(v, m)
 
 
+PINNED_MIRROR_BYTES = 256 << 20      # state readbacks up to this size land in page-locked memory
+
+
+def _host_state(n: int) -> np.ndarray:
+    """A fresh (n, 3) f64 host array for a readback: page-locked (one DMA,
+    pooled, no first-touch page faults) up to PINNED_MIRROR_BYTES, else
+    ordinary memory."""
+    if n * 24 <= PINNED_MIRROR_BYTES:
+        try:
+            return _lib.pinned_empty((n, 3))
+        except _lib.CudaError:           # page-locked memory exhausted
+            pass
+    return np.empty((n, 3))
+
+
 class _Mirror:
     """Lazy host copy of one (N,3) device array with lend/upload tracking."""
 
@@ -323,9 +338,9 @@ class Engine:
         if not (need_x or need_v or need_p):
             return
         has_prev = C.c_int(0)
-        x = np.empty((n, 3)) if need_x else None
-        v = np.empty((n, 3)) if need_v else None
-        p = np.empty((n, 3)) if need_p else None
+        x = _host_state(n) if need_x else None
+        v = _host_state(n) if need_v else None
+        p = _host_state(n) if need_p else None
         _lib.check(lib.ss_get_state(self._h, _lib.dptr(x), _lib.dptr(v), _lib.dptr(p),
                                     C.byref(has_prev)), "ss_get_state")
         if need_x:

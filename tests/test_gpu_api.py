@@ -549,3 +549,33 @@ def test_results_do_not_depend_on_batching(precision, scene):
         runs.append((eng.x.tobytes(), eng.v.tobytes()))
         eng.close()
     assert runs[0] == runs[1] == runs[2]
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_page_locked_state_arrays(precision):
+    """State assigned from page-locked arrays (one DMA) and from ordinary
+    numpy arrays (staged) gives the same bits; readbacks land in pooled
+    page-locked buffers and stay valid while the caller holds them."""
+    from paper_2207_09334_b200 import lattice as L, pinned_copy
+    from paper_2207_09334_b200 import _lib
+    sc = L.excite(L.block_scene(12), seed=11)
+    out = []
+    for pin in (False, True):
+        eng = Engine(sc, integrator="verlet", precision=precision)
+        eng.step(5)
+        x, v, xp = eng.x.copy(), eng.v.copy(), eng.x_prev.copy()
+        x[:, 0] += 1e-3
+        if pin:
+            x, v, xp = pinned_copy(x), pinned_copy(v), pinned_copy(xp)
+        held = []
+        for _ in range(3):
+            eng.x, eng.v, eng.x_prev = x, v, xp
+            eng.step(7)
+            held.append(eng.x)                            # a readback the caller keeps
+        assert all(h.tobytes() == held[0].tobytes() for h in held)
+        out.append((held[-1].tobytes(), eng.v.tobytes(), eng.x_prev.tobytes()))
+        eng.close()
+    assert out[0] == out[1]
+    a = _lib.pinned_empty((1000, 3))
+    a[:] = 1.5
+    assert a.flags.c_contiguous and float(a.sum()) == 4500.0
