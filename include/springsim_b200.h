@@ -36,6 +36,7 @@ extern "C" {
 #define SS_ECUDA          2   /* CUDA runtime error (no device, OOM, launch failure)        */
 #define SS_EDIVERGED      3   /* DivergenceError (engine.py:44-52,375-381)                   */
 #define SS_ENOMEM         4   /* host allocation failure                                     */
+#define SS_EFALLBACK      5   /* scene document outside the native fast path: use the host parser */
 
 /* integrators (engine.py:34-37) */
 #define SS_EULER   0
@@ -296,6 +297,30 @@ int ss_set_gpe_datum(ss_engine *h, double datum);
  * must equal the library's bit for bit; tests/test_gpu_f64_kernel.py). */
 int ss_check_f64_fastpath(int32_t device, const double *a, const double *b, int64_t n,
                           double *out, int32_t *ok);
+
+/* Scene documents (sceneio.py:57-239): native codec for the bulk "masses"
+ * and "springs" arrays (paper_2207_09334_b200/csrc/sceneio.cpp).
+ * ss_doc_render_*: the exact text json.dumps(doc, indent=2) writes for that
+ * array (entries joined by ",\n", without the brackets), malloc'd, freed by
+ * ss_doc_free_text; SS_EFALLBACK for non-finite values (the host raises the
+ * reference's error).  ss_doc_parse: strict fast path over a whole ASCII
+ * document; SS_EFALLBACK sends the document to the reference-exact host
+ * parser (any error, unusual field, escape or literal). */
+typedef struct ss_doc ss_doc;
+int  ss_doc_render_masses(int64_t n, const double *m, const double *x, const double *v, const double *f,
+                          const uint8_t *fixed, char **out, int64_t *len);
+int  ss_doc_render_springs(int64_t n, const int64_t *si, const int64_t *sj, const double *k, const double *l0,
+                           const int32_t *group, const char *const *labels, int32_t n_labels, char **out,
+                           int64_t *len);
+void ss_doc_free_text(char *p);
+int  ss_doc_repr(int64_t n, const double *v, char **out, int64_t *len);
+int  ss_doc_parse(const char *text, int64_t len, ss_doc **out);
+int  ss_doc_info(const ss_doc *d, int64_t *n_masses, int64_t *n_springs, int32_t *n_keys, int32_t *n_labels);
+int  ss_doc_key(const ss_doc *d, int32_t i, const char **name, int64_t *off, int64_t *len);
+const char *ss_doc_label(const ss_doc *d, int32_t i);
+int  ss_doc_masses(const ss_doc *d, double *m, double *x, double *v, double *f, uint8_t *fixed);
+int  ss_doc_springs(const ss_doc *d, int64_t *si, int64_t *sj, double *k, double *l0, int32_t *group);
+void ss_doc_free(ss_doc *d);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ import numpy as np
 LIB_NAME = "libspringsim_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-SS_OK, SS_EINVAL, SS_ECUDA, SS_EDIVERGED, SS_ENOMEM = 0, 1, 2, 3, 4
+SS_OK, SS_EINVAL, SS_ECUDA, SS_EDIVERGED, SS_ENOMEM, SS_EFALLBACK = 0, 1, 2, 3, 4, 5
 SS_EULER, SS_VERLET, SS_RK4 = 0, 1, 2
 SS_F64, SS_F32 = 0, 1
 SS_LAYOUT_AUTO, SS_LAYOUT_CSR, SS_LAYOUT_ELL, SS_LAYOUT_TILE = 0, 1, 2, 3
@@ -108,6 +108,19 @@ SIGNATURES = {
     "ss_check_f64_fastpath": (C.c_int, [C.c_int32, _dp, _dp, C.c_int64, _dp, _i32p]),
     "ss_pending_wait": (C.c_int, [C.c_void_p, C.c_int64]),
     "ss_set_gpe_datum": (C.c_int, [C.c_void_p, C.c_double]),
+    "ss_doc_render_masses": (C.c_int, [C.c_int64, _dp, _dp, _dp, _dp, _u8p, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_int64)]),
+    "ss_doc_render_springs": (C.c_int, [C.c_int64, _i64p, _i64p, _dp, _dp, _i32p, C.POINTER(C.c_char_p),
+                                        C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "ss_doc_free_text": (None, [C.c_void_p]),
+    "ss_doc_repr": (C.c_int, [C.c_int64, _dp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "ss_doc_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "ss_doc_info": (C.c_int, [C.c_void_p, _i64p, _i64p, _i32p, _i32p]),
+    "ss_doc_key": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_char_p), _i64p, _i64p]),
+    "ss_doc_label": (C.c_char_p, [C.c_void_p, C.c_int32]),
+    "ss_doc_masses": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _u8p]),
+    "ss_doc_springs": (C.c_int, [C.c_void_p, _i64p, _i64p, _dp, _dp, _i32p]),
+    "ss_doc_free": (None, [C.c_void_p]),
 }
 
 _lib = None

@@ -13,10 +13,12 @@ via ``validate_scene``) and returns an :class:`ArrayScene` ready for
 
 from __future__ import annotations
 
+import ctypes as C
 import json
 
 import numpy as np
 
+from . import _lib
 from .model import ActuationGroup, ArrayScene, ContactPlane, Material, scene_arrays, validate_scene
 
 SCHEMA_VERSION = 1
@@ -38,18 +40,12 @@ def _vec(a) -> list:
 
 def render_scene(scene) -> str:
     """Serialize ``scene`` (Scene, ArrayScene or a reference Scene) to the
-    versioned document text (sceneio.py:57-75)."""
+    versioned document text (sceneio.py:57-75).  The masses and springs
+    arrays are written by the native codec (csrc/sceneio.cpp), the rest by
+    json.dumps; non-finite values go through the host writer, which raises
+    the reference's error."""
     a = scene_arrays(scene)
     labels = [g[0] for g in a.group_params]
-    x, v, f = a.x.tolist(), a.v.tolist(), a.f_ext.tolist()
-    m, fixed = a.m.tolist(), a.fixed.tolist()
-    masses = [{"id": i, "m": m[i], "x": x[i], "v": v[i], "f_ext": f[i], "fixed": bool(fixed[i])}
-              for i in range(len(m))]
-    si, sj, k, l0 = a.si.tolist(), a.sj.tolist(), a.k.tolist(), a.l0.tolist()
-    grp = a.group.tolist() if a.group is not None else None
-    springs = [{"id": s, "i": si[s], "j": sj[s], "k": k[s], "l0": l0[s],
-                "group": (labels[grp[s]] if grp is not None and grp[s] >= 0 else None)}
-               for s in range(len(si))]
     mats = [{"name": mt.name, "k0": mt.k0, "l_ref": mt.l_ref, "density": mt.density,
              "total_mass": mt.total_mass, "mass_per_node": mt.mass_per_node}
             for mt in getattr(scene, "materials", [])]
@@ -58,11 +54,69 @@ def render_scene(scene) -> str:
     planes = [{"normal": _vec(nrm), "offset": off, "penalty": pen, "friction": fr}
               for nrm, off, pen, fr in a.planes]
     doc = {"schema_version": SCHEMA_VERSION, "gravity": _vec(a.gravity), "dt": a.dt, "damping": a.damping,
-           "masses": masses, "springs": springs, "materials": mats, "groups": groups, "planes": planes}
+           "masses": [], "springs": [], "materials": mats, "groups": groups, "planes": planes}
+    bodies = _native_bodies(a, labels)
+    if bodies is None:
+        doc["masses"], doc["springs"] = _mass_entries(a), _spring_entries(a, labels)
     try:
-        return json.dumps(doc, indent=2, allow_nan=False) + "\n"
+        text = json.dumps(doc, indent=2, allow_nan=False) + "\n"
     except ValueError as exc:
         raise SceneFormatError("$", f"non-finite value in scene: {exc}") from exc
+    if bodies is not None:
+        for key, body in zip(("masses", "springs"), bodies):
+            if body:
+                text = text.replace(f'\n  "{key}": [],\n', f'\n  "{key}": [\n{body}\n  ],\n', 1)
+    return text
+
+
+def _mass_entries(a) -> list:
+    x, v, f = a.x.tolist(), a.v.tolist(), a.f_ext.tolist()
+    m, fixed = a.m.tolist(), a.fixed.tolist()
+    return [{"id": i, "m": m[i], "x": x[i], "v": v[i], "f_ext": f[i], "fixed": bool(fixed[i])}
+            for i in range(len(m))]
+
+
+def _spring_entries(a, labels) -> list:
+    si, sj, k, l0 = a.si.tolist(), a.sj.tolist(), a.k.tolist(), a.l0.tolist()
+    grp = a.group.tolist() if a.group is not None else None
+    return [{"id": s, "i": si[s], "j": sj[s], "k": k[s], "l0": l0[s],
+             "group": (labels[grp[s]] if grp is not None and grp[s] >= 0 else None)}
+            for s in range(len(si))]
+
+
+def _take_text(ptr, n) -> str:
+    lib = _lib.lib()
+    try:
+        return C.string_at(ptr, n).decode("ascii")
+    finally:
+        lib.ss_doc_free_text(ptr)
+
+
+def _native_bodies(a, labels):
+    """(masses text, springs text) from the native writer, or None when a
+    value is non-finite (the host writer reports it)."""
+    lib = _lib.lib()
+    f64 = lambda arr: np.ascontiguousarray(arr, dtype=np.float64)
+    m, x, v, f = f64(a.m), f64(a.x), f64(a.v), f64(a.f_ext)
+    fixed = np.ascontiguousarray(a.fixed, dtype=np.uint8)
+    ptr, n = C.c_void_p(), C.c_int64()
+    rc = lib.ss_doc_render_masses(m.shape[0], _lib.dptr(m), _lib.dptr(x), _lib.dptr(v), _lib.dptr(f),
+                                  _lib.u8ptr(fixed), C.byref(ptr), C.byref(n))
+    if rc == _lib.SS_EFALLBACK:
+        return None
+    _lib.check(rc, "ss_doc_render_masses")
+    masses = _take_text(ptr, n.value)
+    si = np.ascontiguousarray(a.si, dtype=np.int64)
+    sj = np.ascontiguousarray(a.sj, dtype=np.int64)
+    k, l0 = f64(a.k), f64(a.l0)
+    group = None if a.group is None else np.ascontiguousarray(a.group, dtype=np.int32)
+    lab = (C.c_char_p * max(1, len(labels)))(*[json.dumps(t).encode("ascii") for t in labels])
+    rc = lib.ss_doc_render_springs(si.shape[0], _lib.i64ptr(si), _lib.i64ptr(sj), _lib.dptr(k), _lib.dptr(l0),
+                                   _lib.i32ptr(group), lab, len(labels), C.byref(ptr), C.byref(n))
+    if rc == _lib.SS_EFALLBACK:
+        return None
+    _lib.check(rc, "ss_doc_render_springs")
+    return masses, _take_text(ptr, n.value)
 
 
 # ------------------------------------------------------------ parsing
@@ -139,15 +193,68 @@ _PLANE = dict(required={"normal": "vec3"},
 
 
 def parse_scene(text: str) -> ArrayScene:
-    """Parse and validate a scene document (sceneio.py:173-239) into arrays."""
-    try:
-        raw = json.loads(text)
-    except json.JSONDecodeError as exc:
-        raise SceneFormatError("$", f"malformed document: {exc}") from exc
+    """Parse and validate a scene document (sceneio.py:173-239) into arrays.
+    The native fast path (csrc/sceneio.cpp) decodes plain documents; any
+    document it does not accept whole goes through the host parser below,
+    which reports the reference's error for it."""
+    fast = _parse_native(text)
+    return fast if fast is not None else _parse_host(text)
+
+
+def _check_top(raw) -> dict:
     top = _expect(raw, "$", **_TOP)
     if top["schema_version"] != SCHEMA_VERSION:
         raise SceneFormatError("$.schema_version",
                                f"unsupported version {top['schema_version']} (this reader handles {SCHEMA_VERSION})")
+    return top
+
+
+def _parse_native(text: str):
+    if not text.isascii():
+        return None
+    lib = _lib.lib()
+    raw_bytes = text.encode("ascii")
+    h = C.c_void_p()
+    rc = lib.ss_doc_parse(raw_bytes, len(raw_bytes), C.byref(h))
+    if rc == _lib.SS_EFALLBACK:
+        return None
+    _lib.check(rc, "ss_doc_parse")
+    try:
+        nm, ns = C.c_int64(), C.c_int64()
+        nk, nl = C.c_int32(), C.c_int32()
+        _lib.check(lib.ss_doc_info(h, C.byref(nm), C.byref(ns), C.byref(nk), C.byref(nl)), "ss_doc_info")
+        raw = {}
+        for i in range(nk.value):
+            name, off, span = C.c_char_p(), C.c_int64(), C.c_int64()
+            _lib.check(lib.ss_doc_key(h, i, C.byref(name), C.byref(off), C.byref(span)), "ss_doc_key")
+            key = name.value.decode("ascii")
+            raw[key] = [] if key in ("masses", "springs") else json.loads(raw_bytes[off.value:off.value + span.value])
+        top = _check_top(raw)
+        n, s = nm.value, ns.value
+        m, x, v, f = np.empty(n), np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 3))
+        fixed = np.empty(n, dtype=np.uint8)
+        _lib.check(lib.ss_doc_masses(h, _lib.dptr(m), _lib.dptr(x), _lib.dptr(v), _lib.dptr(f), _lib.u8ptr(fixed)),
+                   "ss_doc_masses")
+        si, sj = np.empty(s, dtype=np.int64), np.empty(s, dtype=np.int64)
+        k, l0 = np.empty(s), np.empty(s)
+        lab = np.empty(s, dtype=np.int32)
+        _lib.check(lib.ss_doc_springs(h, _lib.i64ptr(si), _lib.i64ptr(sj), _lib.dptr(k), _lib.dptr(l0),
+                                      _lib.i32ptr(lab)), "ss_doc_springs")
+        names = [lib.ss_doc_label(h, g).decode("ascii") for g in range(nl.value)]
+    finally:
+        lib.ss_doc_free(h)
+    dup = _first_duplicate(si, sj, n)       # every entry decoded cleanly: the first duplicate is the first error
+    if dup is not None:
+        raise SceneFormatError(f"$.springs[{dup}]", f"duplicate spring between masses {si[dup]} and {sj[dup]}")
+    return _assemble(top, x, v, f, m, fixed.astype(bool), si, sj, k, l0, names, lab)
+
+
+def _parse_host(text: str) -> ArrayScene:
+    try:
+        raw = json.loads(text)
+    except json.JSONDecodeError as exc:
+        raise SceneFormatError("$", f"malformed document: {exc}") from exc
+    top = _check_top(raw)
     n = len(top["masses"])
     x = np.empty((n, 3))
     v = np.empty((n, 3))
@@ -165,8 +272,9 @@ def parse_scene(text: str) -> ArrayScene:
     sj = np.empty(s_count, dtype=np.int64)
     k = np.empty(s_count)
     l0 = np.empty(s_count)
-    labels: list = []
-    glist = []
+    names: list = []
+    lab = np.full(s_count, -1, dtype=np.int32)
+    pairs = set()
     for idx, entry in enumerate(top["springs"]):
         path = f"$.springs[{idx}]"
         fl = _expect(entry, path, **_SPRING)
@@ -175,8 +283,23 @@ def parse_scene(text: str) -> ArrayScene:
         for end in ("i", "j"):
             if not 0 <= fl[end] < n:
                 raise SceneFormatError(f"{path}.{end}", f"no such mass {fl[end]}")
+        pair = (min(fl["i"], fl["j"]), max(fl["i"], fl["j"]))
+        if pair in pairs:                   # Scene.add_spring (model.py:171-176) raises inside the loop
+            raise SceneFormatError(path, f"duplicate spring between masses {fl['i']} and {fl['j']}")
+        pairs.add(pair)
         si[idx], sj[idx], k[idx], l0[idx] = fl["i"], fl["j"], fl["k"], fl["l0"]
-        glist.append(fl["group"])
+        if fl["group"] is not None:
+            if fl["group"] not in names:
+                names.append(fl["group"])
+            lab[idx] = names.index(fl["group"])
+    return _assemble(top, x, v, f, m, fixed, si, sj, k, l0, names, lab)
+
+
+def _assemble(top, x, v, f, m, fixed, si, sj, k, l0, names, lab) -> ArrayScene:
+    """Materials, groups, planes and the whole-scene checks (sceneio.py:
+    210-239) over decoded columns; ``lab`` indexes ``names``, the distinct
+    spring group strings (-1: no group)."""
+    s_count = si.shape[0]
     mats = [Material(**_expect(e, f"$.materials[{i}]", **_MATERIAL)) for i, e in enumerate(top["materials"])]
     groups = {}
     for i, e in enumerate(top["groups"]):
@@ -190,30 +313,35 @@ def parse_scene(text: str) -> ArrayScene:
         groups[g.label] = g
     labels = list(groups)
     group = None
-    if any(g is not None for g in glist):
-        group = np.full(s_count, -1, dtype=np.int32)
-        for idx, g in enumerate(glist):
-            if g is not None:
-                group[idx] = labels.index(g) if g in groups else -2      # -2: unknown, reported below
+    unknown = [t for t in names if t not in groups]
+    if (lab >= 0).any():                    # defined labels -> group index; others -> -2 - q (validate_scene reports them)
+        lut = np.array([labels.index(t) if t in groups else -2 - unknown.index(t) for t in names], dtype=np.int32)
+        group = np.where(lab >= 0, lut[np.maximum(lab, 0)], -1).astype(np.int32)
     planes = [ContactPlane(**_expect(e, f"$.planes[{i}]", **_PLANE)) for i, e in enumerate(top["planes"])]
     scene = ArrayScene(x=x, m=m, si=si, sj=sj, k=k, l0=l0, v=v, f_ext=f, fixed=fixed, gravity=top["gravity"],
                        dt=top["dt"], damping=top["damping"], groups=groups, group=None, planes=planes,
                        materials=mats)
     if group is not None:
-        if (group == -2).any():
-            bad = int(np.flatnonzero(group == -2)[0])
-            raise SceneFormatError(f"$.springs[{bad}]", f"unknown actuation group {glist[bad]!r}")
         scene.group = group
-    pair = np.sort(np.stack([si, sj], axis=1), axis=1)
-    if s_count and np.unique(pair, axis=0).shape[0] != s_count:
-        _, first = np.unique(pair, axis=0, return_index=True)
-        dup = sorted(set(range(s_count)) - set(first.tolist()))[0]
-        raise SceneFormatError(f"$.springs[{dup}]", f"duplicate spring between masses {si[dup]} and {sj[dup]}")
+        scene.unknown_group_labels = unknown
     violations = validate_scene(scene)
     if violations:
         first = violations[0]
         raise SceneFormatError(f"$.{first.where}", first.message)
     return scene
+
+
+def _first_duplicate(si, sj, n):
+    """Lowest spring index whose unordered pair occurred before (Scene.add_spring's
+    duplicate rule, model.py:171-176), or None: one stable sort of pair keys."""
+    if si.shape[0] < 2:
+        return None
+    lo, hi = np.minimum(si, sj), np.maximum(si, sj)
+    key = lo * max(int(n), 1) + hi
+    order = np.argsort(key, kind="stable")
+    k = key[order]
+    repeat = k[1:] == k[:-1]
+    return int(order[1:][repeat].min()) if repeat.any() else None
 
 
 def save_scene(scene, path) -> None:
