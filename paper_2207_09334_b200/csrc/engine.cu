@@ -101,6 +101,8 @@ struct ss_engine {
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     double *d_raw = nullptr;
     double *d_w = nullptr;
+    double *d_raw2 = nullptr;                  // fp32: second caller-layout buffer (v, x_prev)
+    double *d_x0dev = nullptr;                 // fp32 tiles: X0 per device slot, fp64
     size_t pinned_bytes[3] = {0, 0, 0};
     cudaEvent_t staged = nullptr;              // recorded after asynchronous uploads from `pinned`
     cudaEvent_t chunk_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // chunked downloads
@@ -1434,6 +1436,62 @@ __global__ void device_to_raw_kernel(const double4 *__restrict__ in, const int *
     raw[3 * s + 2] = o.z;
 }
 
+// fp32 tile engines (displacement state r = x - X0, X0 fp64 per device
+// slot): the caller-layout f64 arrays converted on the device with the host
+// packers' exact arithmetic (pack_positions / pack_vec / the u = x - x_prev
+// rounding of set_state_impl, and their inverses), so fp32 state also
+// crosses the bus as the caller's (N,3) f64 arrays.
+__global__ void raw_to_f32_kernel(const double *__restrict__ raw, const double *__restrict__ raw_prev,
+                                  const int *__restrict__ orig_of, int64_t nd, const double *__restrict__ x0,
+                                  const double *__restrict__ w, float4 *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int64_t s = orig_of ? orig_of[i] : i;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (s >= 0) {
+        if (x0) {                                          // position: r = x - X0, w = +-m
+            o.x = (float)(raw[3 * s] - x0[3 * i]);
+            o.y = (float)(raw[3 * s + 1] - x0[3 * i + 1]);
+            o.z = (float)(raw[3 * s + 2] - x0[3 * i + 2]);
+            o.w = (float)w[i];
+        } else if (raw_prev) {                             // increment: u = x - x_prev
+            o.x = (float)(raw[3 * s] - raw_prev[3 * s]);
+            o.y = (float)(raw[3 * s + 1] - raw_prev[3 * s + 1]);
+            o.z = (float)(raw[3 * s + 2] - raw_prev[3 * s + 2]);
+        } else {                                           // velocity
+            o.x = (float)raw[3 * s];
+            o.y = (float)raw[3 * s + 1];
+            o.z = (float)raw[3 * s + 2];
+        }
+    }
+    out[i] = o;
+}
+
+// x = X0 + r (u == null), x_prev = X0 + (r - u), or v (x0 == null).
+__global__ void f32_to_raw_kernel(const float4 *__restrict__ in, const float4 *__restrict__ u,
+                                  const int *__restrict__ orig_of, int64_t nd, const double *__restrict__ x0,
+                                  double *__restrict__ raw) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int64_t s = orig_of ? orig_of[i] : i;
+    if (s < 0) return;
+    const float4 r = in[i];
+    if (!x0) {
+        raw[3 * s] = (double)r.x;
+        raw[3 * s + 1] = (double)r.y;
+        raw[3 * s + 2] = (double)r.z;
+    } else if (!u) {
+        raw[3 * s] = x0[3 * i] + (double)r.x;
+        raw[3 * s + 1] = x0[3 * i + 1] + (double)r.y;
+        raw[3 * s + 2] = x0[3 * i + 2] + (double)r.z;
+    } else {
+        const float4 q = u[i];
+        raw[3 * s] = x0[3 * i] + ((double)r.x - (double)q.x);
+        raw[3 * s + 1] = x0[3 * i + 1] + ((double)r.y - (double)q.y);
+        raw[3 * s + 2] = x0[3 * i + 2] + ((double)r.z - (double)q.z);
+    }
+}
+
 size_t chunk_bytes() {
     static const size_t bytes = [] {
         const char *e = getenv("SS_CHUNK_MB");                // transfer chunk (MB), 4 by default
@@ -1561,6 +1619,35 @@ int raw_download(ss_engine *h, const void *src_vec, double *dst) {
     return d2h_chunked(h, dst, h->d_raw, (size_t)h->N * 3 * sizeof(double));
 }
 
+// Device X0 and the second raw buffer of the fp32 caller-layout transfers.
+int f32_xfer_setup(ss_engine *h) {
+    int rc = chunk_setup(h);
+    if (rc) return rc;
+    if (!h->d_raw2 && (rc = h->alloc(&h->d_raw2, (size_t)h->N * 3 * sizeof(double)))) return rc;
+    if (!h->d_x0dev) {
+        if ((rc = h->alloc(&h->d_x0dev, h->x0.size() * sizeof(double)))) return rc;
+        if ((rc = upload(h, h->d_x0dev, h->x0.data(), h->x0.size() * sizeof(double)))) return rc;
+    }
+    return SS_OK;
+}
+
+// raw (caller layout, already on the device) -> one fp32 state vector
+void f32_from_raw(ss_engine *h, const double *raw, const double *raw_prev, bool position, void *dst) {
+    const unsigned grid = (unsigned)((h->ND + 255) / 256);
+    raw_to_f32_kernel<<<grid, 256, 0, h->stream>>>(raw, raw_prev, h->d_orig_of, h->ND,
+                                                   position ? h->d_x0dev : nullptr, h->d_w,
+                                                   reinterpret_cast<float4 *>(dst));
+}
+
+int f32_download(ss_engine *h, const void *vec, const void *u, bool position, double *dst) {
+    const unsigned grid = (unsigned)((h->ND + 255) / 256);
+    f32_to_raw_kernel<<<grid, 256, 0, h->stream>>>(reinterpret_cast<const float4 *>(vec),
+                                                   reinterpret_cast<const float4 *>(u), h->d_orig_of, h->ND,
+                                                   position ? h->d_x0dev : nullptr, h->d_raw);
+    CK(cudaGetLastError());
+    return d2h_chunked(h, dst, h->d_raw, (size_t)h->N * 3 * sizeof(double));
+}
+
 template <bool F32>
 int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
     using T = typename Prec<F32>::T;
@@ -1575,6 +1662,20 @@ int get_state_impl(ss_engine *h, double *x, double *v, double *x_prev) {
         if (x && (rc = raw_download(h, h->X[h->cur], x))) return rc;
         if (v && (rc = raw_download(h, h->V, v))) return rc;
         if (x_prev && h->has_prev && (rc = raw_download(h, h->X[h->cur ^ 1], x_prev))) return rc;
+        return SS_OK;
+    } else if (h->rx0) {                          // fp32 tiles: converted on the device, caller layout over the bus
+        if ((rc = f32_xfer_setup(h))) return rc;
+        if (h->staged_pending) {
+            CK(cudaEventSynchronize(h->staged));
+            h->staged_pending = false;
+        }
+        if (x && (rc = f32_download(h, h->X[h->cur], nullptr, true, x))) return rc;
+        if (v && (rc = f32_download(h, h->V, nullptr, false, v))) return rc;
+        if (x_prev && h->has_prev) {
+            rc = h->U ? f32_download(h, h->X[h->cur], h->U, true, x_prev)
+                      : f32_download(h, h->X[h->cur ^ 1], nullptr, true, x_prev);
+            if (rc) return rc;
+        }
         return SS_OK;
     }
     T4 *tmp;
@@ -1633,6 +1734,30 @@ int set_state_impl(ss_engine *h, const double *x, const double *v, const double 
         x_prev = keep_prev.data();
     }
     int rc;
+    if constexpr (F32) {
+        // fp32 tiles: caller layout over the bus, converted on the device
+        // (an x_prev without x, under increment-form Verlet, keeps the host path)
+        if (h->rx0 && !(h->U && x_prev && !x)) {
+            if ((rc = f32_xfer_setup(h))) return rc;
+            const size_t bytes = (size_t)h->N * 3 * sizeof(double);
+            if (x) {
+                if ((rc = h2d_chunked(h, h->d_raw, x, bytes))) return rc;
+                f32_from_raw(h, h->d_raw, nullptr, true, h->X[h->cur]);
+            }
+            if (v) {
+                if ((rc = h2d_chunked(h, h->d_raw2, v, bytes))) return rc;
+                f32_from_raw(h, h->d_raw2, nullptr, false, h->V);
+            }
+            if (x_prev) {
+                if ((rc = h2d_chunked(h, h->d_raw2, x_prev, bytes))) return rc;
+                if (h->U) f32_from_raw(h, h->d_raw, h->d_raw2, false, h->U);     // u = x - x_prev
+                else f32_from_raw(h, h->d_raw2, nullptr, true, h->X[h->cur ^ 1]);
+                h->has_prev = true;
+            }
+            CK(cudaGetLastError());
+            return SS_OK;
+        }
+    }
     if constexpr (!F32) {                         // caller layout over the bus, permuted on the device
         if ((rc = chunk_setup(h))) return rc;
         if (x && (rc = raw_upload(h, x, h->X[h->cur], true))) return rc;

@@ -7,10 +7,12 @@ from paper_2207_09334_b200 import Engine, crawler_scene, lattice as L, replicate
 
 scenes = {"crawler": crawler_scene, "crawler_x12": lambda: replicate(crawler_scene(), 12), "beam40": lambda: L.beam_lattice(length=4.0),
           "cube9": lambda: L.excite(L.block_scene(9)), "crawler_x64": lambda: replicate(crawler_scene(), 64)}
+if "SS_RESIDENT" not in os.environ:
+    os.environ["SS_RESIDENT"] = "16"          # (the default cap; "1" would limit residency to one-tile scenes)
 for name, mk in scenes.items():
     for prec in ("f64", "f32"):
         row = {"scene": name, "prec": prec}
-        for res in (os.environ.get("RES_ON", "1"), "0"):
+        for res in (os.environ.get("RES_ON", "16"), "0"):
             os.environ["SS_RESIDENT"] = res
             e = Engine(mk(), integrator="verlet", precision=prec)
             row["slots"] = e.info()["n_masses"]
