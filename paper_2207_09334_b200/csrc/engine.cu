@@ -903,6 +903,8 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     // fp32: clusters of up to kResidentMaxCtas CTAs (measured faster than a
     // launch per step); fp64: one CTA only (its multi-CTA cluster was slower)
     int max_ctas = F32 ? kResidentMaxCtas : 1;
+    if (!F32)
+        if (const char *e = getenv("SS_RESIDENT_F64")) max_ctas = std::min(kResidentMaxCtas, atoi(e));   // A/B
     if (const char *e = getenv("SS_RESIDENT")) max_ctas = std::min(max_ctas, atoi(e));  // 0: off
     if (n_ctas > max_ctas) return SS_OK;
     std::vector<int64_t> dev(h->N);
