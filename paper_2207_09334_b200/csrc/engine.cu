@@ -129,6 +129,9 @@ struct ss_engine {
         *cnt = nullptr;
     int2 *inc = nullptr;
     unsigned char *d_blob = nullptr;
+    double2 *d_kl_inline = nullptr;            // fp64 inline tile format (tiles.h)
+    int8_t *d_g_inline = nullptr;
+    unsigned long long *d_kl_off = nullptr;
     unsigned long long *d_toff = nullptr;
     unsigned int *d_tsplit = nullptr;
     uint32_t blob_smem = 0, max_halo = 0;
@@ -439,6 +442,9 @@ Params<T> base_params(const ss_engine *h) {
     tp.blob_smem = h->blob_smem;
     tp.max_halo = h->max_halo;
     tp.n_tiles = (int)h->tl.n_tiles;
+    tp.kl_inline = h->d_kl_inline;
+    tp.g_inline = h->d_g_inline;
+    tp.kl_off = h->d_kl_off;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -585,6 +591,12 @@ template <bool GROUPS>
 void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
     const bool euler = h->integrator == SS_EULER;
     void (*k)(Params<double>) = nullptr;
+    if (h->tl.inline_kl) {                                 // general graphs: (k, l0) streamed per incidence
+        k = euler ? tile_f64_kernel<0, GROUPS, 2, 4, true> : tile_f64_kernel<1, GROUPS, 2, 4, true>;
+        if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
+        else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
+        return;
+    }
     switch (h->f64_variant) {
         case 1: k = euler ? tile_f64_kernel<0, GROUPS, 1, 4> : tile_f64_kernel<1, GROUPS, 1, 4>; break;
         case 2: k = euler ? tile_f64_kernel<0, GROUPS, 2, 3> : tile_f64_kernel<1, GROUPS, 2, 3>; break;
@@ -602,11 +614,12 @@ void launch_tile_f64(ss_engine *h, const Params<double> &p, int grid) {
 template <bool GROUPS>
 void launch_rk4_f64(ss_engine *h, const Params<double> &p, int grid, int stage) {
     void (*k)(Params<double>) = nullptr;
+    const bool inl = h->tl.inline_kl;
     switch (stage) {
-        case 1: k = tile_f64_kernel<2, GROUPS, 2, 4>; break;
-        case 2: k = tile_f64_kernel<3, GROUPS, 2, 4>; break;
-        case 3: k = tile_f64_kernel<4, GROUPS, 2, 4>; break;
-        default: k = tile_f64_kernel<5, GROUPS, 2, 4>; break;
+        case 1: k = inl ? tile_f64_kernel<2, GROUPS, 2, 4, true> : tile_f64_kernel<2, GROUPS, 2, 4>; break;
+        case 2: k = inl ? tile_f64_kernel<3, GROUPS, 2, 4, true> : tile_f64_kernel<3, GROUPS, 2, 4>; break;
+        case 3: k = inl ? tile_f64_kernel<4, GROUPS, 2, 4, true> : tile_f64_kernel<4, GROUPS, 2, 4>; break;
+        default: k = inl ? tile_f64_kernel<5, GROUPS, 2, 4, true> : tile_f64_kernel<5, GROUPS, 2, 4>; break;
     }
     if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
     else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
@@ -1183,6 +1196,17 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         h->d_toff = reinterpret_cast<unsigned long long *>(p);
         if ((rc = up_vec(h, &p, L.split))) return rc;
         h->d_tsplit = reinterpret_cast<unsigned int *>(p);
+        if (L.inline_kl) {                        // fp64 general-graph format: records streamed, not staged
+            if ((rc = up_vec(h, &p, L.kl_inline))) return rc;
+            h->d_kl_inline = reinterpret_cast<double2 *>(p);
+            if (!L.g_inline.empty()) {
+                if ((rc = up_vec(h, &p, L.g_inline))) return rc;
+                h->d_g_inline = reinterpret_cast<int8_t *>(p);
+            }
+            std::vector<unsigned long long> ko(L.kl_off.begin(), L.kl_off.end());
+            if ((rc = up_vec(h, &p, ko))) return rc;
+            h->d_kl_off = reinterpret_cast<unsigned long long *>(p);
+        }
         h->blob_smem = (L.max_tile_smem + 127u) & ~127u;
         h->max_halo = L.max_halo;
         h->smem_bytes = 128 + h->blob_smem + (size_t)(kTile + L.max_halo) * sizeof(T4);   // one staged vector per mass
@@ -1259,7 +1283,13 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_f64_kernel<2, false, 2, 4>, tile_f64_kernel<3, false, 2, 4>,
                                  tile_f64_kernel<4, false, 2, 4>, tile_f64_kernel<5, false, 2, 4>,
                                  tile_f64_kernel<2, true, 2, 4>, tile_f64_kernel<3, true, 2, 4>,
-                                 tile_f64_kernel<4, true, 2, 4>, tile_f64_kernel<5, true, 2, 4>})
+                                 tile_f64_kernel<4, true, 2, 4>, tile_f64_kernel<5, true, 2, 4>,
+                                 tile_f64_kernel<0, false, 2, 4, true>, tile_f64_kernel<1, false, 2, 4, true>,
+                                 tile_f64_kernel<0, true, 2, 4, true>, tile_f64_kernel<1, true, 2, 4, true>,
+                                 tile_f64_kernel<2, false, 2, 4, true>, tile_f64_kernel<3, false, 2, 4, true>,
+                                 tile_f64_kernel<4, false, 2, 4, true>, tile_f64_kernel<5, false, 2, 4, true>,
+                                 tile_f64_kernel<2, true, 2, 4, true>, tile_f64_kernel<3, true, 2, 4, true>,
+                                 tile_f64_kernel<4, true, 2, 4, true>, tile_f64_kernel<5, true, 2, 4, true>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max));
             }
         }
@@ -2517,12 +2547,13 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->ell_width_ref = h->tl.max_Wr;
         info->canonical_order = h->tl.canonical ? 1 : 0;
         info->tile_count = h->tl.n_tiles;
-        info->tile_blob_bytes = (int64_t)h->tl.blob.size();
+        info->tile_blob_bytes = (int64_t)(h->tl.blob.size() + 8 * h->tl.kl_inline.size() + h->tl.g_inline.size());
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
         info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1)
-                          : h->f64_smem ? 4 : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
+                          : h->f64_smem ? (h->tl.inline_kl ? 5 : 4)
+                                        : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
         info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->f64_smem ? h->f64_smem : h->smem_bytes);
     } else {
         info->ell_width_own = h->lay.W;
@@ -2559,7 +2590,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     info->ell_width_ref = tl.max_Wr;
     info->canonical_order = tl.canonical ? 1 : 0;
     info->tile_count = tl.n_tiles;
-    info->tile_blob_bytes = (int64_t)tl.blob.size();
+    info->tile_blob_bytes = (int64_t)(tl.blob.size() + 8 * tl.kl_inline.size() + tl.g_inline.size());
     info->tile_halo_ratio = tl.halo_ratio;
     info->tile_foreign_frac = tl.foreign_frac;
     const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
@@ -2568,7 +2599,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     info->kernel_smem = info->smem_per_block;
-    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : (tl.compact ? 3 : 0);
+    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : (tl.inline_kl ? 5 : tl.compact ? 3 : 0);
     return SS_OK;
 }
 

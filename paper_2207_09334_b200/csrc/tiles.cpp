@@ -135,11 +135,11 @@ void put(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 // over a per-tile dictionary of distinct (k, l0, group).  SS_EAGAIN_DICT when
 // a tile does not fit (more than 64 dictionary entries, more than 768 halo
 // slots, a mass of degree > 255, a self spring).
-int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
+int build_tiles_f64_compact(const TileInput &in, TileLayout &L, bool inline_kl) {
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     for (int64_t s = 0; s < S; ++s)
-        if (in.si[s] == in.sj[s]) return SS_EAGAIN_DICT;
+        if (in.si[s] == in.sj[s]) return SS_EAGAIN_SHAPE;
     L = TileLayout{};
     std::vector<int32_t> zcell;
     tile_order(in, L.orig_of, &zcell);
@@ -172,8 +172,10 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
     std::vector<std::vector<uint8_t>> parts(n_tiles);
     std::vector<uint32_t> tW(n_tiles), tH(n_tiles), tSplit(n_tiles), tN(n_tiles);
     std::vector<double> tRatio(n_tiles);
+    std::vector<std::vector<double>> tKL(inline_kl ? n_tiles : 0);
+    std::vector<std::vector<int8_t>> tG(inline_kl && in.group ? n_tiles : 0);
     const bool has_g = in.group != nullptr;
-    int err = 0;
+    int err = 0;        // 3: a tile's shape does not fit (degree, halo); 4: its dictionary does not
 
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = 0; t < n_tiles; ++t) {
@@ -219,39 +221,53 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
             err = 3;
             continue;
         }
-        // dictionary of distinct (k, l0, group), in first-use order
+        // dictionary of distinct (k, l0, group), in first-use order; inline
+        // format: (k, l0) and the group per incidence instead
         std::vector<std::tuple<uint64_t, uint64_t, int32_t>> keys;
         std::vector<uint16_t> incs((size_t)W * kTile, 0);
+        if (inline_kl) {
+            tKL[t].assign((size_t)2 * W * kTile, 0.0);
+            if (has_g) tG[t].assign((size_t)W * kTile, (int8_t)-1);
+        }
         bool fits = true;
         for (int l = 0; l < n && fits; ++l) {
             const int64_t m = base + l;
             for (int64_t q = ptr[m]; q < ptr[m + 1]; ++q) {
                 const int32_t s = inc_s[q], o = inc_o[q];
-                uint64_t kb, lb;
-                std::memcpy(&kb, &in.k[s], 8);
-                std::memcpy(&lb, &in.l0[s], 8);
-                const auto key = std::make_tuple(kb, lb, has_g ? in.group[s] : -1);
+                const size_t at = (size_t)(q - ptr[m]) * kTile + l;
                 size_t di = 0;
-                while (di < keys.size() && keys[di] != key) ++di;
-                if (di == keys.size()) {
-                    if (keys.size() == 64) { fits = false; break; }
-                    keys.push_back(key);
+                if (inline_kl) {
+                    tKL[t][2 * at] = in.k[s];
+                    tKL[t][2 * at + 1] = in.l0[s];
+                    if (has_g) tG[t][at] = (int8_t)in.group[s];
+                } else {
+                    uint64_t kb, lb;
+                    std::memcpy(&kb, &in.k[s], 8);
+                    std::memcpy(&lb, &in.l0[s], 8);
+                    const auto key = std::make_tuple(kb, lb, has_g ? in.group[s] : -1);
+                    while (di < keys.size() && keys[di] != key) ++di;
+                    if (di == keys.size()) {
+                        if (keys.size() == 64) { fits = false; break; }
+                        keys.push_back(key);
+                    }
                 }
                 const uint32_t slot = (o >= base && o < base + n)
                                           ? (uint32_t)(o - base)
                                           : halo_slot[std::lower_bound(halo.begin(), halo.end(), o) - halo.begin()];
-                incs[(size_t)(q - ptr[m]) * kTile + l] = (uint16_t)(slot | (di << 10));
+                incs[at] = (uint16_t)(slot | (di << 10));
             }
         }
         if (!fits) {
+            if (err != 3) {
 #pragma omp atomic write
-            err = 3;
+                err = 4;
+            }
             continue;
         }
         const uint32_t nd = (uint32_t)keys.size();
         TileHdr h{};
         h.n = n; h.W = W; h.Wr = W; h.n_halo = (uint32_t)halo_ids.size();
-        h.canonical = 1u | 2u;                 // bit 1: compact format
+        h.canonical = 1u | 2u | (inline_kl ? 4u : 0u);   // bit 1: compact format; bit 2: inline (k, l0)
         h.slice_log2 = 8;
         h.n_dict = nd;
         uint32_t off = align16(sizeof(TileHdr));
@@ -280,6 +296,7 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
         tSplit[t] = h.off_cnt | ((uint32_t)(n - 1) << 24);
         tRatio[t] = (double)(n + halo.size()) / n;
     }
+    if (err == 3) return SS_EAGAIN_SHAPE;
     if (err) return SS_EAGAIN_DICT;
     if (in.group) {
         for (int64_t s = 0; s < S; ++s)
@@ -287,6 +304,18 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
     }
     L.canonical = true;
     L.compact = true;
+    L.inline_kl = inline_kl;
+    if (inline_kl) {
+        L.kl_off.assign(n_tiles + 1, 0);
+        for (int64_t t = 0; t < n_tiles; ++t) L.kl_off[t + 1] = L.kl_off[t] + tKL[t].size() / 2;
+        L.kl_inline.resize(2 * L.kl_off[n_tiles]);
+        if (has_g) L.g_inline.resize(L.kl_off[n_tiles]);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < n_tiles; ++t) {
+            std::memcpy(L.kl_inline.data() + 2 * L.kl_off[t], tKL[t].data(), tKL[t].size() * 8);
+            if (has_g) std::memcpy(L.g_inline.data() + L.kl_off[t], tG[t].data(), tG[t].size());
+        }
+    }
     L.split = tSplit;
     L.off.assign(n_tiles + 1, 0);
     for (int64_t t = 0; t < n_tiles; ++t) L.off[t + 1] = L.off[t] + parts[t].size();
@@ -314,10 +343,15 @@ int build_tiles_f64_compact(const TileInput &in, TileLayout &L) {
 int build_tiles(const TileInput &in, TileLayout &L) {
     if (in.f32) return build_tiles_f32(in, L);
     {
-        const char *env = getenv("SS_TILE_DICT");     // 0: the explicit fp64 format
-        if (!env || atoi(env) != 0) {
-            const int rc = build_tiles_f64_compact(in, L);
-            if (rc != SS_EAGAIN_DICT) return rc;
+        // SS_TILE_DICT: unset -> dictionary, else inline, else explicit;
+        // "0" -> inline (the general-graph format); "explicit" -> explicit
+        const char *env = getenv("SS_TILE_DICT");
+        const bool explicit_only = env && std::strcmp(env, "explicit") == 0;
+        const bool inline_only = env && !explicit_only && atoi(env) == 0;
+        if (!explicit_only) {
+            int rc = inline_only ? SS_EAGAIN_DICT : build_tiles_f64_compact(in, L, false);
+            if (rc == SS_EAGAIN_DICT) rc = build_tiles_f64_compact(in, L, true);
+            if (rc != SS_EAGAIN_DICT && rc != SS_EAGAIN_SHAPE) return rc;
         }
     }
     const int64_t N = in.N, S = in.S;

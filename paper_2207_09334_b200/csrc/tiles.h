@@ -7,7 +7,8 @@
 namespace ss {
 
 constexpr int kTile = 256;            // masses per tile == threads per CTA
-constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compact format
+constexpr int SS_EAGAIN_DICT = -1000;  // internal: a tile's (k, l0, group) dictionary does not fit the compact format
+constexpr int SS_EAGAIN_SHAPE = -1001; // internal: a tile's degree or halo (or a self spring) does not fit it at all
 
 // Per-tile blob header (all offsets in bytes from the tile start, 16-B aligned).
 // [0, off_cnt) (header + halo ids) is copied first so the halo gather
@@ -21,7 +22,15 @@ constexpr int SS_EAGAIN_DICT = -1000; // internal: a tile does not fit the compa
 //   dictionary of n_dict (k, l0) double pairs at off_okl | int8 groups at
 //   off_og.
 //
-// fp64 explicit builds (the fallback; tiles.cpp build_tiles): 32-wide ELL slices.
+// fp64 inline builds (canonical bits 1|2|4; the general-graph format, used
+// when some tile has more than 64 distinct (k, l0, group) -- jittered
+// robot populations, irregular meshes -- or with SS_TILE_DICT=0): the
+// compact layout without a dictionary.  Incidences are the partner slot
+// only, and each incidence's (k, l0) double pair (and int8 group) sits in
+// the separate global arrays TileLayout::kl_inline / g_inline at
+// kl_off[tile] + q*256 + l, streamed by the kernel instead of staged.
+//
+// fp64 explicit builds (the old fallback, SS_TILE_DICT=explicit; tiles.cpp build_tiles): 32-wide ELL slices.
 //   Section order: header | halo ids | counts | own other | own (k,l0) |
 //   own grp | refs | foreign owner | foreign (k,l0) | foreign grp.
 //   counts: n_own | n_ref << 8.  A mass sums references then own records,
@@ -103,7 +112,11 @@ struct TileLayout {
     int max_W = 0, max_Wr = 0;
     bool canonical = true;
     bool has_self = false;          // a spring joins a mass to itself
-    bool compact = false;           // fp32 compact format (tiles_f32.cpp)
+    bool compact = false;           // compact format (fp32 tiles_f32.cpp, fp64 build_tiles_f64_compact)
+    bool inline_kl = false;         // fp64 inline format: (k, l0) per incidence in kl_inline
+    std::vector<double> kl_inline;  // inline format: (k, l0) pairs, tile t at kl_off[t] pairs
+    std::vector<int8_t> g_inline;   // inline format: group per incidence (empty: no groups)
+    std::vector<uint64_t> kl_off;   // inline format: n_tiles + 1 pair offsets
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };

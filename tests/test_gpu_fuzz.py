@@ -75,7 +75,7 @@ CASES = [  # (seed, masses, long-range fraction, lattice, layout, expected tile 
     (4, 2744, 0.0, True, "auto", 3),
     (5, 700, 0.05, False, "auto", None),     # long-range springs: big halos / fallbacks
     (6, 1500, 0.0, False, "csr", None),
-    (7, 1200, 0.0, False, "auto", 0),        # every spring distinct: explicit fp64 format
+    (7, 1200, 0.0, False, "auto", 5),        # every spring distinct: the inline (general-graph) fp64 format
     (8, 3375, 0.01, True, "auto", None),
 ]
 
@@ -87,7 +87,7 @@ def test_random_scene_fp64_bitwise(seed, n, long_range, lattice, layout, fmt, in
     scene = random_scene(seed, n, long_range=long_range, lattice=lattice)
     eng = Engine(scene, integrator=integrator, precision="f64", layout=layout)
     if fmt is not None and integrator != "rk4":
-        # compact fp64 tiles step on tile_f64_kernel (4), explicit ones on step_kernel (0)
+        # compact fp64 tiles step on tile_f64_kernel (4; 5 with inline records)
         assert eng.info()["tile_kernel"] == (4 if fmt == 3 else fmt)
     ref = orc.OracleEngine(scene_arrays(scene), integrator=integrator)
     steps = (17, 40) if integrator == "rk4" else (37, 120)

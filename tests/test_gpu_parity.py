@@ -42,14 +42,16 @@ def test_fp64_bitwise_vs_reference(case, layout):
         assert eng.degenerate_springs == int(d[f"deg_{c}"])
 
 
+@pytest.mark.parametrize("fmt,kernel", [("0", 5), ("explicit", 0)])
 @pytest.mark.parametrize("case", golden_cases())
-def test_fp64_explicit_tile_format_bitwise(case, monkeypatch):
-    """The explicit fp64 tile format (the fallback for tiles with more than
-    64 distinct (k, l0, group) records; SS_TILE_DICT=0 forces it) is bitwise
-    equal to the reference too."""
-    monkeypatch.setenv("SS_TILE_DICT", "0")
+def test_fp64_general_tile_formats_bitwise(case, fmt, kernel, monkeypatch):
+    """The fp64 formats for graphs whose tiles do not fit the 64-entry
+    (k, l0, group) dictionary are bitwise equal to the reference too: the
+    inline format (the general-graph path; SS_TILE_DICT=0 forces it) and the
+    older explicit format (SS_TILE_DICT=explicit)."""
+    monkeypatch.setenv("SS_TILE_DICT", fmt)
     d, eng = run_engine(case, "tile")
-    assert eng.info()["tile_kernel"] == 0
+    assert eng.info()["tile_kernel"] == kernel
     done = 0
     for c in d["checkpoints"]:
         eng.step(int(c) - done)
@@ -70,36 +72,39 @@ def test_fp64_compact_format_is_the_default():
 
 @pytest.mark.parametrize("integrator", ["verlet", "euler", "rk4"])
 def test_fp64_compact_equals_explicit_on_a_crawler_batch(integrator, monkeypatch):
-    """Both fp64 tile formats on 48 jittered crawlers (2 actuation groups,
-    ground contact with friction): identical bits after 600 steps."""
+    """The three fp64 tile formats on 48 jittered crawlers (2 actuation
+    groups, ground contact with friction): identical bits after 600 steps."""
     from paper_2207_09334_b200 import crawler_scene, replicate
     batch = replicate(crawler_scene(), 48, jitter=1e-6, seed=3)
     runs = []
-    for fmt in ("1", "0"):
+    for fmt, kernel in (("1", 4), ("0", 5), ("explicit", 0)):
         monkeypatch.setenv("SS_TILE_DICT", fmt)
         eng = Engine(batch, integrator=integrator, precision="f64", layout="tile")
-        assert eng.info()["tile_kernel"] == (4 if fmt == "1" else 0)
+        assert eng.info()["tile_kernel"] == kernel
         eng.set_damping(1e-4)
         eng.step(600)
         runs.append((eng.x.copy(), eng.v.copy(), eng.degenerate_springs))
         eng.close()
-    assert runs[0][0].tobytes() == runs[1][0].tobytes()
-    assert runs[0][1].tobytes() == runs[1][1].tobytes()
-    assert runs[0][2] == runs[1][2]
+    for other in runs[1:]:
+        assert runs[0][0].tobytes() == other[0].tobytes()
+        assert runs[0][1].tobytes() == other[1].tobytes()
+        assert runs[0][2] == other[2]
 
 
 def test_fp64_compact_equals_explicit_on_a_multi_tile_cube(monkeypatch):
-    """An excited 13^3-cell cube (11 tiles with halos): identical bits."""
+    """An excited 13^3-cell cube (11 tiles with halos), all three formats:
+    identical bits."""
     scene = L.excite(L.block_scene(13), seed=5)
     runs = []
-    for fmt in ("1", "0"):
+    for fmt in ("1", "0", "explicit"):
         monkeypatch.setenv("SS_TILE_DICT", fmt)
         eng = Engine(scene, integrator="verlet", precision="f64", layout="tile")
         eng.step(300)
         runs.append((eng.x.copy(), eng.v.copy()))
         eng.close()
-    assert runs[0][0].tobytes() == runs[1][0].tobytes()
-    assert runs[0][1].tobytes() == runs[1][1].tobytes()
+    for other in runs[1:]:
+        assert runs[0][0].tobytes() == other[0].tobytes()
+        assert runs[0][1].tobytes() == other[1].tobytes()
 
 
 @pytest.mark.parametrize("layout", ["csr", "ell", "tile"])

@@ -149,8 +149,9 @@ def test_tile_plan_statistics_on_host():
 def test_fp64_compact_tile_plan_on_host(monkeypatch):
     """fp64 tiles use the compact format (spring-id ordered incidence lists
     over a per-tile (k, l0, group) dictionary) when every tile has at most 64
-    distinct records; a tile with more falls back to the explicit format, and
-    SS_TILE_DICT=0 forces it."""
+    distinct records; a tile with more falls back to the inline format ((k,
+    l0) per incidence), which SS_TILE_DICT=0 forces; SS_TILE_DICT=explicit
+    forces the older explicit format."""
     from paper_2207_09334_b200.engine import plan
     cube = L.block_scene(15)
     info = plan(cube, precision="f64")
@@ -159,8 +160,12 @@ def test_fp64_compact_tile_plan_on_host(monkeypatch):
     assert info["smem_per_block"] <= 56 * 1024          # 4 CTAs per SM
     rnd = L.block_scene(15)
     rnd.k = rnd.k * (1.0 + 1e-6 * np.arange(rnd.k.size))    # every spring distinct
-    assert plan(rnd, precision="f64")["tile_kernel"] == 0
+    inl = plan(rnd, precision="f64")
+    assert inl["tile_kernel"] == 5
+    assert inl["tile_blob_bytes"] >= 16 * 2 * rnd.spring_count      # (k, l0) at both endpoints
     monkeypatch.setenv("SS_TILE_DICT", "0")
+    assert plan(cube, precision="f64")["tile_kernel"] == 5
+    monkeypatch.setenv("SS_TILE_DICT", "explicit")
     assert plan(cube, precision="f64")["tile_kernel"] == 0
 
 
