@@ -671,7 +671,8 @@ int launch_steps(ss_engine *h, int64_t count) {
         p.scale = G ? scale : nullptr;
         const bool euler = h->integrator == SS_EULER;
         auto *k = h->res_g == 8 ? (euler ? resident_kernel<F32, 0, 8> : resident_kernel<F32, 1, 8>)
-                                : (euler ? resident_kernel<F32, 0, 4> : resident_kernel<F32, 1, 4>);
+                : h->res_g == 4 ? (euler ? resident_kernel<F32, 0, 4> : resident_kernel<F32, 1, 4>)
+                                : (euler ? resident_kernel<F32, 0, 1> : resident_kernel<F32, 1, 1>);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)h->res_ctas);
         cfg.blockDim = dim3((unsigned)h->res_threads);
@@ -1066,9 +1067,12 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
             if (h->src_of(i) >= 0) used = i + 1;
     }
     h->res_g = used * 8 <= 1024 ? 8 : 4;
+    if (!F32)
+        if (const char *e = getenv("SS_RESIDENT_G")) h->res_g = atoi(e) == 1 ? 1 : h->res_g;   // A/B
     h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
     for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
-                           (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>}) {
+                           (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>,
+                           (const void *)resident_kernel<F32, 0, 1>, (const void *)resident_kernel<F32, 1, 1>}) {
         // per-function attributes are shared by every engine in the process:
         // grant the device maximum, never this engine's size
         cudaFuncAttributes fa{};
@@ -1089,8 +1093,9 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int clusters = 0;
-        const void *fn = h->integrator == SS_EULER ? (const void *)resident_kernel<F32, 0, 4>
-                                                   : (const void *)resident_kernel<F32, 1, 4>;
+        const bool e0 = h->integrator == SS_EULER;
+        const void *fn = h->res_g == 1 ? (e0 ? (const void *)resident_kernel<F32, 0, 1> : (const void *)resident_kernel<F32, 1, 1>)
+                                       : (e0 ? (const void *)resident_kernel<F32, 0, 4> : (const void *)resident_kernel<F32, 1, 4>);
         if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess || clusters < 1) {
             cudaGetLastError();
             h->res_image = nullptr;                                  // (freed with the engine)

@@ -25,6 +25,7 @@
 
 #include "kernels.cuh"
 #include "tile_f32.cuh"
+#include "tile_f64.cuh"
 
 namespace ss {
 
@@ -134,6 +135,75 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
             s.y = s.y + __shfl_down_sync(gmask, s.y, w, G);
             s.z = s.z + __shfl_down_sync(gmask, s.z, w, G);
         }
+    } else if constexpr (G == 1) {
+        // fp64, one lane per mass: the list in order, two incidences in
+        // flight through tile_f64.cuh's branch-free IEEE fast paths; any
+        // incidence outside them (or degenerate) redoes the mass with the
+        // library operators, exactly as tile_f64_kernel does
+        const double2 *dict = reinterpret_cast<const double2 *>(smem + a.off_dict);
+        const int *dg = reinterpret_cast<const int *>(smem + a.off_grp);
+        auto term = [&](uint32_t e, double &c, double &dx, double &dy, double &dz) -> bool {
+            const double2 kl = dict[e >> 13];
+            double l0 = kl.y;
+            if (scale) {
+                const int g = dg[e >> 13];
+                if (g >= 0) l0 = l0 * scale[g];
+            }
+            const double4 xo = xs[e & 0xfffu];
+            dx = xo.x - x4.x;
+            dy = xo.y - x4.y;
+            dz = xo.z - x4.z;
+            bool ok_s, ok_d;
+            const double len = sqrt_rn_fast((dx * dx + dy * dy) + dz * dz, ok_s);
+            const double num = kl.x * (len - l0);
+            c = div_rn_fast(num, len, ok_d);          // (a zero quotient's sign cannot reach the sum, tile_f64.cuh)
+            const bool zero = (__double2hiint(num) & 0x7fffffff) == 0 && __double2loint(num) == 0;
+            return ok_s && (ok_d || zero) && __double2hiint(len) > kDegenerateHi;
+        };
+        bool ok = true;
+        int q = 0;
+        for (; q + 2 <= n; q += 2) {
+            double c0, x0, y0, z0, c1, x1, y1, z1;
+            ok &= term(inc[q0 + q], c0, x0, y0, z0);
+            ok &= term(inc[q0 + q + 1], c1, x1, y1, z1);
+            s.x = s.x + c0 * x0;
+            s.y = s.y + c0 * y0;
+            s.z = s.z + c0 * z0;
+            s.x = s.x + c1 * x1;
+            s.y = s.y + c1 * y1;
+            s.z = s.z + c1 * z1;
+        }
+        if (q < n) {
+            double c0, x0, y0, z0;
+            ok &= term(inc[q0 + q], c0, x0, y0, z0);
+            s.x = s.x + c0 * x0;
+            s.y = s.y + c0 * y0;
+            s.z = s.z + c0 * z0;
+        }
+        if (!ok) {                                              // the exact loop (_kernels.py:51-70)
+            s = {0.0, 0.0, 0.0};
+            for (q = 0; q < n; ++q) {
+                const uint32_t e = inc[q0 + q];
+                const double2 kl = dict[e >> 13];
+                double l0 = kl.y;
+                if (scale) {
+                    const int g = dg[e >> 13];
+                    if (g >= 0) l0 = l0 * scale[g];
+                }
+                const double4 xo = xs[e & 0xfffu];
+                const double dx = xo.x - x4.x, dy = xo.y - x4.y, dz = xo.z - x4.z;
+                const double len = sqrt((dx * dx + dy * dy) + dz * dz);
+                if (len < 1e-12) {
+                    if (e & 0x1000u) ++deg;
+                    continue;
+                }
+                const double c = spring_c64(kl.x, len, l0);
+                s.x = s.x + c * dx;
+                s.y = s.y + c * dy;
+                s.z = s.z + c * dz;
+            }
+        }
+        return s;
     } else {
         const double2 *dict = reinterpret_cast<const double2 *>(smem + a.off_dict);
         const int *dg = reinterpret_cast<const int *>(smem + a.off_grp);
@@ -184,7 +254,8 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
 
 // INTEG: 0 Euler, 1 Verlet.  G lanes per mass slot: slot m = tid / G.
 template <bool F32, int INTEG, int G>
-__global__ void __launch_bounds__(1024, 1) resident_kernel(Params<typename Prec<F32>::T> p, ResidentArgs a) {
+__global__ void __launch_bounds__(G == 1 ? 256 : 1024, 1) resident_kernel(Params<typename Prec<F32>::T> p,
+                                                                        ResidentArgs a) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
     namespace cg = cooperative_groups;
