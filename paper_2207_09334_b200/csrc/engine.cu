@@ -914,11 +914,10 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     if (h->integrator == SS_RK4 || n_ctas > kResidentMaxCtas || (F32 && !h->rx0) ||
         h->groups.size() > (size_t)kResidentMaxGroups)
         return SS_OK;
-    // fp32: clusters of up to kResidentMaxCtas CTAs (measured faster than a
-    // launch per step); fp64: one CTA only (its multi-CTA cluster was slower)
-    int max_ctas = F32 ? kResidentMaxCtas : 1;
-    if (!F32)
-        if (const char *e = getenv("SS_RESIDENT_F64")) max_ctas = std::min(kResidentMaxCtas, atoi(e));   // A/B
+    // clusters of up to kResidentMaxCtas CTAs, one tile each (measured
+    // faster than a launch per step: fp32 beam 4.80 -> 3.67 us, fp64 with one
+    // lane per mass 6.73 -> 6.39 us, 64 fp64 walkers 5.85 -> 4.89 us)
+    int max_ctas = kResidentMaxCtas;
     if (const char *e = getenv("SS_RESIDENT")) max_ctas = std::min(max_ctas, atoi(e));  // 0: off
     if (n_ctas > max_ctas) return SS_OK;
     std::vector<int64_t> dev(h->N);
@@ -1066,9 +1065,16 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
         for (int64_t i = 0; i < ND; ++i)
             if (h->src_of(i) >= 0) used = i + 1;
     }
-    h->res_g = used * 8 <= 1024 ? 8 : 4;
-    if (!F32)
-        if (const char *e = getenv("SS_RESIDENT_G")) h->res_g = atoi(e) == 1 ? 1 : h->res_g;   // A/B
+    // lanes per mass: fp32 4-8 lanes add partial sums in a fixed tree; fp64
+    // adds in list order, where 4 lanes cost more in shuffles than they
+    // save, so full tiles (and clusters) take one lane per mass with the
+    // branch-free IEEE sequences (crawler x12: 5.72 -> 3.24 us), small
+    // scenes 8 lanes (crawler 2.5 us against 3.0 with one)
+    h->res_g = used * 8 <= 1024 ? 8 : (F32 ? 4 : 1);
+    if (const char *e = getenv("SS_RESIDENT_G")) {                 // A/B: 1, 4 or 8
+        const int g = atoi(e);
+        if ((g == 1 || g == 4 || g == 8) && used * g <= 1024) h->res_g = g;
+    }
     h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
     for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
                            (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>,

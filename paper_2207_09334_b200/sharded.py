@@ -365,8 +365,10 @@ def bench_slabs(cells: int, precision: str, steps: int, warmup: int, sub: int, l
     if dist is not None:
         dist.barrier()
     launches = eng.launch_count - launches0
-    # e2e through the public API: host state in, positions out (per rank, max over ranks)
-    x_h, v_h, xp_h = eng.x.copy(), eng.v.copy(), eng.x_prev.copy()
+    # e2e through the public API: host state in (page-locked arrays up to
+    # 1 GiB each, as the N=1 line), positions out (per rank, max over ranks)
+    pin = eng.mass_count * 24 <= 1 << 30
+    x_h, v_h, xp_h = ((_lib.pinned_copy(a) if pin else a.copy()) for a in (eng.x, eng.v, eng.x_prev))
     e2e_steps = 2
     if dist is not None:
         dist.barrier()
@@ -379,12 +381,12 @@ def bench_slabs(cells: int, precision: str, steps: int, warmup: int, sub: int, l
         _ = eng.x
     ew = float(reduce_max(time.perf_counter() - w0))
     n_local = slab.scene.mass_count
-    vec = 16 if precision == "f32" else 32
+    vec = 24                                # the caller's (N, 3) f64 arrays
     out = {"cells": cells, "springs": slab.springs_global, "masses": n_masses, "ms": ms, "steps": steps,
            "substeps": sub, "launches": launches, "e2e_wall_s": ew, "e2e_steps": e2e_steps,
            "h2d_bytes_per_step": 3 * n_local * vec * world, "d2h_bytes_per_step": n_local * vec * world,
            "transport": transport, "build_s": build_s, "tile_kernel": info["tile_kernel"],
-           "layout": info["layout"], "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * vec,
+           "layout": info["layout"], "halo_plane_bytes": int(slab.send_hi.shape[0] or slab.send_lo.shape[0]) * (16 if precision == "f32" else 32),
            "records_bytes": info["tile_blob_bytes"]}
     eng.close()
     return out

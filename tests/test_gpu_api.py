@@ -451,6 +451,39 @@ def test_cluster_resident_fp32_matches_per_step_launches(monkeypatch):
     assert got["8"][1:] == got["0"][1:]
 
 
+@pytest.mark.parametrize("integrator", ["verlet", "euler"])
+def test_cluster_resident_fp64_is_bitwise_the_launches(integrator, monkeypatch):
+    """fp64 scenes of 2-16 tiles run one thread-block cluster, one lane per
+    mass adding in list order (resident.cuh): bitwise the per-step launches
+    of tile_f64_kernel and the reference's order, including the divergence
+    step and mass, and the 4/8-lane variants."""
+    from paper_2207_09334_b200 import crawler_scene, lattice as L, replicate
+    for scene in (L.beam_lattice(length=4.0), replicate(crawler_scene(), 64, jitter=1e-6, seed=4)):
+        out = {}
+        for res, g in (("16", ""), ("0", ""), ("16", "4")):
+            monkeypatch.setenv("SS_RESIDENT", res)
+            monkeypatch.setenv("SS_RESIDENT_G", g)
+            eng = Engine(scene, integrator=integrator, precision="f64")
+            eng.set_damping(1e-4)
+            eng.step(3)
+            eng.step(1500)
+            out[res, g] = (eng.x.tobytes(), eng.v.tobytes(), eng.n)
+            eng.close()
+        assert out["16", ""] == out["0", ""] == out["16", "4"]
+    monkeypatch.setenv("SS_RESIDENT_G", "")
+    blown = L.excite(L.block_scene(9), seed=11)
+    blown.dt = 0.05
+    got = {}
+    for res in ("16", "0"):
+        monkeypatch.setenv("SS_RESIDENT", res)
+        eng = Engine(blown, integrator=integrator, precision="f64")
+        with pytest.raises(DivergenceError) as err:
+            eng.step(10000)
+        got[res] = (err.value.mass_id, err.value.step, eng.n, eng.x.tobytes())
+        eng.close()
+    assert got["16"] == got["0"]
+
+
 def test_command_posted_mid_batch_lands_within_the_batch():
     """The reference drains the command queue before every step
     (engine.py:366-370).  A command posted by another thread while one long
