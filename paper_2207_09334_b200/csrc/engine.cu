@@ -1066,11 +1066,11 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
             if (h->src_of(i) >= 0) used = i + 1;
     }
     // lanes per mass: fp32 4-8 lanes add partial sums in a fixed tree; fp64
-    // adds in list order, where 4 lanes cost more in shuffles than they
-    // save, so full tiles (and clusters) take one lane per mass with the
-    // branch-free IEEE sequences (crawler x12: 5.72 -> 3.24 us), small
-    // scenes 8 lanes (crawler 2.5 us against 3.0 with one)
-    h->res_g = used * 8 <= 1024 ? 8 : (F32 ? 4 : 1);
+    // adds in list order, where lanes cost more in shuffles than they save:
+    // one lane per mass, four incidences in flight through the branch-free
+    // IEEE sequences (crawler 2.50 -> 2.14 us, 12 crawlers 5.72 -> 2.68, the
+    // 40x4x4 beam as a cluster 5.08 against 6.71 with launches)
+    h->res_g = F32 ? (used * 8 <= 1024 ? 8 : 4) : 1;
     if (const char *e = getenv("SS_RESIDENT_G")) {                 // A/B: 1, 4 or 8
         const int g = atoi(e);
         if ((g == 1 || g == 4 || g == 8) && used * g <= 1024) h->res_g = g;

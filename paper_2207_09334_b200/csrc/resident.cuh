@@ -160,20 +160,23 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
             const bool zero = (__double2hiint(num) & 0x7fffffff) == 0 && __double2loint(num) == 0;
             return ok_s && (ok_d || zero) && __double2hiint(len) > kDegenerateHi;
         };
+        // kFly incidences in flight: a lone CTA per SM has the registers, and
+        // the step's latency is this one lane's chain over its list
+        constexpr int kFly = 4;
         bool ok = true;
         int q = 0;
-        for (; q + 2 <= n; q += 2) {
-            double c0, x0, y0, z0, c1, x1, y1, z1;
-            ok &= term(inc[q0 + q], c0, x0, y0, z0);
-            ok &= term(inc[q0 + q + 1], c1, x1, y1, z1);
-            s.x = s.x + c0 * x0;
-            s.y = s.y + c0 * y0;
-            s.z = s.z + c0 * z0;
-            s.x = s.x + c1 * x1;
-            s.y = s.y + c1 * y1;
-            s.z = s.z + c1 * z1;
+        for (; q + kFly <= n; q += kFly) {
+            double c[kFly], dx[kFly], dy[kFly], dz[kFly];
+#pragma unroll
+            for (int u = 0; u < kFly; ++u) ok &= term(inc[q0 + q + u], c[u], dx[u], dy[u], dz[u]);
+#pragma unroll
+            for (int u = 0; u < kFly; ++u) {
+                s.x = s.x + c[u] * dx[u];
+                s.y = s.y + c[u] * dy[u];
+                s.z = s.z + c[u] * dz[u];
+            }
         }
-        if (q < n) {
+        for (; q < n; ++q) {
             double c0, x0, y0, z0;
             ok &= term(inc[q0 + q], c0, x0, y0, z0);
             s.x = s.x + c0 * x0;
