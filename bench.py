@@ -259,8 +259,8 @@ def kernel_of(info: dict) -> tuple[str, str]:
     fp32 = info["precision"] == 1
     tk = info["tile_kernel"]
     if fp32:
-        return ("tile_compact", "tile_lean_kernel") if tk == 2 else \
-               ("tile_explicit", "tile_lean_kernel" if tk == 1 else "step_kernel")
+        return {2: ("tile_compact", "tile_lean_kernel"), 6: ("tile_inline", "tile_lean_kernel"),
+                1: ("tile_explicit", "tile_lean_kernel")}.get(tk, ("tile_explicit", "step_kernel"))
     return {5: ("tile_inline", "tile_f64_kernel"), 4: ("tile_compact", "tile_f64_kernel"),
             3: ("tile_compact", "step_kernel")}.get(tk, ("tile_explicit", "step_kernel"))
 
@@ -490,9 +490,9 @@ def run_single(args):
         line["general_graph_format"] = {
             "value": general["value"], "unit": UNIT, "ms_per_step": general["ms_per_step"],
             "dtype": general["dtype"], "roofline": general["roofline"],
-            "note": "SS_TILE_DICT=0: the general-graph record format (fp64: (k, l0) per incidence "
-                    "streamed from HBM; fp32: explicit per-spring records) -- what a scene whose tiles "
-                    "do not fit the 64-entry dictionary runs -- on the same cube"}
+            "note": "SS_TILE_DICT=0: the general-graph record format (records per incidence streamed "
+                    "from HBM: fp64 (k, l0), fp32 (k, k*l0, D)) -- what a scene whose tiles do not fit "
+                    "the 64-entry dictionary runs -- on the same cube"}
     if scaling:
         line["scaling_1gpu"] = scaling
     print(json.dumps(line), flush=True)

@@ -130,6 +130,8 @@ struct ss_engine {
     int2 *inc = nullptr;
     unsigned char *d_blob = nullptr;
     double2 *d_kl_inline = nullptr;            // fp64 inline tile format (tiles.h)
+    float4 *d_kd_inline = nullptr;             // fp32 inline tile format
+    float *d_dz_inline = nullptr;
     int8_t *d_g_inline = nullptr;
     unsigned long long *d_kl_off = nullptr;
     unsigned long long *d_toff = nullptr;
@@ -445,6 +447,8 @@ Params<T> base_params(const ss_engine *h) {
     tp.kl_inline = h->d_kl_inline;
     tp.g_inline = h->d_g_inline;
     tp.kl_off = h->d_kl_off;
+    tp.kd_inline = h->d_kd_inline;
+    tp.dz_inline = h->d_dz_inline;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -563,6 +567,17 @@ template <bool GROUPS>
 void launch_rk4_lean(ss_engine *h, const Params<float> &p, int grid, int stage) {
     const bool two = h->lean_lanes == 2;
     void (*k)(Params<float>) = nullptr;
+    if (h->tl.inline_kl) {
+        switch (stage) {
+            case 1: k = tile_lean_kernel<2, GROUPS, 6, 1, false, true>; break;
+            case 2: k = tile_lean_kernel<3, GROUPS, 6, 1, false, true>; break;
+            case 3: k = tile_lean_kernel<4, GROUPS, 6, 1, false, true>; break;
+            default: k = tile_lean_kernel<5, GROUPS, 6, 1, false, true>; break;
+        }
+        if (h->pdl) launch_pdl(k, grid, kTile, h->lean_smem, h->stream, p);
+        else k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+        return;
+    }
     switch (stage) {
         case 1: k = two ? tile_lean_kernel<2, GROUPS, 6, 2> : tile_lean_kernel<2, GROUPS>; break;
         case 2: k = two ? tile_lean_kernel<3, GROUPS, 6, 2> : tile_lean_kernel<3, GROUPS>; break;
@@ -576,6 +591,16 @@ void launch_rk4_lean(ss_engine *h, const Params<float> &p, int grid, int stage) 
 
 template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
+    const bool euler = h->integrator == SS_EULER;
+    if (h->tl.inline_kl) {                                 // general graphs: records streamed per incidence
+        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, 6, 1, true, true>
+                                      : tile_lean_kernel<1, GROUPS, 6, 1, true, true>)
+                             : (euler ? tile_lean_kernel<0, GROUPS, 6, 1, false, true>
+                                      : tile_lean_kernel<1, GROUPS, 6, 1, false, true>);
+        if (h->pdl) launch_pdl(ki, grid, kTile, h->lean_smem, h->stream, p);
+        else ki<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+        return;
+    }
     auto *k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS> : tile_lean_kernel<1, GROUPS>;
     if (h->lean_lanes == 2)
         k = h->integrator == SS_EULER ? tile_lean_kernel<0, GROUPS, 6, 2> : tile_lean_kernel<1, GROUPS, 6, 2>;
@@ -1207,9 +1232,16 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         h->d_toff = reinterpret_cast<unsigned long long *>(p);
         if ((rc = up_vec(h, &p, L.split))) return rc;
         h->d_tsplit = reinterpret_cast<unsigned int *>(p);
-        if (L.inline_kl) {                        // fp64 general-graph format: records streamed, not staged
-            if ((rc = up_vec(h, &p, L.kl_inline))) return rc;
-            h->d_kl_inline = reinterpret_cast<double2 *>(p);
+        if (L.inline_kl) {                        // general-graph format: records streamed, not staged
+            if (F32) {
+                if ((rc = up_vec(h, &p, L.kd_inline))) return rc;
+                h->d_kd_inline = reinterpret_cast<float4 *>(p);
+                if ((rc = up_vec(h, &p, L.dz_inline))) return rc;
+                h->d_dz_inline = reinterpret_cast<float *>(p);
+            } else {
+                if ((rc = up_vec(h, &p, L.kl_inline))) return rc;
+                h->d_kl_inline = reinterpret_cast<double2 *>(p);
+            }
             if (!L.g_inline.empty()) {
                 if ((rc = up_vec(h, &p, L.g_inline))) return rc;
                 h->d_g_inline = reinterpret_cast<int8_t *>(p);
@@ -1242,7 +1274,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                 // 512-thread CTAs, twice the warps for the same tiles
                 int sms = 0;
                 CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                h->lean_lanes = L.n_tiles <= 3 * (int64_t)sms ? 2 : 1;
+                h->lean_lanes = L.n_tiles <= 3 * (int64_t)sms && !L.inline_kl ? 2 : 1;
                 if (const char *e = getenv("SS_LEAN_LANES")) h->lean_lanes = atoi(e) == 2 ? 2 : 1;
                 if (h->lean_lanes == 2) {
                     h->lean_smem += (size_t)kTile * sizeof(float4);        // lane 1's partial sums
@@ -1264,7 +1296,15 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_lean_kernel<3, false, 6, 2>, tile_lean_kernel<4, false, 6, 2>,
                                  tile_lean_kernel<5, false, 6, 2>, tile_lean_kernel<2, true, 6, 2>,
                                  tile_lean_kernel<3, true, 6, 2>, tile_lean_kernel<4, true, 6, 2>,
-                                 tile_lean_kernel<5, true, 6, 2>})
+                                 tile_lean_kernel<5, true, 6, 2>, tile_lean_kernel<0, false, 6, 1, false, true>,
+                                 tile_lean_kernel<1, false, 6, 1, false, true>, tile_lean_kernel<0, true, 6, 1, false, true>,
+                                 tile_lean_kernel<1, true, 6, 1, false, true>, tile_lean_kernel<0, false, 6, 1, true, true>,
+                                 tile_lean_kernel<1, false, 6, 1, true, true>, tile_lean_kernel<0, true, 6, 1, true, true>,
+                                 tile_lean_kernel<1, true, 6, 1, true, true>, tile_lean_kernel<2, false, 6, 1, false, true>,
+                                 tile_lean_kernel<3, false, 6, 1, false, true>, tile_lean_kernel<4, false, 6, 1, false, true>,
+                                 tile_lean_kernel<5, false, 6, 1, false, true>, tile_lean_kernel<2, true, 6, 1, false, true>,
+                                 tile_lean_kernel<3, true, 6, 1, false, true>, tile_lean_kernel<4, true, 6, 1, false, true>,
+                                 tile_lean_kernel<5, true, 6, 1, false, true>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
@@ -2558,11 +2598,12 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->ell_width_ref = h->tl.max_Wr;
         info->canonical_order = h->tl.canonical ? 1 : 0;
         info->tile_count = h->tl.n_tiles;
-        info->tile_blob_bytes = (int64_t)(h->tl.blob.size() + 8 * h->tl.kl_inline.size() + h->tl.g_inline.size());
+        info->tile_blob_bytes = (int64_t)(h->tl.blob.size() + 8 * h->tl.kl_inline.size() + h->tl.g_inline.size() +
+                                          4 * (h->tl.kd_inline.size() + h->tl.dz_inline.size()));
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
-        info->tile_kernel = h->lean_smem ? (h->tl.compact ? 2 : 1)
+        info->tile_kernel = h->lean_smem ? (h->tl.inline_kl ? 6 : h->tl.compact ? 2 : 1)
                           : h->f64_smem ? (h->tl.inline_kl ? 5 : 4)
                                         : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
         info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->f64_smem ? h->f64_smem : h->smem_bytes);
@@ -2601,7 +2642,8 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     info->ell_width_ref = tl.max_Wr;
     info->canonical_order = tl.canonical ? 1 : 0;
     info->tile_count = tl.n_tiles;
-    info->tile_blob_bytes = (int64_t)(tl.blob.size() + 8 * tl.kl_inline.size() + tl.g_inline.size());
+    info->tile_blob_bytes = (int64_t)(tl.blob.size() + 8 * tl.kl_inline.size() + tl.g_inline.size() +
+                                      4 * (tl.kd_inline.size() + tl.dz_inline.size()));
     info->tile_halo_ratio = tl.halo_ratio;
     info->tile_foreign_frac = tl.foreign_frac;
     const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
@@ -2610,7 +2652,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     info->kernel_smem = info->smem_per_block;
-    info->tile_kernel = f32 ? (tl.compact ? 2 : 1) : (tl.inline_kl ? 5 : tl.compact ? 3 : 0);
+    info->tile_kernel = f32 ? (tl.inline_kl ? 6 : tl.compact ? 2 : 1) : (tl.inline_kl ? 5 : tl.compact ? 3 : 0);
     return SS_OK;
 }
 

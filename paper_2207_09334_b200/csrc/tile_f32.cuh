@@ -179,25 +179,56 @@ __device__ __forceinline__ void acc3(V3<float> &s, float c, float dx, float dy, 
 // LANES > 1: this thread takes incidences lane, lane + LANES, ... and the
 // caller combines the lanes' sums; dmin_out gets the smallest d^2 seen (the
 // degenerate recount, by lane 0, covers all own springs).
-template <bool GROUPS, int LANES = 1>
+// (k, k*l0, Dx, Dy), Dz and group of incidence q (entry e): the tile's
+// dictionary, or (INLINE, general graphs) this mass's column of the inline
+// records in global memory (tiles.h), streamed.
+template <bool INLINE>
+struct F32Rec {
+    const float4 *dict;          // dictionary (2 float4 per entry), or the inline (k, k*l0, Dx, Dy) + column
+    const float *dz;             // inline Dz + column
+    const int8_t *g;             // inline groups + column (null: none)
+    __device__ __forceinline__ void get(uint32_t e, int q, float4 &kd, float &dz_, int &grp) const {
+        if constexpr (INLINE) {
+            kd = __ldcs(dict + (q << 8));
+            dz_ = __ldcs(dz + (q << 8));
+            grp = g ? g[q << 8] : -1;
+        } else {
+            const float4 *ent = dict + 2 * (e >> 10);
+            kd = ent[0];
+            const float4 ez = ent[1];                       // (Dz, group bits, -, -)
+            dz_ = ez.x;
+            grp = __float_as_int(ez.y);
+        }
+    }
+};
+
+template <bool GROUPS, int LANES = 1, bool INLINE = false>
 __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const TileView &v, int l, const float4 &rm,
                                                   int n_own, int n_inc, V3<float> &s, int lane = 0,
-                                                  float *dmin_out = nullptr) {
+                                                  float *dmin_out = nullptr, int tile = 0) {
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(v.bl + v.h->off_oo) + l;
-    const float4 *dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);   // 2 float4 per entry
+    F32Rec<INLINE> rec;
+    if constexpr (INLINE) {
+        const unsigned long long b0 = p.topo.kl_off[tile] + (unsigned long long)l;
+        rec.dict = p.topo.kd_inline + b0;
+        rec.dz = p.topo.dz_inline + b0;
+        rec.g = p.topo.g_inline ? p.topo.g_inline + b0 : nullptr;
+    } else {
+        rec.dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);
+    }
     float dmin = INFINITY;
     auto body = [&](int q) {
         const uint32_t e = inc[q << 8];
-        const float4 *ent = dict + 2 * (e >> 10);
-        const float4 kd = ent[0];                           // (k, k*l0, Dx, Dy)
-        const float4 ez = ent[1];                           // (Dz, group bits, -, -)
+        float4 kd;                                          // (k, k*l0, Dx, Dy)
+        float dzr;
+        int g;
+        rec.get(e, q, kd, dzr, g);
         float kl0 = kd.y;
         if constexpr (GROUPS) {
-            const int g = __float_as_int(ez.y);
             if (g >= 0) kl0 = kl0 * p.scale[g];
         }
         const float4 ro = v.sY[e & 0x3ffu];
-        const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = ez.x + (ro.z - rm.z);
+        const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = dzr + (ro.z - rm.z);
         float d2;
         const float c = spring_c(dx, dy, dz_, kd.x, kl0, d2);
         dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
@@ -221,10 +252,12 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
     if (dmin < 1e-24f) {                                    // rare: count the degenerate own springs
         for (int r = 0; r < n_own; ++r) {
             const uint32_t e = inc[r << 8];
-            const float4 *ent = dict + 2 * (e >> 10);
-            const float4 kd = ent[0], ez = ent[1];
+            float4 kd;
+            float dzr;
+            int g;
+            rec.get(e, r, kd, dzr, g);
             const float4 ro = v.sY[e & 0x3ffu];
-            const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = ez.x + (ro.z - rm.z);
+            const float dx = kd.z + (ro.x - rm.x), dy = kd.w + (ro.y - rm.y), dz_ = dzr + (ro.z - rm.z);
             const float d2 = __fmaf_rn(dz_, dz_, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
             deg += d2 < 1e-24f ? 1u : 0u;
         }
@@ -269,8 +302,9 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
 // mass l = t mod 256 with lane t / 256 taking every other incidence, and the
 // lanes' sums meet in shared memory in a fixed order -- twice the warps for
 // the same tiles, for scenes too small to fill the GPU.
-template <int INTEG, bool GROUPS, int LANES = 1, bool ORDERED = false>
+template <int INTEG, bool GROUPS, int LANES = 1, bool ORDERED = false, bool INLINE = false>
 __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char *smem) {
+    static_assert(!(INLINE && LANES > 1), "inline records step with one lane per mass");
     const Topology<float> &t = p.topo;
     const int tid = threadIdx.x;
     const int l = tid % kTile, lane = tid / kTile;
@@ -348,7 +382,8 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         if (!active) return;
         if (p.debug != 1) {
             const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
-            flush_degenerate(p.degenerate, incidence_sum<GROUPS>(p, v, l, x4, cnt & 0xff, cnt >> 8, s));
+            flush_degenerate(p.degenerate,
+                             incidence_sum<GROUPS, 1, INLINE>(p, v, l, x4, cnt & 0xff, cnt >> 8, s, 0, nullptr, tile));
         }
     } else {
         // lane 1's partial sums (and its smallest d^2) meet lane 0's in shared
@@ -376,11 +411,11 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev, tile);
 }
 
-template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1, bool ORDERED = false>
+template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1, bool ORDERED = false, bool INLINE = false>
 __global__ void __launch_bounds__(kTile * LANES, LANES == 1 ? MINB : 3) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    lean_body<INTEG, GROUPS, LANES, ORDERED>(p, smem);
+    lean_body<INTEG, GROUPS, LANES, ORDERED, INLINE>(p, smem);
     xchg_finish(p, lean_tile<ORDERED>(p));
 }
 

@@ -53,7 +53,12 @@ constexpr int SS_EAGAIN_SHAPE = -1001; // internal: a tile's degree or halo (or 
 //    n_inc); dictionary of 32-byte entries at off_okl: float4 (k, k*l0, Dx,
 //    Dy), float4 (Dz, group as int32 bits (-1 passive), 0, 0); int8 groups
 //    also at off_og.  2 B per incidence, 4 B per spring.
-//  * explicit (canonical bit 1 clear): counts = n_own | n_ref << 8; own
+//  * inline (canonical bits 1|2|4; the fp32 general-graph format when a tile
+//    has more than 64 distinct records, or with SS_TILE_DICT=0): the compact
+//    incidence lists with partner slots only, and each incidence's (k, k*l0,
+//    Dx, Dy) float4, Dz float and int8 group in TileLayout::kd_inline /
+//    dz_inline / g_inline at kl_off[tile] + q*256 + l, streamed from HBM.
+//  * explicit (canonical bit 1 clear; SS_TILE_DICT=explicit): counts = n_own | n_ref << 8; own
 //    records (other u16 off_oo, then planar k, k*l0, Dx, Dy, Dz [W*256 each]
 //    at off_okl, grp i8 off_og); a spring whose owner lies in another tile is
 //    copied into the partner's tile (owner u16 off_fo, partner u8 off_fl,
@@ -116,7 +121,9 @@ struct TileLayout {
     bool inline_kl = false;         // fp64 inline format: (k, l0) per incidence in kl_inline
     std::vector<double> kl_inline;  // inline format: (k, l0) pairs, tile t at kl_off[t] pairs
     std::vector<int8_t> g_inline;   // inline format: group per incidence (empty: no groups)
-    std::vector<uint64_t> kl_off;   // inline format: n_tiles + 1 pair offsets
+    std::vector<uint64_t> kl_off;   // inline format: n_tiles + 1 slot offsets (W * 256 per tile)
+    std::vector<float> kd_inline;   // fp32 inline format: (k, k*l0, Dx, Dy) per incidence slot
+    std::vector<float> dz_inline;   // fp32 inline format: Dz per incidence slot
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };

@@ -40,7 +40,8 @@ void put_at(std::vector<uint8_t> &blob, uint32_t off, const T &v) {
 
 }  // namespace
 
-int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict);
+// mode: 0 explicit, 1 compact with the dictionary, 2 compact with inline records
+int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode);
 
 namespace {
 size_t own_total(const std::vector<std::vector<int32_t>> &own) {
@@ -50,19 +51,24 @@ size_t own_total(const std::vector<std::vector<int32_t>> &own) {
 }
 }  // namespace
 
-// Compact format when every tile has at most 64 distinct (k, k*l0, group)
-// records and at most 768 halo slots, the explicit format otherwise
-// (SS_TILE_DICT=0 forces it).
+// Compact format when every tile has at most 64 distinct (k, k*l0, group, D)
+// records and at most 768 halo slots; compact lists with inline records when
+// only the dictionary overflows (SS_TILE_DICT=0 forces it); the explicit
+// format otherwise (SS_TILE_DICT=explicit forces it).
 int build_tiles_f32(const TileInput &in, TileLayout &L) {
     const char *env = getenv("SS_TILE_DICT");
-    if (!env || atoi(env) != 0) {
-        const int rc = build_tiles_f32_fmt(in, L, true);
-        if (rc != SS_EAGAIN_DICT) return rc;
+    const bool explicit_only = env && std::strcmp(env, "explicit") == 0;
+    const bool inline_only = env && !explicit_only && atoi(env) == 0;
+    if (!explicit_only) {
+        int rc = inline_only ? SS_EAGAIN_DICT : build_tiles_f32_fmt(in, L, 1);
+        if (rc == SS_EAGAIN_DICT) rc = build_tiles_f32_fmt(in, L, 2);
+        if (rc != SS_EAGAIN_DICT && rc != SS_EAGAIN_SHAPE) return rc;
     }
-    return build_tiles_f32_fmt(in, L, false);
+    return build_tiles_f32_fmt(in, L, 0);
 }
 
-int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
+int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
+    const bool use_dict = mode != 0, inline_rec = mode == 2;
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
@@ -139,7 +145,9 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
     std::vector<uint32_t> tH(n_tiles), tHr(n_tiles), tSplit(n_tiles), tN(n_tiles), tW(n_tiles), tWr(n_tiles);
     std::vector<int64_t> tFor(n_tiles), tRefs(n_tiles);
     const bool has_g = in.group != nullptr;
-    int err = 0;
+    std::vector<std::vector<float>> tKD(inline_rec ? n_tiles : 0), tDZ(inline_rec ? n_tiles : 0);
+    std::vector<std::vector<int8_t>> tG(inline_rec && has_g ? n_tiles : 0);
+    int err = 0;        // 1 hard limit, 3 dictionary overflow, 4 compact shape overflow
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = 0; t < n_tiles; ++t) {
         if (err) continue;
@@ -247,12 +255,20 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 const int64_t m = L.orig_of[base + l];
                 for (const int32_t s : own[l]) inc[l].push_back(s);
                 for (int64_t r = ref_ptr[m]; r < ref_ptr[m + 1]; ++r) inc[l].push_back(ref_sp[r]);
-                for (const int32_t s : inc[l]) dict.emplace(key_of(s, m), 0u);
+                if (!inline_rec)
+                    for (const int32_t s : inc[l]) dict.emplace(key_of(s, m), 0u);
                 Wi = std::max(Wi, (int)inc[l].size());
             }
-            if (dict.size() > 64 || kTile + halo_ids.size() > 1024 || Wi > 255) {
+            if (kTile + halo_ids.size() > 1024 || Wi > 255) {
 #pragma omp atomic write
-                err = 3;
+                err = 4;                                       // the shape does not fit: explicit format
+                continue;
+            }
+            if (dict.size() > 64) {
+                if (err != 4) {
+#pragma omp atomic write
+                    err = 3;                                   // only the dictionary overflows: inline records
+                }
                 continue;
             }
             uint32_t di = 0;
@@ -260,7 +276,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
             const uint32_t D = (uint32_t)dict.size(), inc_n = (uint32_t)Wi << 8;
             TileHdr h{};
             h.n = n; h.W = Wi; h.Wr = 0; h.n_halo = (uint32_t)halo_ids.size(); h.n_foreign = 0;
-            h.canonical = 1 | 2;                               // bit 1: compact format
+            h.canonical = 1 | 2 | (inline_rec ? 4 : 0);       // bit 1: compact format; bit 2: inline records
             h.slice_log2 = 8;
             h.n_dict = D;
             uint32_t off = al16(sizeof(TileHdr));
@@ -286,6 +302,11 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 put_at<int32_t>(blob, h.off_okl + 32 * e + 20, (int32_t)std::get<2>(kv.first));
                 if (has_g) put_at<int8_t>(blob, h.off_og + e, (int8_t)std::get<2>(kv.first));
             }
+            if (inline_rec) {
+                tKD[t].assign((size_t)4 * inc_n, 0.f);
+                tDZ[t].assign((size_t)inc_n, 0.f);
+                if (has_g) tG[t].assign((size_t)inc_n, (int8_t)-1);
+            }
             int64_t n_inc = 0;
             for (int l = 0; l < n; ++l) {
                 const int64_t m = L.orig_of[base + l];
@@ -293,8 +314,21 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
                 for (size_t q = 0; q < inc[l].size(); ++q) {
                     const int32_t s = inc[l][q];
                     const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;   // the other endpoint
-                    const uint32_t v = (uint32_t)slot_of_local(L.new_of[o]) | (dict.at(key_of(s, m)) << 10);
-                    put_at<uint16_t>(blob, h.off_oo + 2 * (((uint32_t)q << 8) | (uint32_t)l), (uint16_t)v);
+                    const uint32_t at = ((uint32_t)q << 8) | (uint32_t)l;
+                    uint32_t di = 0;
+                    if (inline_rec) {
+                        const auto key = key_of(s, m);
+                        tKD[t][4 * at] = std::get<0>(key);
+                        tKD[t][4 * at + 1] = std::get<1>(key);
+                        tKD[t][4 * at + 2] = std::get<3>(key);
+                        tKD[t][4 * at + 3] = std::get<4>(key);
+                        tDZ[t][at] = std::get<5>(key);
+                        if (has_g) tG[t][at] = (int8_t)std::get<2>(key);
+                    } else {
+                        di = dict.at(key_of(s, m));
+                    }
+                    const uint32_t v = (uint32_t)slot_of_local(L.new_of[o]) | (di << 10);
+                    put_at<uint16_t>(blob, h.off_oo + 2 * at, (uint16_t)v);
                 }
                 n_inc += (int64_t)inc[l].size();
             }
@@ -375,8 +409,23 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, bool use_dict) {
         tRefs[t] = n_refs;
     }
     if (err == 1) return fail(SS_EINVAL, "tile exceeds layout limits (degree or halo too large)");
+    if (err == 4) return SS_EAGAIN_SHAPE;
     if (err == 3) return SS_EAGAIN_DICT;
     L.compact = use_dict;
+    L.inline_kl = inline_rec;
+    if (inline_rec) {
+        L.kl_off.assign(n_tiles + 1, 0);
+        for (int64_t t = 0; t < n_tiles; ++t) L.kl_off[t + 1] = L.kl_off[t] + tDZ[t].size();
+        L.kd_inline.resize(4 * L.kl_off[n_tiles]);
+        L.dz_inline.resize(L.kl_off[n_tiles]);
+        if (has_g) L.g_inline.resize(L.kl_off[n_tiles]);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < n_tiles; ++t) {
+            std::memcpy(L.kd_inline.data() + 4 * L.kl_off[t], tKD[t].data(), tKD[t].size() * 4);
+            std::memcpy(L.dz_inline.data() + L.kl_off[t], tDZ[t].data(), tDZ[t].size() * 4);
+            if (has_g) std::memcpy(L.g_inline.data() + L.kl_off[t], tG[t].data(), tG[t].size());
+        }
+    }
     if (in.group) {
         for (int64_t s = 0; s < S; ++s)
             if (in.group[s] > 127) return fail(SS_EINVAL, "at most 128 actuation groups in the tiled layout");

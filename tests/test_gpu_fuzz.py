@@ -107,6 +107,8 @@ def test_random_scene_fp32_within_tolerance(seed, n, long_range, lattice, layout
     import oracle as orc
     scene = random_scene(seed, n, long_range=long_range, lattice=lattice)
     eng = Engine(scene, integrator=integrator, precision="f32", layout=layout)
+    if fmt == 5:                                            # every spring distinct: fp32 inline records
+        assert eng.info()["tile_kernel"] == 6
     ref = orc.OracleEngine(scene_arrays(scene), integrator=integrator)
     count = 60 if integrator == "rk4" else 150
     eng.step(count)

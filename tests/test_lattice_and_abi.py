@@ -167,6 +167,11 @@ def test_fp64_compact_tile_plan_on_host(monkeypatch):
     assert plan(cube, precision="f64")["tile_kernel"] == 5
     monkeypatch.setenv("SS_TILE_DICT", "explicit")
     assert plan(cube, precision="f64")["tile_kernel"] == 0
+    assert plan(cube, precision="f32")["tile_kernel"] == 1
+    monkeypatch.delenv("SS_TILE_DICT")
+    assert plan(cube, precision="f32")["tile_kernel"] == 2
+    f32i = plan(rnd, precision="f32")
+    assert f32i["tile_kernel"] == 6 and f32i["tile_blob_bytes"] >= 20 * 2 * rnd.spring_count
 
 
 def test_engine_without_gpu_fails_loudly():

@@ -361,6 +361,25 @@ def test_sharded_multi_material_cube_bitwise():
     assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["p2p", "copy"])
+def test_sharded_general_graph_bitwise(transport):
+    """A cube whose every spring has its own stiffness (so every tile
+    overflows the 64-entry dictionary and steps on the inline general-graph
+    format) in 3 slabs: bitwise the single engine."""
+    from paper_2207_09334_b200.sharded import ShardGroup
+    c = L.excite(L.block_scene(12), seed=7)
+    c.k = c.k * (1.0 + 1e-7 * np.arange(c.k.size))
+    one = Engine(c, precision="f64")
+    assert one.info()["tile_kernel"] == 5
+    grp = ShardGroup.from_scene(c, 3, precision="f64", transport=transport)
+    for n in (7, 40):
+        one.step(n)
+        grp.step(n)
+        x, v = _assemble(grp)
+        assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
+
+
 def _ipc_beam_worker(rank, world, port, steps, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
