@@ -1318,6 +1318,15 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step" && L.compact && !L.has_self &&
                 (int64_t)f64s <= dev_max) {
                 h->f64_smem = f64s;
+                // programmatic dependent launch lets the next substep's CTAs
+                // take SM slots early; for grids of ~1/3 to 3 CTAs per SM the
+                // waiting CTAs pile onto the SMs left idle and the fp64 step
+                // then runs two tiles on one SM: 360K springs 14.4 us with PDL
+                // against 8.3 without (tools/wave_probe.py); smaller and
+                // larger grids keep it (47 tiles 6.8 vs 8.3, 10M 63.4 vs 67.4)
+                int sms = 0;
+                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+                if (!getenv("SS_PDL") && L.n_tiles >= 48 && L.n_tiles <= 3 * (int64_t)sms) h->pdl = false;
                 if (const char *e = getenv("SS_F64_VARIANT")) h->f64_variant = atoi(e);
                 for (auto *kk : {tile_f64_kernel<0, false, 2, 4>, tile_f64_kernel<1, false, 2, 4>,
                                  tile_f64_kernel<0, true, 2, 4>, tile_f64_kernel<1, true, 2, 4>,
