@@ -1090,12 +1090,15 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
         for (int64_t i = 0; i < ND; ++i)
             if (h->src_of(i) >= 0) used = i + 1;
     }
-    // lanes per mass: fp32 4-8 lanes add partial sums in a fixed tree; fp64
-    // adds in list order, where lanes cost more in shuffles than they save:
-    // one lane per mass, four incidences in flight through the branch-free
-    // IEEE sequences (crawler 2.50 -> 2.14 us, 12 crawlers 5.72 -> 2.68, the
-    // 40x4x4 beam as a cluster 5.08 against 6.71 with launches)
-    h->res_g = F32 ? (used * 8 <= 1024 ? 8 : 4) : 1;
+    // lanes per mass.  fp64 adds in list order, where lanes cost more in
+    // shuffles than they save: one lane per mass, four incidences in flight
+    // through the branch-free IEEE sequences (crawler 2.50 -> 2.14 us, 12
+    // crawlers 5.72 -> 2.68, the 40x4x4 beam as a cluster 5.08 against 6.71
+    // with launches).  fp32: 8 lanes with a fixed-order tree for scenes of
+    // <= 128 masses (crawler 1.03 us against 1.53 with one lane), else one
+    // lane with four partial sums (beam 3.68 -> 3.46 us, the 9^3 cube 4.47
+    // -> 3.52, 64 crawlers 3.68 -> 2.90, against 4 lanes)
+    h->res_g = F32 ? (used * 8 <= 1024 ? 8 : 1) : 1;
     if (const char *e = getenv("SS_RESIDENT_G")) {                 // A/B: 1, 4 or 8
         const int g = atoi(e);
         if ((g == 1 || g == 4 || g == 8) && used * g <= 1024) h->res_g = g;

@@ -110,7 +110,38 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
     using T = typename Prec<F32>::T;
     V3<T> s = {(T)0, (T)0, (T)0};
     const int q0 = (int)row[m], n = (int)row[m + 1] - q0;
-    if constexpr (F32) {
+    if constexpr (F32 && G == 1) {
+        // one lane per mass: four partial sums (incidences q = 0, 1, 2, 3
+        // mod 4) for instruction-level parallelism, combined in a fixed order
+        const float4 *dict = reinterpret_cast<const float4 *>(smem + a.off_dict);
+        V3<float> ps[4] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+        auto term = [&](int q, V3<float> &acc) {
+            const uint32_t e = inc[q0 + q];
+            const float4 kd = dict[2 * (e >> 13)], ez = dict[2 * (e >> 13) + 1];
+            float kl0 = kd.y;
+            if (scale) {
+                const int g = __float_as_int(ez.y);
+                if (g >= 0) kl0 = kl0 * scale[g];
+            }
+            const float4 ro = xs[e & 0xfffu];
+            const float dx = kd.z + (ro.x - x4.x), dy = kd.w + (ro.y - x4.y), dz = ez.x + (ro.z - x4.z);
+            float d2;
+            const float c = spring_c(dx, dy, dz, kd.x, kl0, d2);
+            if (d2 < 1e-24f && (e & 0x1000u)) ++deg;
+            acc.x = __fmaf_rn(c, dx, acc.x);
+            acc.y = __fmaf_rn(c, dy, acc.y);
+            acc.z = __fmaf_rn(c, dz, acc.z);
+        };
+        int q = 0;
+        for (; q + 4 <= n; q += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) term(q + u, ps[u]);
+        }
+        for (int u = 0; q < n; ++q, ++u) term(q, ps[u]);
+        s.x = (ps[0].x + ps[1].x) + (ps[2].x + ps[3].x);
+        s.y = (ps[0].y + ps[1].y) + (ps[2].y + ps[3].y);
+        s.z = (ps[0].z + ps[1].z) + (ps[2].z + ps[3].z);
+    } else if constexpr (F32) {
         const float4 *dict = reinterpret_cast<const float4 *>(smem + a.off_dict);
         for (int q = lane; q < n; q += G) {
             const uint32_t e = inc[q0 + q];
