@@ -314,6 +314,10 @@ int  ss_doc_render_masses(int64_t n, const double *m, const double *x, const dou
 int  ss_doc_render_springs(int64_t n, const int64_t *si, const int64_t *sj, const double *k, const double *l0,
                            const int32_t *group, const char *const *labels, int32_t n_labels, char **out,
                            int64_t *len);
+int  ss_doc_render(int64_t n_masses, const double *m, const double *x, const double *v, const double *f,
+                   const uint8_t *fixed, int64_t n_springs, const int64_t *si, const int64_t *sj, const double *k,
+                   const double *l0, const int32_t *group, const char *const *labels, int32_t n_labels,
+                   const char *pre, const char *mid, const char *post, char **out, int64_t *len);
 void ss_doc_free_text(char *p);
 int  ss_doc_repr(int64_t n, const double *v, char **out, int64_t *len);
 int  ss_doc_parse(const char *text, int64_t len, ss_doc **out);

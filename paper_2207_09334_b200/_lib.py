@@ -112,6 +112,9 @@ SIGNATURES = {
                                        C.POINTER(C.c_int64)]),
     "ss_doc_render_springs": (C.c_int, [C.c_int64, _i64p, _i64p, _dp, _dp, _i32p, C.POINTER(C.c_char_p),
                                         C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "ss_doc_render": (C.c_int, [C.c_int64, _dp, _dp, _dp, _dp, _u8p, C.c_int64, _i64p, _i64p, _dp, _dp, _i32p,
+                                C.POINTER(C.c_char_p), C.c_int32, C.c_char_p, C.c_char_p, C.c_char_p,
+                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "ss_doc_free_text": (None, [C.c_void_p]),
     "ss_doc_repr": (C.c_int, [C.c_int64, _dp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "ss_doc_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),

@@ -123,15 +123,9 @@ bool all_finite(const double *a, int64_t n) {
     return true;
 }
 
-// Render entries [0, n) in parallel blocks, then concatenate.
+// Render entries [0, n) in parallel blocks (entries joined by ",\n").
 template <typename One>
-int render_blocks(int64_t n, size_t per_entry, One one, char **out, int64_t *len) {
-    *out = nullptr;
-    *len = 0;
-    if (n == 0) {
-        *out = static_cast<char *>(std::malloc(1));
-        return *out ? SS_OK : SS_EINVAL;
-    }
+std::vector<std::string> render_parts(int64_t n, size_t per_entry, One one) {
     const int64_t block = 1 << 14;
     const int64_t nb = (n + block - 1) / block;
     std::vector<std::string> parts((size_t)nb);
@@ -147,18 +141,31 @@ int render_blocks(int64_t n, size_t per_entry, One one, char **out, int64_t *len
         }
         s.resize((size_t)(p - s.data()));
     }
-    size_t total = 0;
-    for (auto &s : parts) total += s.size();
-    char *buf = static_cast<char *>(std::malloc(total + 1));
-    if (!buf) return SS_EINVAL;
-    size_t o = 0;
-    for (auto &s : parts) {
-        std::memcpy(buf + o, s.data(), s.size());
-        o += s.size();
-    }
+    return parts;
+}
+
+// The pieces in order, into one malloc'd buffer (parallel copies).
+int concat(const std::vector<const std::string *> &pieces, char **out, int64_t *len) {
+    std::vector<size_t> off(pieces.size() + 1, 0);
+    for (size_t i = 0; i < pieces.size(); ++i) off[i + 1] = off[i] + pieces[i]->size();
+    char *buf = static_cast<char *>(std::malloc(off.back() + 1));
+    if (!buf) return SS_ENOMEM;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < (int64_t)pieces.size(); ++i)
+        std::memcpy(buf + off[i], pieces[i]->data(), pieces[i]->size());
     *out = buf;
-    *len = (int64_t)total;
+    *len = (int64_t)off.back();
     return SS_OK;
+}
+
+template <typename One>
+int render_blocks(int64_t n, size_t per_entry, One one, char **out, int64_t *len) {
+    *out = nullptr;
+    *len = 0;
+    const auto parts = render_parts(n, per_entry, one);
+    std::vector<const std::string *> pieces;
+    for (const auto &p : parts) pieces.push_back(&p);
+    return concat(pieces, out, len);
 }
 
 // ------------------------------------------------------------------ parse
@@ -484,16 +491,11 @@ bool read_array(Reader &r, ReadOne one) {
 
 struct ss_doc : Doc {};
 
-extern "C" {
+namespace {
 
-// sceneio.py:57-75 for the "masses" array: the text between "masses": [ and
-// the closing bracket line (entries at indent 4, joined by ",\n").
-int ss_doc_render_masses(int64_t n, const double *m, const double *x, const double *v, const double *f,
-                         const uint8_t *fixed, char **out, int64_t *len) {
-    if (!out || !len || n < 0 || (n && (!m || !x || !v || !f || !fixed))) return SS_EINVAL;
-    if (!all_finite(m, n) || !all_finite(x, 3 * n) || !all_finite(v, 3 * n) || !all_finite(f, 3 * n))
-        return SS_EFALLBACK;                   // json.dumps(allow_nan=False) raises: the host path words it
-    return render_blocks(n, kMassMax, [&](char *p, int64_t i) {
+// One "masses" / "springs" entry at indent 4 (the text json.dumps writes).
+auto mass_entry(const double *m, const double *x, const double *v, const double *f, const uint8_t *fixed) {
+    return [=](char *p, int64_t i) {
         p = put_str(p, "    {\n      \"id\": ");
         p = put_i64(p, i);
         p = put_str(p, ",\n      \"m\": ");
@@ -504,24 +506,13 @@ int ss_doc_render_masses(int64_t n, const double *m, const double *x, const doub
         p = put_vec(p, "      \"v\": [\n", v + 3 * i);
         p = put_str(p, ",\n");
         p = put_vec(p, "      \"f_ext\": [\n", f + 3 * i);
-        p = put_str(p, fixed[i] ? ",\n      \"fixed\": true\n    }" : ",\n      \"fixed\": false\n    }");
-        return p;
-    }, out, len);
+        return put_str(p, fixed[i] ? ",\n      \"fixed\": true\n    }" : ",\n      \"fixed\": false\n    }");
+    };
 }
 
-// The "springs" array; labels[g] is the JSON text of group g's label (the
-// host escapes it), group[s] < 0 renders null.
-int ss_doc_render_springs(int64_t n, const int64_t *si, const int64_t *sj, const double *k, const double *l0,
-                          const int32_t *group, const char *const *labels, int32_t n_labels, char **out,
-                          int64_t *len) {
-    if (!out || !len || n < 0 || (n && (!si || !sj || !k || !l0))) return SS_EINVAL;
-    if (!all_finite(k, n) || !all_finite(l0, n)) return SS_EFALLBACK;
-    size_t longest = 4;
-    for (int32_t g = 0; g < n_labels; ++g) longest = std::max(longest, std::strlen(labels[g]));
-    if (group)
-        for (int64_t s = 0; s < n; ++s)
-            if (group[s] >= n_labels) return SS_EINVAL;
-    return render_blocks(n, kSpringFixed + longest, [&](char *p, int64_t s) {
+auto spring_entry(const int64_t *si, const int64_t *sj, const double *k, const double *l0, const int32_t *group,
+                  const char *const *labels) {
+    return [=](char *p, int64_t s) {
         p = put_str(p, "    {\n      \"id\": ");
         p = put_i64(p, s);
         p = put_str(p, ",\n      \"i\": ");
@@ -535,7 +526,79 @@ int ss_doc_render_springs(int64_t n, const int64_t *si, const int64_t *sj, const
         p = put_str(p, ",\n      \"group\": ");
         p = put_str(p, group && group[s] >= 0 ? labels[group[s]] : "null");
         return put_str(p, "\n    }");
-    }, out, len);
+    };
+}
+
+// Argument checks shared by the renderers: SS_EINVAL, SS_EFALLBACK for a
+// non-finite value (json.dumps(allow_nan=False) raises: the host words it),
+// else SS_OK with the longest group label in *longest.
+int check_masses(int64_t n, const double *m, const double *x, const double *v, const double *f, const uint8_t *fixed) {
+    if (n < 0 || (n && (!m || !x || !v || !f || !fixed))) return SS_EINVAL;
+    if (!all_finite(m, n) || !all_finite(x, 3 * n) || !all_finite(v, 3 * n) || !all_finite(f, 3 * n))
+        return SS_EFALLBACK;
+    return SS_OK;
+}
+
+int check_springs(int64_t n, const int64_t *si, const int64_t *sj, const double *k, const double *l0,
+                  const int32_t *group, const char *const *labels, int32_t n_labels, size_t *longest) {
+    if (n < 0 || (n && (!si || !sj || !k || !l0)) || n_labels < 0 || (n_labels && !labels)) return SS_EINVAL;
+    if (!all_finite(k, n) || !all_finite(l0, n)) return SS_EFALLBACK;
+    *longest = 4;
+    for (int32_t g = 0; g < n_labels; ++g) *longest = std::max(*longest, std::strlen(labels[g]));
+    if (group)
+        for (int64_t s = 0; s < n; ++s)
+            if (group[s] >= n_labels) return SS_EINVAL;
+    return SS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// sceneio.py:57-75 for the "masses" array: the text between "masses": [ and
+// the closing bracket line (entries at indent 4, joined by ",\n").
+int ss_doc_render_masses(int64_t n, const double *m, const double *x, const double *v, const double *f,
+                         const uint8_t *fixed, char **out, int64_t *len) {
+    if (!out || !len) return SS_EINVAL;
+    const int rc = check_masses(n, m, x, v, f, fixed);
+    if (rc) return rc;
+    return render_blocks(n, kMassMax, mass_entry(m, x, v, f, fixed), out, len);
+}
+
+// The "springs" array; labels[g] is the JSON text of group g's label (the
+// host escapes it), group[s] < 0 renders null.
+int ss_doc_render_springs(int64_t n, const int64_t *si, const int64_t *sj, const double *k, const double *l0,
+                          const int32_t *group, const char *const *labels, int32_t n_labels, char **out,
+                          int64_t *len) {
+    if (!out || !len) return SS_EINVAL;
+    size_t longest = 0;
+    const int rc = check_springs(n, si, sj, k, l0, group, labels, n_labels, &longest);
+    if (rc) return rc;
+    return render_blocks(n, kSpringFixed + longest, spring_entry(si, sj, k, l0, group, labels), out, len);
+}
+
+// The whole document: pre + masses entries + mid + springs entries + post
+// (the host renders the small top-level values and passes the text around
+// the two arrays), built in parallel into one buffer.
+int ss_doc_render(int64_t n_masses, const double *m, const double *x, const double *v, const double *f,
+                  const uint8_t *fixed, int64_t n_springs, const int64_t *si, const int64_t *sj, const double *k,
+                  const double *l0, const int32_t *group, const char *const *labels, int32_t n_labels,
+                  const char *pre, const char *mid, const char *post, char **out, int64_t *len) {
+    if (!out || !len || !pre || !mid || !post) return SS_EINVAL;
+    *out = nullptr;
+    *len = 0;
+    int rc = check_masses(n_masses, m, x, v, f, fixed);
+    size_t longest = 0;
+    if (rc || (rc = check_springs(n_springs, si, sj, k, l0, group, labels, n_labels, &longest))) return rc;
+    const auto mp = render_parts(n_masses, kMassMax, mass_entry(m, x, v, f, fixed));
+    const auto sp = render_parts(n_springs, kSpringFixed + longest, spring_entry(si, sj, k, l0, group, labels));
+    const std::string a(pre), b(mid), c(post);
+    std::vector<const std::string *> pieces{&a};
+    for (const auto &q : mp) pieces.push_back(&q);
+    pieces.push_back(&b);
+    for (const auto &q : sp) pieces.push_back(&q);
+    pieces.push_back(&c);
+    return concat(pieces, out, len);
 }
 
 void ss_doc_free_text(char *p) { std::free(p); }

@@ -41,10 +41,17 @@ def _vec(a) -> list:
 def render_scene(scene) -> str:
     """Serialize ``scene`` (Scene, ArrayScene or a reference Scene) to the
     versioned document text (sceneio.py:57-75).  The masses and springs
-    arrays are written by the native codec (csrc/sceneio.cpp), the rest by
-    json.dumps; non-finite values go through the host writer, which raises
-    the reference's error."""
-    a = scene_arrays(scene)
+    arrays are written by the native codec (csrc/sceneio.cpp) around the rest
+    of the document, which json.dumps renders; non-finite values go through
+    the host writer, which raises the reference's error."""
+    native = _render_native(scene)
+    if native is None:
+        return _render_host(scene)
+    ptr, n = native
+    return _take_text(ptr, n)
+
+
+def _small_doc(scene, a, masses, springs) -> dict:
     labels = [g[0] for g in a.group_params]
     mats = [{"name": mt.name, "k0": mt.k0, "l_ref": mt.l_ref, "density": mt.density,
              "total_mass": mt.total_mass, "mass_per_node": mt.mass_per_node}
@@ -53,20 +60,54 @@ def render_scene(scene) -> str:
               for lab, mode, amp, freq, ph in a.group_params]
     planes = [{"normal": _vec(nrm), "offset": off, "penalty": pen, "friction": fr}
               for nrm, off, pen, fr in a.planes]
-    doc = {"schema_version": SCHEMA_VERSION, "gravity": _vec(a.gravity), "dt": a.dt, "damping": a.damping,
-           "masses": [], "springs": [], "materials": mats, "groups": groups, "planes": planes}
-    bodies = _native_bodies(a, labels)
-    if bodies is None:
-        doc["masses"], doc["springs"] = _mass_entries(a), _spring_entries(a, labels)
+    return {"schema_version": SCHEMA_VERSION, "gravity": _vec(a.gravity), "dt": a.dt, "damping": a.damping,
+            "masses": masses, "springs": springs, "materials": mats, "groups": groups, "planes": planes}, labels
+
+
+def _dumps(doc) -> str:
     try:
-        text = json.dumps(doc, indent=2, allow_nan=False) + "\n"
+        return json.dumps(doc, indent=2, allow_nan=False) + "\n"
     except ValueError as exc:
         raise SceneFormatError("$", f"non-finite value in scene: {exc}") from exc
-    if bodies is not None:
-        for key, body in zip(("masses", "springs"), bodies):
-            if body:
-                text = text.replace(f'\n  "{key}": [],\n', f'\n  "{key}": [\n{body}\n  ],\n', 1)
-    return text
+
+
+def _render_host(scene) -> str:
+    a = scene_arrays(scene)
+    doc, labels = _small_doc(scene, a, None, None)
+    doc["masses"], doc["springs"] = _mass_entries(a), _spring_entries(a, labels)
+    return _dumps(doc)
+
+
+def _render_native(scene):
+    """(pointer, length) of the whole document rendered natively (free with
+    ss_doc_free_text), or None when a value is non-finite."""
+    a = scene_arrays(scene)
+    doc, labels = _small_doc(scene, a, [], [])
+    text = _dumps(doc)                       # the small values; raises on non-finite ones
+    nm, ns = a.m.shape[0], a.si.shape[0]
+    im = text.index('\n  "masses": [],\n') + 3
+    js = text.index('\n  "springs": [],\n') + 3
+    pre = text[:im] + ('"masses": [\n' if nm else '"masses": []')
+    mid = ("\n  ]" if nm else "") + text[im + len('"masses": []'):js] + ('"springs": [\n' if ns else '"springs": []')
+    post = ("\n  ]" if ns else "") + text[js + len('"springs": []'):]
+    lib = _lib.lib()
+    f64 = lambda arr: np.ascontiguousarray(arr, dtype=np.float64)
+    m, x, v, f = f64(a.m), f64(a.x), f64(a.v), f64(a.f_ext)
+    fixed = np.ascontiguousarray(a.fixed, dtype=np.uint8)
+    si = np.ascontiguousarray(a.si, dtype=np.int64)
+    sj = np.ascontiguousarray(a.sj, dtype=np.int64)
+    k, l0 = f64(a.k), f64(a.l0)
+    group = None if a.group is None else np.ascontiguousarray(a.group, dtype=np.int32)
+    lab = (C.c_char_p * max(1, len(labels)))(*[json.dumps(t).encode("ascii") for t in labels])
+    ptr, n = C.c_void_p(), C.c_int64()
+    rc = lib.ss_doc_render(nm, _lib.dptr(m), _lib.dptr(x), _lib.dptr(v), _lib.dptr(f), _lib.u8ptr(fixed),
+                           ns, _lib.i64ptr(si), _lib.i64ptr(sj), _lib.dptr(k), _lib.dptr(l0), _lib.i32ptr(group),
+                           lab, len(labels), pre.encode("ascii"), mid.encode("ascii"), post.encode("ascii"),
+                           C.byref(ptr), C.byref(n))
+    if rc == _lib.SS_EFALLBACK:
+        return None
+    _lib.check(rc, "ss_doc_render")
+    return ptr, n.value
 
 
 def _mass_entries(a) -> list:
@@ -90,33 +131,6 @@ def _take_text(ptr, n) -> str:
         return C.string_at(ptr, n).decode("ascii")
     finally:
         lib.ss_doc_free_text(ptr)
-
-
-def _native_bodies(a, labels):
-    """(masses text, springs text) from the native writer, or None when a
-    value is non-finite (the host writer reports it)."""
-    lib = _lib.lib()
-    f64 = lambda arr: np.ascontiguousarray(arr, dtype=np.float64)
-    m, x, v, f = f64(a.m), f64(a.x), f64(a.v), f64(a.f_ext)
-    fixed = np.ascontiguousarray(a.fixed, dtype=np.uint8)
-    ptr, n = C.c_void_p(), C.c_int64()
-    rc = lib.ss_doc_render_masses(m.shape[0], _lib.dptr(m), _lib.dptr(x), _lib.dptr(v), _lib.dptr(f),
-                                  _lib.u8ptr(fixed), C.byref(ptr), C.byref(n))
-    if rc == _lib.SS_EFALLBACK:
-        return None
-    _lib.check(rc, "ss_doc_render_masses")
-    masses = _take_text(ptr, n.value)
-    si = np.ascontiguousarray(a.si, dtype=np.int64)
-    sj = np.ascontiguousarray(a.sj, dtype=np.int64)
-    k, l0 = f64(a.k), f64(a.l0)
-    group = None if a.group is None else np.ascontiguousarray(a.group, dtype=np.int32)
-    lab = (C.c_char_p * max(1, len(labels)))(*[json.dumps(t).encode("ascii") for t in labels])
-    rc = lib.ss_doc_render_springs(si.shape[0], _lib.i64ptr(si), _lib.i64ptr(sj), _lib.dptr(k), _lib.dptr(l0),
-                                   _lib.i32ptr(group), lab, len(labels), C.byref(ptr), C.byref(n))
-    if rc == _lib.SS_EFALLBACK:
-        return None
-    _lib.check(rc, "ss_doc_render_springs")
-    return masses, _take_text(ptr, n.value)
 
 
 # ------------------------------------------------------------ parsing
@@ -212,8 +226,11 @@ def _check_top(raw) -> dict:
 def _parse_native(text: str):
     if not text.isascii():
         return None
+    return _parse_native_bytes(text.encode("ascii"))
+
+
+def _parse_native_bytes(raw_bytes: bytes):
     lib = _lib.lib()
-    raw_bytes = text.encode("ascii")
     h = C.c_void_p()
     rc = lib.ss_doc_parse(raw_bytes, len(raw_bytes), C.byref(h))
     if rc == _lib.SS_EFALLBACK:
@@ -345,10 +362,27 @@ def _first_duplicate(si, sj, n):
 
 
 def save_scene(scene, path) -> None:
-    with open(path, "w") as fh:
-        fh.write(render_scene(scene))
+    """Write the document; the natively rendered text goes to the file
+    straight from the library's buffer."""
+    native = _render_native(scene)
+    if native is None:
+        with open(path, "w") as fh:
+            fh.write(_render_host(scene))
+        return
+    ptr, n = native
+    try:
+        with open(path, "wb") as fh:
+            fh.write(memoryview((C.c_char * n).from_address(ptr.value)) if n else b"")
+    finally:
+        _lib.lib().ss_doc_free_text(ptr)
 
 
 def load_scene(path) -> ArrayScene:
-    with open(path) as fh:
-        return parse_scene(fh.read())
+    """Read and parse a document: the native fast path reads the file's bytes
+    as they are; anything it does not accept is parsed from the text."""
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    fast = _parse_native_bytes(raw) if raw.isascii() else None
+    if fast is not None:
+        return fast
+    return _parse_host(raw.decode("utf-8"))
