@@ -186,10 +186,28 @@ struct ss_engine {
     unsigned res_dict_bytes = 0, res_off[3] = {0, 0, 0};   // smem offsets: dict, groups, segment
     size_t res_smem = 0;
     int res_ctas = 0, res_pslots = 0, res_g = 0, res_threads = 0;
+    // CUDA-graph replays of whole batches (launch_steps): a batch of `count`
+    // substeps from buffer parity `cur` with identical launch parameters is
+    // captured once (on its second occurrence) and replayed; the step
+    // numbers come from the device word d_step_base (Params::step_base)
+    struct GraphEntry {
+        std::vector<unsigned char> key;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t last_use = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    std::vector<std::vector<unsigned char>> graph_seen;   // keys met once
+    uint64_t graph_clock = 0;
+    long long *d_step_base = nullptr;
+    int64_t graph_base_n = -1;                            // the device step base after the queued work (-1: unknown)
+    bool use_graphs = true;                               // SS_GRAPH=0: off
+    bool graph_capturing = false;
 
     ~ss_engine() {
         if (device >= 0) cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
+        for (auto &g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
         for (int s = 0; s < 2; ++s) {
             if (!peer_ipc[s]) continue;
             if (peer_mailbox[s]) cudaIpcCloseMemHandle(peer_mailbox[s]);
@@ -650,13 +668,110 @@ void launch_rk4_f64(ss_engine *h, const Params<double> &p, int grid, int stage) 
     else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
 }
 
+__global__ void step_base_set(long long *base, long long n) { *base = n; }
+__global__ void step_base_add(long long *base, long long count) { *base += count; }
+
+// The identity of a batch for the graph cache: its launch parameters (the
+// Params every substep starts from, which holds every pointer and scalar the
+// kernels read), count, parity and the engine's kernel choices.
+template <typename T>
+std::vector<unsigned char> graph_key(const ss_engine *h, const Params<T> &p, int64_t count) {
+    std::vector<unsigned char> k(sizeof(Params<T>) + 64, 0);
+    std::memcpy(k.data(), &p, sizeof(Params<T>));
+    int64_t extra[8] = {count, h->cur, h->integrator, h->pdl ? 1 : 0, h->lean_lanes, h->f64_variant,
+                        (int64_t)(intptr_t)h->scale, h->has_prev ? 1 : 0};
+    std::memcpy(k.data() + sizeof(Params<T>), extra, sizeof extra);
+    return k;
+}
+
+template <bool F32, int LAYOUT>
+int launch_steps(ss_engine *h, int64_t count);
+
+// Replay (or capture, on a key's second occurrence) the launch loop of a
+// batch as a CUDA graph: the launch gap between substeps goes (mid-size
+// scenes 1.5-2 us of ~8 us per substep, 0.7 us of 64 us on the 10M cube).
+// Returns 1 if the batch was enqueued as a graph, 0 to launch it normally.
+template <bool F32, int LAYOUT>
+int try_graph(ss_engine *h, int64_t count, Params<typename Prec<F32>::T> p, int *rc_out) {
+    using T = typename Prec<F32>::T;
+    *rc_out = SS_OK;
+    if (!h->use_graphs || count < 2 || h->nccl || h->p2p_on || (h->integrator == SS_VERLET && !h->has_prev))
+        return 0;
+    const auto key = graph_key<T>(h, p, count);
+    auto *entry = [&]() -> ss_engine::GraphEntry * {
+        for (auto &g : h->graphs)
+            if (g.key == key) return &g;
+        return nullptr;
+    }();
+    if (!entry) {
+        bool seen = false;
+        for (auto &k : h->graph_seen) seen = seen || k == key;
+        if (!seen) {                                         // first occurrence: remember, launch normally
+            if (h->graph_seen.size() >= 16) h->graph_seen.erase(h->graph_seen.begin());
+            h->graph_seen.push_back(key);
+            return 0;
+        }
+        if (!h->d_step_base) {
+            int rc = h->alloc(&h->d_step_base, sizeof(long long));
+            if (rc) { *rc_out = rc; return 1; }
+        }
+        // capture the loop with step numbers relative to the device base
+        const int cur0 = h->cur;
+        const bool prev0 = h->has_prev;
+        const int64_t launches0 = h->launches, n0 = h->n;
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        h->n = 0;                                            // (the loop numbers steps h->n + s + 1)
+        h->graph_capturing = true;
+        int rc = launch_steps<F32, LAYOUT>(h, count);
+        h->graph_capturing = false;
+        h->n = n0;
+        if (rc == SS_OK) step_base_add<<<1, 1, 0, h->stream>>>(h->d_step_base, (long long)count);
+        const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+        h->cur = cur0;                                       // (replayed below)
+        h->has_prev = prev0;
+        h->launches = launches0;
+        if (rc) { *rc_out = rc; return 1; }
+        if (ec != cudaSuccess || !graph) {
+            cudaGetLastError();
+            h->use_graphs = false;                           // capture unsupported here: launch normally from now on
+            return 0;
+        }
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) {
+            cudaGetLastError();
+            h->use_graphs = false;
+            return 0;
+        }
+        if (h->graphs.size() >= 4) {                         // evict the least recently used
+            auto victim = std::min_element(h->graphs.begin(), h->graphs.end(),
+                                           [](const auto &a, const auto &b) { return a.last_use < b.last_use; });
+            cudaGraphExecDestroy(victim->exec);
+            h->graphs.erase(victim);
+        }
+        h->graphs.push_back({key, exec, 0});
+        entry = &h->graphs.back();
+    }
+    entry->last_use = ++h->graph_clock;
+    if (h->graph_base_n != h->n) step_base_set<<<1, 1, 0, h->stream>>>(h->d_step_base, (long long)h->n);
+    CK(cudaGraphLaunch(entry->exec, h->stream));
+    h->graph_base_n = h->n + count;
+    const int stages = h->integrator == SS_RK4 ? 4 : 1;
+    h->launches += count * stages;
+    if (h->integrator != SS_RK4) h->cur ^= (int)(count & 1);
+    if (h->integrator == SS_VERLET) h->has_prev = true;
+    return 1;
+}
+
 template <bool F32, int LAYOUT>
 int launch_steps(ss_engine *h, int64_t count) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
     const int stages = h->integrator == SS_RK4 ? 4 : 1;
     const size_t G = h->groups.size();
-    if (G) {
+    if (G && !h->graph_capturing) {                          // (a capture re-enters here: the table is uploaded)
         std::vector<double> tab;
         build_scales(h, count, stages, h->t, h->n, tab);
         int rc = upload_scales<T>(h, tab);
@@ -754,6 +869,12 @@ int launch_steps(ss_engine *h, int64_t count) {
         if (h->integrator == SS_VERLET) h->has_prev = true;
         CK(cudaGetLastError());
         return SS_OK;
+    }
+    if (!h->graph_capturing) {
+        int grc = SS_OK;
+        if (try_graph<F32, LAYOUT>(h, count, p, &grc)) return grc;
+    } else {
+        p.step_base = h->d_step_base;                        // capturing: step numbers relative to the base
     }
     for (int64_t s = 0; s < count; ++s) {
         p.step = h->n + s + 1;
@@ -1264,6 +1385,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         // the process: grant the device maximum, never a per-engine size
         if ((rc = set_tile_smem<F32>((size_t)dev_max))) return rc;
         if (const char *e = getenv("SS_PDL")) h->pdl = atoi(e) != 0;
+        if (const char *e = getenv("SS_GRAPH")) h->use_graphs = atoi(e) != 0;
         if constexpr (F32) {
             // fp32 Euler/Verlet on compact tiles: tile_lean_kernel (tile_f32.cuh)
             // unless SS_KERNEL=step1 asks for kernels.cuh's step_kernel; the

@@ -612,3 +612,59 @@ def test_page_locked_state_arrays(precision):
     a = _lib.pinned_empty((1000, 3))
     a[:] = 1.5
     assert a.flags.c_contiguous and float(a.sum()) == 4500.0
+
+
+def _graph_pair(make, monkeypatch, **kw):
+    """The same scene in two engines: batches replayed as CUDA graphs
+    (default) and launched one by one (SS_GRAPH=0)."""
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SS_GRAPH", flag)
+        out.append(Engine(make(), **kw))
+    monkeypatch.delenv("SS_GRAPH")
+    return out
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("integrator", ["verlet", "euler", "rk4"])
+def test_graph_replays_are_bitwise_the_launches(precision, integrator, monkeypatch):
+    """Repeated batches of one shape are captured once and replayed as CUDA
+    graphs (step numbers from a device word, actuation tables re-uploaded
+    per batch); a parameter change between batches makes a new graph.  The
+    replays give the bits of one launch per substep, in both precisions."""
+    from paper_2207_09334_b200 import crawler_scene, lattice as L, replicate
+    monkeypatch.setenv("SS_RESIDENT", "0")
+    for make in (lambda: L.excite(L.block_scene(20), seed=3),
+                 lambda: replicate(crawler_scene(), 48, jitter=1e-6, seed=2)):     # 2 groups, contact
+        g, n = _graph_pair(make, monkeypatch, integrator=integrator, precision=precision)
+        for eng in (g, n):
+            for b in range(6):
+                if b == 3:
+                    eng.set_damping(2e-3)                   # new launch parameters: a new graph
+                eng.step(25)
+            eng.step(7)
+            eng.step(25)
+        assert g.x.tobytes() == n.x.tobytes() and g.v.tobytes() == n.v.tobytes()
+        assert g.n == n.n == 182 and g.t == n.t
+        assert g.launch_count == n.launch_count
+        g.close()
+        n.close()
+
+
+def test_graph_replays_report_divergence_like_the_launches(monkeypatch):
+    """A step that diverges inside a replayed batch: the same DivergenceError
+    (step and lowest mass) and the same state as one launch per substep."""
+    from paper_2207_09334_b200 import lattice as L
+    monkeypatch.setenv("SS_RESIDENT", "0")
+    blown = L.excite(L.block_scene(20), seed=11)
+    blown.dt = 0.004
+    got = []
+    for eng in _graph_pair(lambda: blown, monkeypatch, integrator="euler", precision="f64"):
+        eng.step(10)
+        with pytest.raises(DivergenceError) as err:
+            for _ in range(200):
+                eng.step(10)
+        got.append((err.value.mass_id, err.value.step, eng.n, eng.x.tobytes()))
+        eng.close()
+    assert got[0] == got[1]
+    assert got[0][1] > 30                                   # (diverged inside a replayed batch)
