@@ -190,11 +190,13 @@ def _ipc_worker(rank, world, port, cells, steps, precision, q):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(600)
-def test_peer_memory_shards_across_processes():
-    """Two processes, one shard each, sharing one GPU: mailboxes mapped with
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_memory_shards_across_processes(world):
+    """Two or three processes, one shard each, sharing one GPU (with three,
+    the middle shard exchanges with two neighbours): mailboxes mapped with
     cudaIpcOpenMemHandle, planes pushed and landed every substep with no host
     round trip; the assembled fp64 state is bitwise the single engine's."""
-    cells, steps, world = 9, 30, 2
+    cells, steps = 9, 30
     full = L.excite(L.block_scene(cells), seed=11)
     one = Engine(full, precision="f64")
     one.step(steps)
@@ -202,7 +204,7 @@ def test_peer_memory_shards_across_processes():
     one.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 2000) + 7
+    port = 29500 + (os.getpid() % 2000) + 7 + world
     procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, cells, steps, "f64", q)) for r in range(world)]
     for p in procs:
         p.start()
