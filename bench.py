@@ -454,13 +454,15 @@ def run_single(args):
         if not args.no_extra:
             alt = "f32" if args.precision == "f64" else "f64"
             other = engine_leg(scene, alt, args, clk, workload, e2e_steps, "other precision")
-        general = None
+        general = {}
         if not args.no_extra:
-            # the general-graph record format (explicit per-spring records, what
-            # any scene that does not fit the compact dictionary runs) on the same cube
+            # the general-graph record format (records per incidence, what any
+            # scene whose tiles do not fit the compact dictionary runs) on the
+            # same cube, in both precisions
             os.environ["SS_TILE_DICT"] = "0"
             try:
-                general = engine_leg(scene, args.precision, args, clk, workload, 0, "explicit records")
+                for prec in (args.precision, "f32" if args.precision == "f64" else "f64"):
+                    general[prec] = engine_leg(scene, prec, args, clk, workload, 0, "inline records")
             finally:
                 del os.environ["SS_TILE_DICT"]
         scaling = None
@@ -498,10 +500,11 @@ def run_single(args):
                      "note": ("fp32 production mode: displacement form, within 1e-4 relative of the "
                               "reference (DESIGN.md 5)") if other["dtype"] == "f32" else
                              "fp64 validation mode, bitwise equal to the reference's serial engine"}
-    if general:
-        line["general_graph_format"] = {
-            "value": general["value"], "unit": UNIT, "ms_per_step": general["ms_per_step"],
-            "dtype": general["dtype"], "roofline": general["roofline"],
+    for prec, g in general.items():
+        key = "general_graph_format" if prec == args.precision else "general_graph_format_" + prec
+        line[key] = {
+            "value": g["value"], "unit": UNIT, "ms_per_step": g["ms_per_step"],
+            "dtype": g["dtype"], "roofline": g["roofline"],
             "note": "SS_TILE_DICT=0: the general-graph record format (records per incidence streamed "
                     "from HBM: fp64 (k, l0), fp32 (k, k*l0, D)) -- what a scene whose tiles do not fit "
                     "the 64-entry dictionary runs -- on the same cube"}
