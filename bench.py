@@ -506,7 +506,7 @@ def run_single(args):
             "value": g["value"], "unit": UNIT, "ms_per_step": g["ms_per_step"],
             "dtype": g["dtype"], "roofline": g["roofline"],
             "note": "SS_TILE_DICT=0: the general-graph record format (records per incidence streamed "
-                    "from HBM: fp64 (k, l0), fp32 (k, k*l0, D)) -- what a scene whose tiles do not fit "
+                    "from HBM: fp64 (k, l0), fp32 (k, k*l0) with D formed from the staged X0) -- what a scene whose tiles do not fit "
                     "the 64-entry dictionary runs -- on the same cube"}
     if scaling:
         line["scaling_1gpu"] = scaling

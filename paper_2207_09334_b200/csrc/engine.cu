@@ -45,6 +45,9 @@ using namespace ss;
 namespace {
 
 constexpr int kBlock = kBlockThreads;
+// fp32 inline tiles stage X0 too (tile_f32.cuh): ~57 KB per CTA on the 10M
+// cube, so at most 4 CTAs per SM -- let the kernel have the registers
+constexpr int kInlineMinB = 4;
 
 struct Group {
     int mode;
@@ -130,8 +133,7 @@ struct ss_engine {
     int2 *inc = nullptr;
     unsigned char *d_blob = nullptr;
     double2 *d_kl_inline = nullptr;            // fp64 inline tile format (tiles.h)
-    float4 *d_kd_inline = nullptr;             // fp32 inline tile format
-    float *d_dz_inline = nullptr;
+    float2 *d_kd_inline = nullptr;             // fp32 inline tile format (+ d_x0dev)
     int8_t *d_g_inline = nullptr;
     unsigned long long *d_kl_off = nullptr;
     unsigned long long *d_toff = nullptr;
@@ -466,7 +468,7 @@ Params<T> base_params(const ss_engine *h) {
     tp.g_inline = h->d_g_inline;
     tp.kl_off = h->d_kl_off;
     tp.kd_inline = h->d_kd_inline;
-    tp.dz_inline = h->d_dz_inline;
+    tp.x0 = h->d_x0dev;
     for (int c = 0; c < 3; ++c) p.g[c] = (T)h->gravity[c];
     p.dt = (T)h->dt;
     p.half_dt = (T)(0.5 * h->dt);
@@ -587,10 +589,10 @@ void launch_rk4_lean(ss_engine *h, const Params<float> &p, int grid, int stage) 
     void (*k)(Params<float>) = nullptr;
     if (h->tl.inline_kl) {
         switch (stage) {
-            case 1: k = tile_lean_kernel<2, GROUPS, 6, 1, false, true>; break;
-            case 2: k = tile_lean_kernel<3, GROUPS, 6, 1, false, true>; break;
-            case 3: k = tile_lean_kernel<4, GROUPS, 6, 1, false, true>; break;
-            default: k = tile_lean_kernel<5, GROUPS, 6, 1, false, true>; break;
+            case 1: k = tile_lean_kernel<2, GROUPS, kInlineMinB, 1, false, true>; break;
+            case 2: k = tile_lean_kernel<3, GROUPS, kInlineMinB, 1, false, true>; break;
+            case 3: k = tile_lean_kernel<4, GROUPS, kInlineMinB, 1, false, true>; break;
+            default: k = tile_lean_kernel<5, GROUPS, kInlineMinB, 1, false, true>; break;
         }
         if (h->pdl) launch_pdl(k, grid, kTile, h->lean_smem, h->stream, p);
         else k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
@@ -611,10 +613,10 @@ template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     const bool euler = h->integrator == SS_EULER;
     if (h->tl.inline_kl) {                                 // general graphs: records streamed per incidence
-        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, 6, 1, true, true>
-                                      : tile_lean_kernel<1, GROUPS, 6, 1, true, true>)
-                             : (euler ? tile_lean_kernel<0, GROUPS, 6, 1, false, true>
-                                      : tile_lean_kernel<1, GROUPS, 6, 1, false, true>);
+        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, true, true>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, true, true>)
+                             : (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, false, true>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, false, true>);
         if (h->pdl) launch_pdl(ki, grid, kTile, h->lean_smem, h->stream, p);
         else ki<<<grid, kTile, h->lean_smem, h->stream>>>(p);
         return;
@@ -1359,9 +1361,9 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         if (L.inline_kl) {                        // general-graph format: records streamed, not staged
             if (F32) {
                 if ((rc = up_vec(h, &p, L.kd_inline))) return rc;
-                h->d_kd_inline = reinterpret_cast<float4 *>(p);
-                if ((rc = up_vec(h, &p, L.dz_inline))) return rc;
-                h->d_dz_inline = reinterpret_cast<float *>(p);
+                h->d_kd_inline = reinterpret_cast<float2 *>(p);
+                if ((rc = h->alloc(&h->d_x0dev, h->x0.size() * sizeof(double)))) return rc;
+                if ((rc = upload(h, h->d_x0dev, h->x0.data(), h->x0.size() * sizeof(double)))) return rc;
             } else {
                 if ((rc = up_vec(h, &p, L.kl_inline))) return rc;
                 h->d_kl_inline = reinterpret_cast<double2 *>(p);
@@ -1395,6 +1397,7 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step1" && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
+                if (L.inline_kl) h->lean_smem += (size_t)(kTile + L.max_halo) * 3 * sizeof(double);   // staged X0
                 // scenes with few tiles (at most 3 per SM) use two lanes per mass:
                 // 512-thread CTAs, twice the warps for the same tiles
                 int sms = 0;
@@ -1421,15 +1424,15 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_lean_kernel<3, false, 6, 2>, tile_lean_kernel<4, false, 6, 2>,
                                  tile_lean_kernel<5, false, 6, 2>, tile_lean_kernel<2, true, 6, 2>,
                                  tile_lean_kernel<3, true, 6, 2>, tile_lean_kernel<4, true, 6, 2>,
-                                 tile_lean_kernel<5, true, 6, 2>, tile_lean_kernel<0, false, 6, 1, false, true>,
-                                 tile_lean_kernel<1, false, 6, 1, false, true>, tile_lean_kernel<0, true, 6, 1, false, true>,
-                                 tile_lean_kernel<1, true, 6, 1, false, true>, tile_lean_kernel<0, false, 6, 1, true, true>,
-                                 tile_lean_kernel<1, false, 6, 1, true, true>, tile_lean_kernel<0, true, 6, 1, true, true>,
-                                 tile_lean_kernel<1, true, 6, 1, true, true>, tile_lean_kernel<2, false, 6, 1, false, true>,
-                                 tile_lean_kernel<3, false, 6, 1, false, true>, tile_lean_kernel<4, false, 6, 1, false, true>,
-                                 tile_lean_kernel<5, false, 6, 1, false, true>, tile_lean_kernel<2, true, 6, 1, false, true>,
-                                 tile_lean_kernel<3, true, 6, 1, false, true>, tile_lean_kernel<4, true, 6, 1, false, true>,
-                                 tile_lean_kernel<5, true, 6, 1, false, true>})
+                                 tile_lean_kernel<5, true, 6, 2>, tile_lean_kernel<0, false, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<1, false, kInlineMinB, 1, false, true>, tile_lean_kernel<0, true, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<1, true, kInlineMinB, 1, false, true>, tile_lean_kernel<0, false, kInlineMinB, 1, true, true>,
+                                 tile_lean_kernel<1, false, kInlineMinB, 1, true, true>, tile_lean_kernel<0, true, kInlineMinB, 1, true, true>,
+                                 tile_lean_kernel<1, true, kInlineMinB, 1, true, true>, tile_lean_kernel<2, false, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<3, false, kInlineMinB, 1, false, true>, tile_lean_kernel<4, false, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<5, false, kInlineMinB, 1, false, true>, tile_lean_kernel<2, true, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<3, true, kInlineMinB, 1, false, true>, tile_lean_kernel<4, true, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<5, true, kInlineMinB, 1, false, true>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
@@ -2733,7 +2736,7 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->canonical_order = h->tl.canonical ? 1 : 0;
         info->tile_count = h->tl.n_tiles;
         info->tile_blob_bytes = (int64_t)(h->tl.blob.size() + 8 * h->tl.kl_inline.size() + h->tl.g_inline.size() +
-                                          4 * (h->tl.kd_inline.size() + h->tl.dz_inline.size()));
+                                          4 * h->tl.kd_inline.size());
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
@@ -2777,7 +2780,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     info->canonical_order = tl.canonical ? 1 : 0;
     info->tile_count = tl.n_tiles;
     info->tile_blob_bytes = (int64_t)(tl.blob.size() + 8 * tl.kl_inline.size() + tl.g_inline.size() +
-                                      4 * (tl.kd_inline.size() + tl.dz_inline.size()));
+                                      4 * tl.kd_inline.size());
     info->tile_halo_ratio = tl.halo_ratio;
     info->tile_foreign_frac = tl.foreign_frac;
     const size_t vec = f32 ? sizeof(float4) : sizeof(double4);

@@ -181,16 +181,28 @@ __device__ __forceinline__ void acc3(V3<float> &s, float c, float dx, float dy, 
 // degenerate recount, by lane 0, covers all own springs).
 // (k, k*l0, Dx, Dy), Dz and group of incidence q (entry e): the tile's
 // dictionary, or (INLINE, general graphs) this mass's column of the inline
-// records in global memory (tiles.h), streamed.
+// (k, k*l0) records in global memory (tiles.h), streamed, with
+// D = fp32(X0_partner - X0_me) from the fp64 rest positions staged in shared
+// memory (sX0: x, y, z planes of ns slots) -- the dictionary's value.
 template <bool INLINE>
 struct F32Rec {
-    const float4 *dict;          // dictionary (2 float4 per entry), or the inline (k, k*l0, Dx, Dy) + column
-    const float *dz;             // inline Dz + column
+    const float4 *dict;          // dictionary (2 float4 per entry)
+    const float2 *kk;            // inline (k, k*l0) + column
     const int8_t *g;             // inline groups + column (null: none)
+    const double *sX0;           // inline: staged X0 planes
+    int ns;                      //   plane stride
+    double mx, my, mz;           //   X0 of this mass
+    __device__ __forceinline__ float2 load(int q) const { return __ldcs(kk + (q << 8)); }
     __device__ __forceinline__ void get(uint32_t e, int q, float4 &kd, float &dz_, int &grp) const {
+        get(e, q, INLINE ? load(q) : make_float2(0.f, 0.f), kd, dz_, grp);
+    }
+    // k2: the inline (k, k*l0) of incidence q, already loaded
+    __device__ __forceinline__ void get(uint32_t e, int q, float2 k2, float4 &kd, float &dz_, int &grp) const {
         if constexpr (INLINE) {
-            kd = __ldcs(dict + (q << 8));
-            dz_ = __ldcs(dz + (q << 8));
+            const uint32_t sl = e & 0x3ffu;
+            kd = make_float4(k2.x, k2.y, __double2float_rn(__dsub_rn(sX0[sl], mx)),
+                             __double2float_rn(__dsub_rn(sX0[ns + sl], my)));
+            dz_ = __double2float_rn(__dsub_rn(sX0[2 * ns + sl], mz));
             grp = g ? g[q << 8] : -1;
         } else {
             const float4 *ent = dict + 2 * (e >> 10);
@@ -210,19 +222,23 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
     F32Rec<INLINE> rec;
     if constexpr (INLINE) {
         const unsigned long long b0 = p.topo.kl_off[tile] + (unsigned long long)l;
-        rec.dict = p.topo.kd_inline + b0;
-        rec.dz = p.topo.dz_inline + b0;
+        rec.kk = p.topo.kd_inline + b0;
         rec.g = p.topo.g_inline ? p.topo.g_inline + b0 : nullptr;
+        rec.ns = kTile + (int)p.topo.max_halo;
+        rec.sX0 = reinterpret_cast<const double *>(v.sY + rec.ns);
+        rec.mx = rec.sX0[l];
+        rec.my = rec.sX0[rec.ns + l];
+        rec.mz = rec.sX0[2 * rec.ns + l];
     } else {
         rec.dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);
     }
     float dmin = INFINITY;
-    auto body = [&](int q) {
+    auto body = [&](int q, float2 k2) {
         const uint32_t e = inc[q << 8];
         float4 kd;                                          // (k, k*l0, Dx, Dy)
         float dzr;
         int g;
-        rec.get(e, q, kd, dzr, g);
+        rec.get(e, q, k2, kd, dzr, g);
         float kl0 = kd.y;
         if constexpr (GROUPS) {
             if (g >= 0) kl0 = kl0 * p.scale[g];
@@ -234,16 +250,37 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
         dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
         acc3(s, c, dx, dy, dz_);
     };
-    int q = lane;
+    if constexpr (INLINE) {
+        // records streamed from HBM, software pipelined: the next group's
+        // loads are in flight while this group computes
+        constexpr int P = 4;
+        float2 kc[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) kc[j] = j < n_inc ? rec.load(j) : make_float2(0.f, 0.f);
 #pragma unroll 1
-    for (; q + 3 * LANES < n_inc; q += 4 * LANES) {
-        body(q);
-        body(q + LANES);
-        body(q + 2 * LANES);
-        body(q + 3 * LANES);
+        for (int q = 0; q < n_inc; q += P) {
+            float2 kn[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) kn[j] = q + P + j < n_inc ? rec.load(q + P + j) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < P; ++j)
+                if (q + j < n_inc) body(q + j, kc[j]);
+#pragma unroll
+            for (int j = 0; j < P; ++j) kc[j] = kn[j];
+        }
+    } else {
+        const float2 none = make_float2(0.f, 0.f);
+        int q = lane;
+#pragma unroll 1
+        for (; q + 3 * LANES < n_inc; q += 4 * LANES) {
+            body(q, none);
+            body(q + LANES, none);
+            body(q + 2 * LANES, none);
+            body(q + 3 * LANES, none);
+        }
+#pragma unroll 1
+        for (; q < n_inc; q += LANES) body(q, none);
     }
-#pragma unroll 1
-    for (; q < n_inc; q += LANES) body(q);
     unsigned deg = 0;
     if (dmin_out) {
         *dmin_out = dmin;
@@ -333,6 +370,30 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         const uint32_t split = t.tsplit[tb] & 0xffffffu;
         bulk_copy(bl, t.blob + g0, split, bar);
         bulk_copy(bl + split, t.blob + g0 + split, bytes - split, bar + 1);
+    }
+    // INLINE: the fp64 rest positions X0 of own and halo slots, as x, y, z
+    // planes behind the staged displacements (rest vectors formed per
+    // incidence); step-independent, so staged before the grid dependency
+    const int ns = kTile + (int)t.max_halo;
+    double *sX0 = reinterpret_cast<double *>(sR + ns);
+    if constexpr (INLINE) {
+        if (active) {
+            sX0[l] = __ldg(t.x0 + 3 * (long long)m);
+            sX0[ns + l] = __ldg(t.x0 + 3 * (long long)m + 1);
+            sX0[2 * ns + l] = __ldg(t.x0 + 3 * (long long)m + 2);
+        }
+        mbar_wait_warp0(bar, 0);                            // halo ids
+        const int *halo = reinterpret_cast<const int *>(bl + reinterpret_cast<const TileHdr *>(bl)->off_halo);
+        const int nh = (int)reinterpret_cast<const TileHdr *>(bl)->n_halo;
+#pragma unroll 1
+        for (int i = tid; i < nh; i += kTile) {
+            const int gm = halo[i];
+            if (gm >= 0) {
+                sX0[kTile + i] = __ldg(t.x0 + 3 * (long long)gm);
+                sX0[ns + kTile + i] = __ldg(t.x0 + 3 * (long long)gm + 1);
+                sX0[2 * ns + kTile + i] = __ldg(t.x0 + 3 * (long long)gm + 2);
+            }
+        }
     }
     // everything below reads the previous substep's state
     asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -55,9 +55,11 @@ constexpr int SS_EAGAIN_SHAPE = -1001; // internal: a tile's degree or halo (or 
 //    also at off_og.  2 B per incidence, 4 B per spring.
 //  * inline (canonical bits 1|2|4; the fp32 general-graph format when a tile
 //    has more than 64 distinct records, or with SS_TILE_DICT=0): the compact
-//    incidence lists with partner slots only, and each incidence's (k, k*l0,
-//    Dx, Dy) float4, Dz float and int8 group in TileLayout::kd_inline /
-//    dz_inline / g_inline at kl_off[tile] + q*256 + l, streamed from HBM.
+//    incidence lists with partner slots only, and each incidence's (k, k*l0)
+//    float2 and int8 group in TileLayout::kd_inline / g_inline at
+//    kl_off[tile] + q*256 + l, streamed from HBM; the rest vector
+//    D = fp32(X0_partner - X0_me) is formed on the device from the staged
+//    fp64 X0 (the same value the dictionary stores).
 //  * explicit (canonical bit 1 clear; SS_TILE_DICT=explicit): counts = n_own | n_ref << 8; own
 //    records (other u16 off_oo, then planar k, k*l0, Dx, Dy, Dz [W*256 each]
 //    at off_okl, grp i8 off_og); a spring whose owner lies in another tile is
@@ -122,8 +124,7 @@ struct TileLayout {
     std::vector<double> kl_inline;  // inline format: (k, l0) pairs, tile t at kl_off[t] pairs
     std::vector<int8_t> g_inline;   // inline format: group per incidence (empty: no groups)
     std::vector<uint64_t> kl_off;   // inline format: n_tiles + 1 slot offsets (W * 256 per tile)
-    std::vector<float> kd_inline;   // fp32 inline format: (k, k*l0, Dx, Dy) per incidence slot
-    std::vector<float> dz_inline;   // fp32 inline format: Dz per incidence slot
+    std::vector<float> kd_inline;   // fp32 inline format: (k, k*l0) per incidence slot
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };

@@ -145,7 +145,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
     std::vector<uint32_t> tH(n_tiles), tHr(n_tiles), tSplit(n_tiles), tN(n_tiles), tW(n_tiles), tWr(n_tiles);
     std::vector<int64_t> tFor(n_tiles), tRefs(n_tiles);
     const bool has_g = in.group != nullptr;
-    std::vector<std::vector<float>> tKD(inline_rec ? n_tiles : 0), tDZ(inline_rec ? n_tiles : 0);
+    std::vector<std::vector<float>> tKD(inline_rec ? n_tiles : 0);
     std::vector<std::vector<int8_t>> tG(inline_rec && has_g ? n_tiles : 0);
     int err = 0;        // 1 hard limit, 3 dictionary overflow, 4 compact shape overflow
 #pragma omp parallel for schedule(dynamic, 16)
@@ -303,8 +303,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
                 if (has_g) put_at<int8_t>(blob, h.off_og + e, (int8_t)std::get<2>(kv.first));
             }
             if (inline_rec) {
-                tKD[t].assign((size_t)4 * inc_n, 0.f);
-                tDZ[t].assign((size_t)inc_n, 0.f);
+                tKD[t].assign((size_t)2 * inc_n, 0.f);
                 if (has_g) tG[t].assign((size_t)inc_n, (int8_t)-1);
             }
             int64_t n_inc = 0;
@@ -316,14 +315,10 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
                     const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;   // the other endpoint
                     const uint32_t at = ((uint32_t)q << 8) | (uint32_t)l;
                     uint32_t di = 0;
-                    if (inline_rec) {
-                        const auto key = key_of(s, m);
-                        tKD[t][4 * at] = std::get<0>(key);
-                        tKD[t][4 * at + 1] = std::get<1>(key);
-                        tKD[t][4 * at + 2] = std::get<3>(key);
-                        tKD[t][4 * at + 3] = std::get<4>(key);
-                        tDZ[t][at] = std::get<5>(key);
-                        if (has_g) tG[t][at] = (int8_t)std::get<2>(key);
+                    if (inline_rec) {                          // (k, k*l0); D from X0 on the device
+                        tKD[t][2 * at] = (float)in.k[s];
+                        tKD[t][2 * at + 1] = (float)(in.k[s] * in.l0[s]);
+                        if (has_g) tG[t][at] = (int8_t)in.group[s];
                     } else {
                         di = dict.at(key_of(s, m));
                     }
@@ -415,14 +410,12 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
     L.inline_kl = inline_rec;
     if (inline_rec) {
         L.kl_off.assign(n_tiles + 1, 0);
-        for (int64_t t = 0; t < n_tiles; ++t) L.kl_off[t + 1] = L.kl_off[t] + tDZ[t].size();
-        L.kd_inline.resize(4 * L.kl_off[n_tiles]);
-        L.dz_inline.resize(L.kl_off[n_tiles]);
+        for (int64_t t = 0; t < n_tiles; ++t) L.kl_off[t + 1] = L.kl_off[t] + tKD[t].size() / 2;
+        L.kd_inline.resize(2 * L.kl_off[n_tiles]);
         if (has_g) L.g_inline.resize(L.kl_off[n_tiles]);
 #pragma omp parallel for schedule(static)
         for (int64_t t = 0; t < n_tiles; ++t) {
-            std::memcpy(L.kd_inline.data() + 4 * L.kl_off[t], tKD[t].data(), tKD[t].size() * 4);
-            std::memcpy(L.dz_inline.data() + L.kl_off[t], tDZ[t].data(), tDZ[t].size() * 4);
+            std::memcpy(L.kd_inline.data() + 2 * L.kl_off[t], tKD[t].data(), tKD[t].size() * 4);
             if (has_g) std::memcpy(L.g_inline.data() + L.kl_off[t], tG[t].data(), tG[t].size());
         }
     }
