@@ -256,8 +256,8 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
  * planes to receive (side lo = lower-x neighbour, hi = upper), plane order
  * identical on both sides.  Transport:
  *   - ss_nccl_unique_id + ss_halo_nccl: one process per GPU; after every
- *     substep ss_step packs, exchanges (ncclSend/ncclRecv on the engine
- *     stream) and unpacks the planes;
+ *     substep (RK4: every stage) ss_step packs, exchanges (ncclSend/ncclRecv
+ *     on the engine stream) and unpacks the planes;
  *   - ss_halo_p2p_export + ss_halo_recv_slots + ss_halo_p2p_attach: one
  *     process per GPU on one node; the step kernel itself stores its
  *     boundary planes into the neighbours' position buffers over peer
@@ -272,8 +272,9 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
  *   - ss_halo_p2p_link: the same transport between engines of one process
  *     (same device or peer-accessible devices), without IPC;
  *   - ss_step_group: several shards on one device stepped in lockstep, the
- *     planes copied device-to-device or, when peer-linked, exchanged by the
- *     step kernels (virtual shards, for testing).
+ *     planes copied device-to-device (RK4: stage by stage) or, when
+ *     peer-linked, exchanged by the step kernels (virtual shards, for
+ *     testing).  The peer-memory transport is Euler/Verlet only.
  */
 int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
                   const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,

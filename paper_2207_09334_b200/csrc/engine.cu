@@ -168,6 +168,7 @@ struct ss_engine {
     ncclComm_t nccl = nullptr;
     int nccl_peer[2] = {-1, -1};
     int64_t halo_exchanges = 0;
+    int rk4_stage_only = 0;        // ss_step_group: launch only this RK4 stage (1-4) of a one-step batch
     // fused peer-memory exchange (kernels.cuh xchg_*): own flag mailbox, the
     // neighbours' mailboxes and position buffers (IPC-mapped or, for shards of
     // one process, plain), their slots for this shard's planes
@@ -527,11 +528,13 @@ void xchg_params(const ss_engine *h, Params<T> &p) {
     p.xchg_error = &mine->error;
 }
 
+// X: the position buffer whose boundary planes travel (default: the current
+// state; RK4 exchanges each stage's trial positions).
 template <typename T4>
-int halo_exchange_nccl(ss_engine *h) {
+int halo_exchange_nccl(ss_engine *h, T4 *X = nullptr) {
     const NcclApi *api = nccl_api();
     if (!api) return SS_ECUDA;
-    T4 *X = reinterpret_cast<T4 *>(h->X[h->cur]);
+    if (!X) X = reinterpret_cast<T4 *>(h->X[h->cur]);
     for (int s = 0; s < 2; ++s)
         if (h->halo_n_send[s] && h->nccl_peer[s] >= 0)
             halo_pack_kernel<T4><<<(h->halo_n_send[s] + 255) / 256, 256, 0, h->stream>>>(
@@ -955,19 +958,27 @@ int launch_steps(ss_engine *h, int64_t count) {
                 if (LAYOUT >= 3 && h->pdl) launch_pdl(k, grid, kBlock, smem, h->stream, p);
                 else k<<<grid, kBlock, smem, h->stream>>>(p);
             };
-            p.scale = G ? scale + ((size_t)s * 4 + 0) * G : nullptr;
-            p.X = Xc; p.V = V; p.Xout = XA; p.Vout = VS;
-            rk4_launch(rk4_kernel<F32, 1, LAYOUT>);
-            p.scale = G ? scale + ((size_t)s * 4 + 1) * G : nullptr;
-            p.X = XA; p.V = VS; p.Xout = XB; p.Vout = VS;
-            rk4_launch(rk4_kernel<F32, 2, LAYOUT>);
-            p.scale = G ? scale + ((size_t)s * 4 + 2) * G : nullptr;
-            p.X = XB; p.V = VS; p.Xout = XA; p.Vout = VS;
-            rk4_launch(rk4_kernel<F32, 3, LAYOUT>);
-            p.scale = G ? scale + ((size_t)s * 4 + 3) * G : nullptr;
-            p.X = XA; p.V = VS; p.Xout = Xc; p.Vout = V;
-            rk4_launch(rk4_kernel<F32, 4, LAYOUT>);
-            h->launches += 4;
+            // sharded (NCCL): every stage's trial positions cross to the
+            // neighbours' halos before the next stage reads them (SURVEY
+            // 8e: four exchanges per step); ss_step_group launches one
+            // stage at a time (rk4_stage_only) and copies the planes itself
+            const int only = h->rk4_stage_only;
+            auto stage_at = [&](int st, void (*k)(Params<T>), T4 *x, T4 *v, T4 *xo, T4 *vo) -> int {
+                if (only && only != st) {
+                    ++stage;
+                    return SS_OK;
+                }
+                p.scale = G ? scale + ((size_t)s * 4 + (st - 1)) * G : nullptr;
+                p.X = x; p.V = v; p.Xout = xo; p.Vout = vo;
+                rk4_launch(k);
+                h->launches += 1;
+                return h->nccl ? halo_exchange_nccl<T4>(h, xo) : SS_OK;
+            };
+            int rc = stage_at(1, rk4_kernel<F32, 1, LAYOUT>, Xc, V, XA, VS);
+            if (!rc) rc = stage_at(2, rk4_kernel<F32, 2, LAYOUT>, XA, VS, XB, VS);
+            if (!rc) rc = stage_at(3, rk4_kernel<F32, 3, LAYOUT>, XB, VS, XA, VS);
+            if (!rc) rc = stage_at(4, rk4_kernel<F32, 4, LAYOUT>, XA, VS, Xc, V);
+            if (rc) return rc;
         }
     }
     CK(cudaGetLastError());
@@ -2468,7 +2479,6 @@ int ss_step_sampled(ss_engine *h, int64_t count, int64_t sample_every, const int
     if (!h || count < 0 || sample_every < 1 || n_ids < 0 || (n_ids && !ids) || max_rows < 0 || !rows_out)
         return ss::fail(SS_EINVAL, "ss_step_sampled: bad arguments");
     if (h->energy_springs < 0) return ss::fail(SS_EINVAL, "ss_step_sampled: call ss_energy_setup first");
-    if (h->integrator == SS_RK4 && h->nccl) return ss::fail(SS_EINVAL, "ss_step_sampled: not for sharded RK4");
     CK(cudaSetDevice(h->device));
     int rc = sync_pending(h);
     if (rc) return rc;
@@ -2811,7 +2821,6 @@ extern "C" int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *sen
                              const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,
                              int64_t n_recv_hi, const int64_t *recv_hi) {
     if (!h) return ss::fail(SS_EINVAL, "null engine");
-    if (h->integrator == SS_RK4) return ss::fail(SS_EINVAL, "halo exchange supports Euler and Verlet");
     CK(cudaSetDevice(h->device));
     const int64_t ns[2] = {n_send_lo, n_send_hi}, nr[2] = {n_recv_lo, n_recv_hi};
     const int64_t *sid[2] = {send_lo, send_hi}, *rid[2] = {recv_lo, recv_hi};
@@ -2893,7 +2902,8 @@ static_assert(sizeof(MailboxBlob) <= 256, "mailbox blob must fit 256 bytes");
 int ensure_mailbox(ss_engine *h) {
     if (h->mailbox) return SS_OK;
     if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
-    if (h->integrator == SS_RK4) return ss::fail(SS_EINVAL, "halo exchange supports Euler and Verlet");
+    if (h->integrator == SS_RK4)
+        return ss::fail(SS_EINVAL, "the peer-memory halo exchange supports Euler and Verlet (RK4: NCCL or copy transport)");
     int rc = h->alloc(&h->mailbox, kMailboxHead);
     if (rc) return rc;
     MailboxHead head{};
@@ -3084,13 +3094,9 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             break;
         }
     }
-    for (int64_t s = 0; s < count && rc == SS_OK; ++s) {
-        for (int k = 0; k < n && rc == SS_OK; ++k) {
-            rc = dispatch_steps(hs[k], 1);
-            hs[k]->n += 1;
-            hs[k]->t = (double)hs[k]->n * hs[k]->dt;
-        }
-        if (p2p) continue;           // the step kernels exchanged the planes themselves
+    // the planes between neighbouring shards: buf(engine) is the position
+    // buffer that just changed (the current state, or an RK4 stage's output)
+    auto copy_planes = [&](auto buf) {
         for (int k = 0; k + 1 < n && rc == SS_OK; ++k) {
             ss_engine *a = hs[k], *b = hs[k + 1];
             const int na = a->halo_n_send[1], nb = b->halo_n_send[0];
@@ -3098,19 +3104,52 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
                 rc = ss::fail(SS_EINVAL, "ss_step_group: halo sizes of shards %d/%d disagree", k, k + 1);
                 break;
             }
+            void *xa = buf(a), *xb = buf(b);
             if (f32) {
                 halo_copy_kernel<float4><<<(na + 255) / 256, 256, 0, a->stream>>>(
-                    (const float4 *)a->X[a->cur], a->halo_send_idx[1], (float4 *)b->X[b->cur], b->halo_recv_idx[0], na);
+                    (const float4 *)xa, a->halo_send_idx[1], (float4 *)xb, b->halo_recv_idx[0], na);
                 halo_copy_kernel<float4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
-                    (const float4 *)b->X[b->cur], b->halo_send_idx[0], (float4 *)a->X[a->cur], a->halo_recv_idx[1], nb);
+                    (const float4 *)xb, b->halo_send_idx[0], (float4 *)xa, a->halo_recv_idx[1], nb);
             } else {
                 halo_copy_kernel<double4><<<(na + 255) / 256, 256, 0, a->stream>>>(
-                    (const double4 *)a->X[a->cur], a->halo_send_idx[1], (double4 *)b->X[b->cur], b->halo_recv_idx[0], na);
+                    (const double4 *)xa, a->halo_send_idx[1], (double4 *)xb, b->halo_recv_idx[0], na);
                 halo_copy_kernel<double4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
-                    (const double4 *)b->X[b->cur], b->halo_send_idx[0], (double4 *)a->X[a->cur], a->halo_recv_idx[1], nb);
+                    (const double4 *)xb, b->halo_send_idx[0], (double4 *)xa, a->halo_recv_idx[1], nb);
             }
             a->launches += 2;
         }
+    };
+    const bool rk4 = hs[0]->integrator == SS_RK4;
+    for (int k = 0; k < n && rc == SS_OK; ++k)
+        if ((hs[k]->integrator == SS_RK4) != rk4) rc = ss::fail(SS_EINVAL, "ss_step_group: mix of RK4 and other integrators");
+    for (int64_t s = 0; s < count && rc == SS_OK; ++s) {
+        if (rk4) {
+            // stage by stage across the shards: each stage's trial positions
+            // reach the neighbours' halos before the next stage reads them
+            // (stages 1 and 3 write XA, 2 writes XB, 4 the state)
+            for (int st = 1; st <= 4 && rc == SS_OK; ++st) {
+                for (int k = 0; k < n && rc == SS_OK; ++k) {
+                    hs[k]->rk4_stage_only = st;
+                    rc = dispatch_steps(hs[k], 1);
+                    hs[k]->rk4_stage_only = 0;
+                }
+                copy_planes([st](ss_engine *e) -> void * {
+                    return st == 2 ? e->XB : st == 4 ? e->X[e->cur] : e->XA;
+                });
+            }
+            for (int k = 0; k < n; ++k) {
+                hs[k]->n += 1;
+                hs[k]->t = (double)hs[k]->n * hs[k]->dt;
+            }
+            continue;
+        }
+        for (int k = 0; k < n && rc == SS_OK; ++k) {
+            rc = dispatch_steps(hs[k], 1);
+            hs[k]->n += 1;
+            hs[k]->t = (double)hs[k]->n * hs[k]->dt;
+        }
+        if (p2p) continue;           // the step kernels exchanged the planes themselves
+        copy_planes([](ss_engine *e) -> void * { return e->X[e->cur]; });
     }
     if (rc == SS_OK) {
         cudaError_t e = cudaGetLastError();

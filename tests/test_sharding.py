@@ -112,10 +112,41 @@ def test_virtual_shards_match_single_device(precision, shards):
 
 
 @pytest.mark.gpu
-def test_nccl_transport_self_loop():
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("shards", [2, 3])
+def test_virtual_shards_rk4(precision, shards):
+    """Sharded RK4 (four exchanges per step): every stage's trial
+    positions reach the neighbours' halos before the next stage.  fp64
+    bitwise against one engine; fp32 to rounding."""
+    cells = 9
+    full = L.excite(L.block_scene(cells), seed=11)
+    v = excited_velocities(full.mass_count)
+    one = Engine(full, integrator="rk4", precision=precision)
+    grp = ShardGroup(cells, shards, precision=precision, v_global=v, integrator="rk4")
+    for n in (1, 12):
+        one.step(n)
+        grp.step(n)
+        if precision == "f64":
+            assert grp.positions().tobytes() == one.x.tobytes()
+            assert grp.velocities().tobytes() == one.v.tobytes()
+        else:
+            disp = np.abs(one.x - full.x).max()
+            assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
+
+
+@pytest.mark.gpu
+def test_rk4_refuses_the_peer_memory_transport():
+    with pytest.raises(Exception, match="RK4: NCCL or copy transport"):
+        ShardGroup(5, 2, precision="f64", transport="p2p", integrator="rk4")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("integrator", ["verlet", "rk4"])
+def test_nccl_transport_self_loop(integrator):
     """Exercise the NCCL path on one GPU: a single rank whose lower and upper
     'neighbours' are itself.  After a step, each halo plane must hold the
-    positions of the plane it is wired to (transport + pack/unpack check)."""
+    positions of the plane it is wired to (transport + pack/unpack check;
+    RK4 exchanges after each of its four stages)."""
     import ctypes as C
 
     import torch  # noqa: F401  (loads libnccl.so.2 into the process)
@@ -127,13 +158,16 @@ def test_nccl_transport_self_loop():
     s = cube_slab(cells, 1, nx - 1, v_global=excited_velocities(nx ** 3))
     # fp64: absolute positions travel (in fp32 only the displacement r does,
     # which is consistent only between the two copies of the SAME mass)
-    eng = Engine(s.scene, precision="f64")
+    eng = Engine(s.scene, precision="f64", integrator=integrator)
     attach_halo(eng, s)
     uid = C.create_string_buffer(128)
     _lib.check(_lib.lib().ss_nccl_unique_id(uid))
     _lib.check(_lib.lib().ss_halo_nccl(eng.handle, uid.raw, 1, 0, 0, 0))
+    n0 = eng.launch_count
     eng.step(3)
     x = eng.x
+    # per step: the stage kernels plus a pack and an unpack per exchange
+    assert eng.launch_count - n0 == 3 * (4 * 3 if integrator == "rk4" else 3)
     assert x[s.recv_lo].tobytes() == x[s.send_lo].tobytes()
     assert x[s.recv_hi].tobytes() == x[s.send_hi].tobytes()
 
@@ -333,9 +367,9 @@ def _assemble(grp):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["copy", "p2p"])
+@pytest.mark.parametrize("transport,integrator", [("copy", "verlet"), ("p2p", "verlet"), ("copy", "euler"),
+                                                  ("p2p", "euler"), ("copy", "rk4")])
 @pytest.mark.parametrize("shards", [2, 3])
-@pytest.mark.parametrize("integrator", ["verlet", "euler"])
 def test_sharded_beam_bitwise(transport, shards, integrator):
     """configs[0]'s loaded cantilever split into x-slabs (fixed root,
     gravity, tip load, damping): fp64 bitwise equal to one engine."""
