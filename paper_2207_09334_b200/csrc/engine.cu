@@ -2172,7 +2172,7 @@ namespace {
 // (TMA, halo gather) is the same.  DESIGN.md §4.
 template <bool F32, int LAYOUT>
 int setup_persistent_ly(ss_engine *h) {
-    if (h->integrator == SS_RK4) return SS_OK;
+    if (h->integrator == SS_RK4 || h->tl.inline_kl) return SS_OK;   // (persist_lean_kernel: dictionary tiles)
     const char *e = getenv("SS_PERSIST");
     if (!e || atoi(e) == 0) return SS_OK;
     int sms = 0, dev_max = 0;
