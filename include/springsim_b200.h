@@ -274,7 +274,7 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
  *   - ss_step_group: several shards on one device stepped in lockstep, the
  *     planes copied device-to-device (RK4: stage by stage) or, when
  *     peer-linked, exchanged by the step kernels (virtual shards, for
- *     testing).  The peer-memory transport is Euler/Verlet only.
+ *     testing).  RK4 exchanges after every stage on every transport.
  */
 int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
                   const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,

@@ -175,6 +175,7 @@ struct ss_engine {
     void *mailbox = nullptr;
     void *peer_mailbox[2] = {nullptr, nullptr};
     void *peer_X[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][buffer]
+    void *peer_XA[2] = {nullptr, nullptr}, *peer_XB[2] = {nullptr, nullptr};   // RK4: the stage buffers
     bool peer_ipc[2] = {false, false};
     std::vector<int32_t> peer_recv[2];          // the neighbour's device slots for this shard's planes
     std::vector<int32_t> halo_send_host[2], halo_recv_host[2];   // this shard's plane slots
@@ -509,15 +510,21 @@ int with_layout(const ss_engine *h, Fn &&fn) {
 // write the received planes into the halo slots.
 // Exchange fields of one step's Params (fused peer-memory transport): the
 // neighbours' buffers for this step's output parity, the flag words.
+// RK4 (stage 1-4): the neighbours' buffer for this stage's trial positions
+// (XA, XB, XA, then the state), sequence number 4 (step - 1) + stage.
 template <typename T>
-void xchg_params(const ss_engine *h, Params<T> &p) {
+void xchg_params(const ss_engine *h, Params<T> &p, int stage = 0) {
     using T4 = typename Params<T>::T4;
     MailboxHead *mine = reinterpret_cast<MailboxHead *>(h->mailbox);
     p.xchg = 1;
+    p.xseq = stage ? 4 * (p.step - 1) + stage : p.step;
     p.tile_role = h->d_tile_role;
     p.peer_slot = h->d_peer_slot;
     for (int s = 0; s < 2; ++s) {
-        p.peer_out[s] = h->peer_mailbox[s] ? reinterpret_cast<T4 *>(h->peer_X[s][h->cur ^ 1]) : nullptr;
+        void *out = stage == 0 ? h->peer_X[s][h->cur ^ 1]
+                  : stage == 4 ? h->peer_X[s][h->cur]
+                  : stage == 2 ? h->peer_XB[s] : h->peer_XA[s];
+        p.peer_out[s] = h->peer_mailbox[s] ? reinterpret_cast<T4 *>(out) : nullptr;
         p.peer_flag[s] = h->peer_mailbox[s] ? &reinterpret_cast<MailboxHead *>(h->peer_mailbox[s])->flag[1 - s]
                                             : nullptr;
         p.my_flag[s] = &mine->flag[s];
@@ -885,7 +892,7 @@ int launch_steps(ss_engine *h, int64_t count) {
     }
     for (int64_t s = 0; s < count; ++s) {
         p.step = h->n + s + 1;
-        if (h->p2p_on) xchg_params(h, p);                  // fused peer-memory exchange (kernels.cuh)
+        if (h->p2p_on && h->integrator != SS_RK4) xchg_params(h, p);   // fused peer-memory exchange (kernels.cuh)
         T4 *Xc = reinterpret_cast<T4 *>(h->X[h->cur]);
         T4 *Xo = reinterpret_cast<T4 *>(h->X[h->cur ^ 1]);
         T4 *V = reinterpret_cast<T4 *>(h->V);
@@ -970,6 +977,7 @@ int launch_steps(ss_engine *h, int64_t count) {
                 }
                 p.scale = G ? scale + ((size_t)s * 4 + (st - 1)) * G : nullptr;
                 p.X = x; p.V = v; p.Xout = xo; p.Vout = vo;
+                if (h->p2p_on) xchg_params(h, p, st);      // fused: pushes into the neighbours' stage buffer
                 rk4_launch(k);
                 h->launches += 1;
                 return h->nccl ? halo_exchange_nccl<T4>(h, xo) : SS_OK;
@@ -1342,7 +1350,11 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         CK(cudaMemsetAsync(h->U, 0, (size_t)ND * sizeof(T4), h->stream));
     }
     if (h->integrator == SS_RK4) {
-        for (void **b : {&h->XA, &h->XB, &h->VS, &h->SV, &h->SA})
+        // XA and XB in one allocation: a sharded RK4 engine exports both
+        // stage buffers to its neighbours under one IPC handle
+        if ((rc = h->alloc(&h->XA, 2 * (size_t)ND * sizeof(T4)))) return rc;
+        h->XB = static_cast<char *>(h->XA) + (size_t)ND * sizeof(T4);
+        for (void **b : {&h->VS, &h->SV, &h->SA})
             if ((rc = h->alloc(b, (size_t)ND * sizeof(T4)))) return rc;
     }
     {
@@ -2890,24 +2902,27 @@ constexpr char kMailboxMagic[8] = {'S', 'S', 'M', 'B', 'O', 'X', '0', '2'};
 struct MailboxBlob {               // what ss_halo_p2p_export hands to the neighbours (256 B)
     char magic[8];
     cudaIpcMemHandle_t mailbox;    // 64 B each
-    cudaIpcMemHandle_t x[2];       // the two position buffers
+    cudaIpcMemHandle_t x[2];       // the two position buffers (RK4: the state, then the XA|XB stage block)
     int64_t n_recv[2];
     int64_t vec;
     int64_t n;
     int32_t cur;
     int32_t device;
+    int32_t integrator;
+    int32_t pad;
+    int64_t xb_off;                // RK4: XB's byte offset in the stage block
 };
 static_assert(sizeof(MailboxBlob) <= 256, "mailbox blob must fit 256 bytes");
 
 int ensure_mailbox(ss_engine *h) {
     if (h->mailbox) return SS_OK;
     if (!h->halo_on) return ss::fail(SS_EINVAL, "call ss_halo_setup first");
-    if (h->integrator == SS_RK4)
-        return ss::fail(SS_EINVAL, "the peer-memory halo exchange supports Euler and Verlet (RK4: NCCL or copy transport)");
+    if (h->integrator == SS_RK4 && h->cur != 0) return ss::fail(SS_EINVAL, "RK4 halo: unexpected buffer parity");
     int rc = h->alloc(&h->mailbox, kMailboxHead);
     if (rc) return rc;
     MailboxHead head{};
-    head.flag[0] = head.flag[1] = (long long)h->n;          // the halos match the current state
+    // the halos match the current state: its sequence number (RK4: four per step)
+    head.flag[0] = head.flag[1] = (long long)h->n * (h->integrator == SS_RK4 ? 4 : 1);
     CK(cudaMemset(h->mailbox, 0, kMailboxHead));
     CK(cudaMemcpy(h->mailbox, &head, sizeof head, cudaMemcpyHostToDevice));
     return SS_OK;
@@ -2964,11 +2979,13 @@ int build_xchg(ss_engine *h) {
     return upload(h, h->d_tile_role, role.data(), role.size());
 }
 
-int link_side(ss_engine *h, int side, void *peer_mailbox, void *peer_x0, void *peer_x1, bool ipc,
-              const int64_t peer_n_recv[2], int64_t vec, int64_t n, int cur, const int32_t *peer_slots,
-              int64_t n_slots) {
+// peer_xa / peer_xb: the neighbour's RK4 stage buffers (null unless RK4).
+int link_side(ss_engine *h, int side, void *peer_mailbox, void *peer_x0, void *peer_x1, void *peer_xa,
+              void *peer_xb, int integrator, bool ipc, const int64_t peer_n_recv[2], int64_t vec, int64_t n,
+              int cur, const int32_t *peer_slots, int64_t n_slots) {
     const int64_t my_vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
     if (vec != my_vec) return ss::fail(SS_EINVAL, "halo peer: precision differs");
+    if (integrator != h->integrator) return ss::fail(SS_EINVAL, "halo peer: integrator differs");
     if (n != h->n || cur != h->cur) return ss::fail(SS_EINVAL, "halo peer: shards are not at the same step");
     if (peer_n_recv[1 - side] != h->halo_n_send[side] || n_slots != h->halo_n_send[side])
         return ss::fail(SS_EINVAL, "halo peer: plane sizes disagree (%lld received, %d sent)",
@@ -2976,6 +2993,8 @@ int link_side(ss_engine *h, int side, void *peer_mailbox, void *peer_x0, void *p
     h->peer_mailbox[side] = peer_mailbox;
     h->peer_X[side][0] = peer_x0;
     h->peer_X[side][1] = peer_x1;
+    h->peer_XA[side] = peer_xa;
+    h->peer_XB[side] = peer_xb;
     h->peer_ipc[side] = ipc;
     h->peer_recv[side].assign(peer_slots, peer_slots + n_slots);
     h->p2p_on = true;
@@ -2993,7 +3012,9 @@ extern "C" int ss_halo_p2p_export(ss_engine *h, unsigned char blob[256]) {
     std::memcpy(b.magic, kMailboxMagic, 8);
     CK(cudaIpcGetMemHandle(&b.mailbox, h->mailbox));
     CK(cudaIpcGetMemHandle(&b.x[0], h->X[0]));
-    CK(cudaIpcGetMemHandle(&b.x[1], h->X[1]));
+    CK(cudaIpcGetMemHandle(&b.x[1], h->integrator == SS_RK4 ? h->XA : h->X[1]));
+    b.integrator = h->integrator;
+    b.xb_off = h->integrator == SS_RK4 ? static_cast<char *>(h->XB) - static_cast<char *>(h->XA) : 0;
     b.n_recv[0] = h->halo_n_recv[0];
     b.n_recv[1] = h->halo_n_recv[1];
     b.vec = h->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
@@ -3033,7 +3054,12 @@ extern "C" int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char bl
                             cudaGetErrorString(e));
         }
     }
-    rc = link_side(h, side, pm[0], pm[1], pm[2], true, b.n_recv, b.vec, b.n, b.cur, peer_slots, n_slots);
+    // (an RK4 neighbour's second handle is its XA|XB stage block; RK4 never
+    // pushes into the other parity of its state)
+    const bool rk4 = b.integrator == SS_RK4;
+    rc = link_side(h, side, pm[0], pm[1], pm[2], rk4 ? pm[2] : nullptr,
+                   rk4 ? static_cast<char *>(pm[2]) + b.xb_off : nullptr, b.integrator, true, b.n_recv, b.vec,
+                   b.n, b.cur, peer_slots, n_slots);
     if (rc)
         for (void *q : pm) cudaIpcCloseMemHandle(q);
     return rc;
@@ -3060,8 +3086,8 @@ extern "C" int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer) {
     const int64_t pnr[2] = {peer->halo_n_recv[0], peer->halo_n_recv[1]};
     const int64_t vec = peer->precision == SS_F32 ? (int64_t)sizeof(float4) : (int64_t)sizeof(double4);
     const std::vector<int32_t> &slots = peer->halo_recv_host[1 - side];
-    return link_side(h, side, peer->mailbox, peer->X[0], peer->X[1], false, pnr, vec, peer->n, peer->cur,
-                     slots.data(), (int64_t)slots.size());
+    return link_side(h, side, peer->mailbox, peer->X[0], peer->X[1], peer->XA, peer->XB, peer->integrator, false,
+                     pnr, vec, peer->n, peer->cur, slots.data(), (int64_t)slots.size());
 }
 
 // Step n same-device shards in lockstep; shard k's upper side is shard k+1's
@@ -3133,9 +3159,10 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
                     rc = dispatch_steps(hs[k], 1);
                     hs[k]->rk4_stage_only = 0;
                 }
-                copy_planes([st](ss_engine *e) -> void * {
-                    return st == 2 ? e->XB : st == 4 ? e->X[e->cur] : e->XA;
-                });
+                if (!p2p)                                  // (peer-linked: the stage kernels pushed them)
+                    copy_planes([st](ss_engine *e) -> void * {
+                        return st == 2 ? e->XB : st == 4 ? e->X[e->cur] : e->XA;
+                    });
             }
             for (int k = 0; k < n; ++k) {
                 hs[k]->n += 1;

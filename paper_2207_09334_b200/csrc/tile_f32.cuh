@@ -54,7 +54,7 @@ __device__ __forceinline__ float spring_c(float dx, float dy, float dz, float k,
 // kernel's spring sum.  X0/V0 step start, SV/SA running sums.
 template <int STAGE>
 __device__ __forceinline__ void rk4_store(const Params<float> &p, int m, V3<float> sum, const float4 &x4,
-                                          const float4 &p4, const float4 &vs4) {
+                                          const float4 &p4, const float4 &vs4, int tile) {
     const float4 x04 = p.X0[m];
     const float mass = fabsf(x04.w);
     const bool fixed = signbit(x04.w);
@@ -99,7 +99,9 @@ __device__ __forceinline__ void rk4_store(const Params<float> &p, int m, V3<floa
 #pragma unroll
         for (int c = 0; c < 3; ++c) { xn[c] = x0[c]; vn[c] = v0[c]; }
     }
-    p.Xout[m] = make_float4(xn[0], xn[1], xn[2], x04.w);
+    const float4 xo = make_float4(xn[0], xn[1], xn[2], x04.w);
+    if (!xchg_store(p, m, xo, tile)) return;                // a ghost: its neighbour writes this stage's trial x
+    p.Xout[m] = xo;
     p.Vout[m] = make_float4(vn[0], vn[1], vn[2], 0.f);
     if constexpr (STAGE == 1) {
         p.SA[m] = make_float4(sa[0], sa[1], sa[2], 0.f);
@@ -118,7 +120,7 @@ __device__ __forceinline__ void integrate_store(const Params<float> &p, int m, V
                                                 float4 p4, float4 v4, float4 xp4, bool need_prev,
                                                 int tile = blockIdx.x) {
     if constexpr (INTEG >= 2) {
-        rk4_store<INTEG - 1>(p, m, sum, x4, p4, v4);
+        rk4_store<INTEG - 1>(p, m, sum, x4, p4, v4, tile);
         return;
     }
     const float mass = fabsf(x4.w);

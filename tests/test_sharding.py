@@ -112,17 +112,20 @@ def test_virtual_shards_match_single_device(precision, shards):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["copy", "p2p"])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 @pytest.mark.parametrize("shards", [2, 3])
-def test_virtual_shards_rk4(precision, shards):
+def test_virtual_shards_rk4(precision, shards, transport):
     """Sharded RK4 (four exchanges per step): every stage's trial
-    positions reach the neighbours' halos before the next stage.  fp64
-    bitwise against one engine; fp32 to rounding."""
+    positions reach the neighbours' halos before the next stage -- plane
+    copies between stages, or pushed by the stage kernels themselves into
+    the neighbours' stage buffers (p2p).  fp64 bitwise against one engine;
+    fp32 to rounding."""
     cells = 9
     full = L.excite(L.block_scene(cells), seed=11)
     v = excited_velocities(full.mass_count)
     one = Engine(full, integrator="rk4", precision=precision)
-    grp = ShardGroup(cells, shards, precision=precision, v_global=v, integrator="rk4")
+    grp = ShardGroup(cells, shards, precision=precision, v_global=v, integrator="rk4", transport=transport)
     for n in (1, 12):
         one.step(n)
         grp.step(n)
@@ -132,12 +135,6 @@ def test_virtual_shards_rk4(precision, shards):
         else:
             disp = np.abs(one.x - full.x).max()
             assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
-
-
-@pytest.mark.gpu
-def test_rk4_refuses_the_peer_memory_transport():
-    with pytest.raises(Exception, match="RK4: NCCL or copy transport"):
-        ShardGroup(5, 2, precision="f64", transport="p2p", integrator="rk4")
 
 
 @pytest.mark.gpu
@@ -197,7 +194,7 @@ def test_peer_memory_shards_match_single_device(precision, layout, shards):
         assert np.abs(grp.positions() - one.x).max() <= 1e-4 * disp
 
 
-def _ipc_worker(rank, world, port, cells, steps, precision, q):
+def _ipc_worker(rank, world, port, cells, steps, precision, q, integrator="verlet"):
     """One shard per process, all on cuda:0: the cross-process (CUDA IPC)
     mailbox mapping and the device-side flag protocol, as under torchrun."""
     try:
@@ -208,7 +205,7 @@ def _ipc_worker(rank, world, port, cells, steps, precision, q):
         nx = cells + 1
         s = cube_slab(cells, *slab_planes(nx, world, rank),
                       v_global=excited_velocities(nx ** 3))
-        eng = Engine(s.scene, integrator="verlet", precision=precision, device=0)
+        eng = Engine(s.scene, integrator=integrator, precision=precision, device=0)
         attach_halo(eng, s)
         attach_peers(eng, rank, world)
         for _ in range(steps // 7):
@@ -224,22 +221,24 @@ def _ipc_worker(rank, world, port, cells, steps, precision, q):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_memory_shards_across_processes(world):
+@pytest.mark.parametrize("world,integrator", [(2, "verlet"), (3, "verlet"), (3, "rk4")])
+def test_peer_memory_shards_across_processes(world, integrator):
     """Two or three processes, one shard each, sharing one GPU (with three,
     the middle shard exchanges with two neighbours): mailboxes mapped with
-    cudaIpcOpenMemHandle, planes pushed and landed every substep with no host
-    round trip; the assembled fp64 state is bitwise the single engine's."""
+    cudaIpcOpenMemHandle, planes pushed and landed every substep (RK4: every
+    stage, into the neighbours' IPC-mapped stage buffers) with no host round
+    trip; the assembled fp64 state is bitwise the single engine's."""
     cells, steps = 9, 30
     full = L.excite(L.block_scene(cells), seed=11)
-    one = Engine(full, precision="f64")
+    one = Engine(full, precision="f64", integrator=integrator)
     one.step(steps)
     ref_x, ref_v = one.x.copy(), one.v.copy()
     one.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 2000) + 7 + world
-    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, cells, steps, "f64", q)) for r in range(world)]
+    port = 29500 + (os.getpid() % 2000) + 7 + world + (20 if integrator == "rk4" else 0)
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, cells, steps, "f64", q, integrator))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=500) for _ in procs], key=lambda t: t[1])
@@ -368,7 +367,7 @@ def _assemble(grp):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("transport,integrator", [("copy", "verlet"), ("p2p", "verlet"), ("copy", "euler"),
-                                                  ("p2p", "euler"), ("copy", "rk4")])
+                                                  ("p2p", "euler"), ("copy", "rk4"), ("p2p", "rk4")])
 @pytest.mark.parametrize("shards", [2, 3])
 def test_sharded_beam_bitwise(transport, shards, integrator):
     """configs[0]'s loaded cantilever split into x-slabs (fixed root,

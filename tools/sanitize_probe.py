@@ -29,9 +29,11 @@ def main():
                 assert np.isfinite(e.x).all()
                 print(name, prec, integ, e.info()["tile_kernel"], flush=True)
     for integ in ("verlet", "rk4"):
-        g = ShardGroup(9, 2, precision="f64", v_global=excited_velocities(1000), integrator=integ)
-        g.step(3)
-        print("shards", integ, flush=True)
+        for transport in ("copy", "p2p"):
+            g = ShardGroup(9, 2, precision="f64", v_global=excited_velocities(1000), integrator=integ,
+                           transport=transport)
+            g.step(3)
+            print("shards", integ, transport, flush=True)
 
 
 if __name__ == "__main__":
