@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 
 /* status codes */
 #define SS_OK             0
@@ -275,6 +275,9 @@ int ss_lattice_box(const double lo[3], const double hi[3], double dim,
  *     planes copied device-to-device (RK4: stage by stage) or, when
  *     peer-linked, exchanged by the step kernels (virtual shards, for
  *     testing).  RK4 exchanges after every stage on every transport.
+ *     The shards share one divergence step: all stop after the first
+ *     non-finite step anywhere; *diverged_shard (may be null) names the
+ *     lowest shard that flagged it and res->diverged_mass its local id.
  */
 int ss_halo_setup(ss_engine *h, int64_t n_send_lo, const int64_t *send_lo, int64_t n_send_hi,
                   const int64_t *send_hi, int64_t n_recv_lo, const int64_t *recv_lo,
@@ -286,7 +289,7 @@ int ss_halo_recv_slots(ss_engine *h, int side, int32_t *out);
 int ss_halo_p2p_attach(ss_engine *h, int side, const unsigned char blob[256], const int32_t *peer_slots,
                        int64_t n_slots);
 int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer);
-int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res);
+int ss_step_group(ss_engine **engines, int n, int64_t count, ss_step_result *res, int32_t *diverged_shard);
 
 /* Engine.gpe_datum (engine.py:240-242): the height GPE is measured from,
  * read by every later on-device energy sample (service.py:462 and

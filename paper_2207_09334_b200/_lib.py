@@ -101,7 +101,8 @@ SIGNATURES = {
     "ss_halo_recv_slots": (C.c_int, [C.c_void_p, C.c_int, _i32p]),
     "ss_halo_p2p_attach": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _i32p, C.c_int64]),
     "ss_halo_p2p_link": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
-    "ss_step_group": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.POINTER(StepResult)]),
+    "ss_step_group": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.POINTER(StepResult),
+                              C.POINTER(C.c_int32)]),
     "ss_lattice_box": (C.c_int, [_dp, _dp, C.c_double, C.c_double, C.c_double,
                                  C.c_int64, C.c_int64, _i64p, _i64p, _i64p,
                                  _dp, _i64p, _i64p, _dp, _dp, _i64p]),
@@ -149,7 +150,7 @@ def lib():
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args
-            if handle.ss_abi_version() != 1:
+            if handle.ss_abi_version() != 2:
                 raise LibraryMissing("libspringsim_b200.so ABI version mismatch; rebuild it")
             _lib = handle
         return _lib

@@ -169,6 +169,7 @@ struct ss_engine {
     int nccl_peer[2] = {-1, -1};
     int64_t halo_exchanges = 0;
     int rk4_stage_only = 0;        // ss_step_group: launch only this RK4 stage (1-4) of a one-step batch
+    long long *group_div_step = nullptr;   // ss_step_group: the group's shared divergence step word
     // fused peer-memory exchange (kernels.cuh xchg_*): own flag mailbox, the
     // neighbours' mailboxes and position buffers (IPC-mapped or, for shards of
     // one process, plain), their slots for this shard's planes
@@ -487,7 +488,7 @@ Params<T> base_params(const ss_engine *h) {
         p.pfric[q] = (T)h->planes[6 * q + 5];
     }
     p.degenerate = h->d_degenerate;
-    p.div_step = h->d_div_step;
+    p.div_step = h->group_div_step ? h->group_div_step : h->d_div_step;
     p.div_mass = h->d_div_mass;
     if (const char *dbg = getenv("SS_DEBUG")) p.debug = atoi(dbg);   // timing experiments only
     return p;
@@ -3090,9 +3091,64 @@ extern "C" int ss_halo_p2p_link(ss_engine *h, int side, ss_engine *peer) {
                      pnr, vec, peer->n, peer->cur, slots.data(), (int64_t)slots.size());
 }
 
+namespace {
+
+// After a group batch: the shared divergence step decides how many steps
+// every shard committed; the lowest shard whose own mass word was set names
+// the mass (shards hold increasing global ids, and within a shard the word
+// holds the lowest caller id).
+int finish_group(ss_engine **hs, int n, int64_t count, const std::vector<int64_t> &n0, const std::vector<int> &cur0,
+                 ss_step_result *res, int32_t *diverged_shard) {
+    CK(cudaSetDevice(hs[0]->device));
+    CK(cudaStreamSynchronize(hs[0]->stream));
+    for (int k = 0; k < n; ++k) {
+        if (!hs[k]->p2p_on) continue;
+        int err = 0;
+        CK(cudaMemcpy(&err, &reinterpret_cast<MailboxHead *>(hs[k]->mailbox)->error, sizeof err,
+                      cudaMemcpyDeviceToHost));
+        if (err) return ss::fail(SS_ECUDA, "halo exchange: a neighbour did not publish its boundary planes within 20 s");
+    }
+    long long dstep = LLONG_MAX;
+    CK(cudaMemcpy(&dstep, hs[0]->d_div_step, sizeof dstep, cudaMemcpyDeviceToHost));
+    int shard = -1, dmass = INT_MAX;
+    for (int k = 0; k < n; ++k) {
+        int mk = INT_MAX;
+        CK(cudaMemcpy(&mk, hs[k]->d_div_mass, sizeof mk, cudaMemcpyDeviceToHost));
+        if (mk != INT_MAX && shard < 0) {
+            shard = k;
+            dmass = mk;
+        }
+        ss_engine *h = hs[k];
+        const int64_t done = dstep != LLONG_MAX ? (int64_t)dstep - n0[k] : count;
+        h->n = n0[k] + done;
+        h->t = (double)h->n * h->dt;
+        if (h->integrator != SS_RK4) h->cur = cur0[k] ^ (int)(done & 1);
+        if (dstep != LLONG_MAX) {
+            int rc = reset_divergence(h);
+            if (rc) return rc;
+        }
+    }
+    if (res) {
+        res->steps_done = dstep != LLONG_MAX ? (int64_t)dstep - n0[0] : count;
+        res->n = hs[0]->n;
+        res->t = hs[0]->t;
+        res->diverged_mass = dstep != LLONG_MAX ? dmass : -1;
+        res->diverged_step = dstep != LLONG_MAX ? (int64_t)dstep : -1;
+    }
+    if (diverged_shard) *diverged_shard = dstep != LLONG_MAX ? shard : -1;
+    if (dstep != LLONG_MAX)
+        return ss::fail(SS_EDIVERGED,
+                        "simulation diverged at step %lld: mass %d of shard %d has a non-finite position or "
+                        "velocity (try a smaller dt)",
+                        dstep, dmass, shard);
+    return SS_OK;
+}
+
+}  // namespace
+
 // Step n same-device shards in lockstep; shard k's upper side is shard k+1's
 // lower side.  All work is serialised on shard 0's stream.
-extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_result *res) {
+extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_result *res, int32_t *diverged_shard) {
     if (!hs || n <= 0) return ss::fail(SS_EINVAL, "ss_step_group: no engines");
     for (int k = 0; k < n; ++k) {
         if (!hs[k] || !hs[k]->halo_on) return ss::fail(SS_EINVAL, "ss_step_group: engine %d has no halo", k);
@@ -3145,6 +3201,9 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
             a->launches += 2;
         }
     };
+    // one divergence step for the whole group (shard 0's word): every shard
+    // retires after the first non-finite step anywhere, like one engine
+    for (int k = 1; k < n; ++k) hs[k]->group_div_step = hs[0]->d_div_step;
     const bool rk4 = hs[0]->integrator == SS_RK4;
     for (int k = 0; k < n && rc == SS_OK; ++k)
         if ((hs[k]->integrator == SS_RK4) != rk4) rc = ss::fail(SS_EINVAL, "ss_step_group: mix of RK4 and other integrators");
@@ -3178,23 +3237,15 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
         if (p2p) continue;           // the step kernels exchanged the planes themselves
         copy_planes([](ss_engine *e) -> void * { return e->X[e->cur]; });
     }
+    for (int k = 0; k < n; ++k) hs[k]->group_div_step = nullptr;
+    if (diverged_shard) *diverged_shard = -1;
     if (rc == SS_OK) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = ss::fail(SS_ECUDA, "ss_step_group: %s", cudaGetErrorString(e));
     }
-    int first_err = rc;
-    for (int k = 0; k < n; ++k) {
-        ss_step_result r{};
-        const int rk = rc == SS_OK ? finish_batch(hs[k], count, n0[k], cur0[k], &r) : SS_OK;
-        if (rk != SS_OK && first_err == SS_OK) {
-            first_err = rk;
-            if (res) *res = r;
-        } else if (k == 0 && res && rk == SS_OK) {
-            *res = r;
-        }
-    }
+    if (rc == SS_OK) rc = finish_group(hs, n, count, n0, cur0, res, diverged_shard);
     for (int k = 0; k < n; ++k) hs[k]->stream = saved[k];
-    return first_err;
+    return rc;
 }
 
 extern "C" int ss_check_f64_fastpath(int32_t device, const double *a, const double *b, int64_t n, double *out,

@@ -262,9 +262,17 @@ class ShardGroup:
             e._push_params()
         arr = (C.c_void_p * len(self.engines))(*[e.handle.value for e in self.engines])
         res = _lib.StepResult()
-        rc = _lib.lib().ss_step_group(arr, len(self.engines), int(count), C.byref(res))
+        shard = C.c_int32(-1)
+        rc = _lib.lib().ss_step_group(arr, len(self.engines), int(count), C.byref(res), C.byref(shard))
         for e in self.engines:
             e._mark_stepped()
+        if rc == _lib.SS_EDIVERGED and shard.value >= 0:
+            # every shard stopped after the same step (one shared divergence
+            # word); the lowest flagged shard names the mass, in global ids
+            slab = self.slabs[shard.value]
+            local = int(res.diverged_mass)
+            gid = int(slab.global_ids[local]) if slab.global_ids is not None else slab.first_global + local
+            raise self.engines[0]._divergence_error(gid, int(res.diverged_step))
         _lib.check(rc, "ss_step_group")
 
     def positions(self) -> np.ndarray:

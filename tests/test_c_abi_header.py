@@ -42,5 +42,5 @@ def test_header_compiles_links_and_runs(tmp_path):
                     "-L", LIBDIR, "-lspringsim_b200", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
     head, rest = out.split("\n", 1)
-    assert head.startswith("1 1|") and "no masses" in head
+    assert head.startswith("2 1|") and "no masses" in head
     assert rest == "0|0.1\n1e-05\n1e+16\n"

@@ -127,7 +127,7 @@ def test_library_exports_every_declared_symbol():
     for name in syms:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} not bound in _lib.SIGNATURES"
-    assert lib.ss_abi_version() == 1
+    assert lib.ss_abi_version() == 2
 
 
 def test_tile_plan_statistics_on_host():

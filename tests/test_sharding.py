@@ -138,6 +138,37 @@ def test_virtual_shards_rk4(precision, shards, transport):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["copy", "p2p"])
+@pytest.mark.parametrize("integrator", ["verlet", "rk4"])
+@pytest.mark.parametrize("where", ["boundary", "interior"])
+def test_sharded_divergence_matches_one_engine(transport, integrator, where):
+    """A mass launched at 1e300 m/s (its springs overflow): one engine raises DivergenceError
+    (engine.py:375-381) at some step for its lowest non-finite mass.  The
+    shards share one divergence step, so all of them stop after that same
+    step, the error names the same global mass and step, and the assembled
+    state is the single engine's diverged state."""
+    from paper_2207_09334_b200 import DivergenceError
+    cells = 9
+    full = L.excite(L.block_scene(cells), seed=11)
+    nx = cells + 1
+    plane = nx * nx
+    i = 5 if where == "boundary" else 7                     # x-plane 5 borders the 2-shard split
+    victim = i * plane + plane // 2
+    full.v[victim] = (1e300, 0.0, 0.0)
+    v = full.v.copy()
+    one = Engine(full, integrator=integrator, precision="f64")
+    with pytest.raises(DivergenceError) as e1:
+        one.step(40)
+    grp = ShardGroup(cells, 2, precision="f64", v_global=v, integrator=integrator, transport=transport)
+    with pytest.raises(DivergenceError) as e2:
+        grp.step(40)
+    assert (e2.value.mass_id, e2.value.step) == (e1.value.mass_id, e1.value.step)
+    assert all(e.n == one.n for e in grp.engines)
+    np.testing.assert_array_equal(grp.positions(), one.x)
+    np.testing.assert_array_equal(grp.velocities(), one.v)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("integrator", ["verlet", "rk4"])
 def test_nccl_transport_self_loop(integrator):
     """Exercise the NCCL path on one GPU: a single rank whose lower and upper
