@@ -827,6 +827,7 @@ int launch_steps(ss_engine *h, int64_t count) {
         const bool euler = h->integrator == SS_EULER;
         auto *k = h->res_g == 8 ? (euler ? resident_kernel<F32, 0, 8> : resident_kernel<F32, 1, 8>)
                 : h->res_g == 4 ? (euler ? resident_kernel<F32, 0, 4> : resident_kernel<F32, 1, 4>)
+                : h->res_g == 2 ? (euler ? resident_kernel<F32, 0, 2> : resident_kernel<F32, 1, 2>)
                                 : (euler ? resident_kernel<F32, 0, 1> : resident_kernel<F32, 1, 1>);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)h->res_ctas);
@@ -1240,17 +1241,21 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     // through the branch-free IEEE sequences (crawler 2.50 -> 2.14 us, 12
     // crawlers 5.72 -> 2.68, the 40x4x4 beam as a cluster 5.08 against 6.71
     // with launches).  fp32: 8 lanes with a fixed-order tree for scenes of
-    // <= 128 masses (crawler 1.03 us against 1.53 with one lane), else one
-    // lane with four partial sums (beam 3.68 -> 3.46 us, the 9^3 cube 4.47
-    // -> 3.52, 64 crawlers 3.68 -> 2.90, against 4 lanes)
-    h->res_g = F32 ? (used * 8 <= 1024 ? 8 : 1) : 1;
-    if (const char *e = getenv("SS_RESIDENT_G")) {                 // A/B: 1, 4 or 8
+    // <= 128 masses (crawler 1.03 us against 1.53 with one lane), else two
+    // lanes (64 crawlers 2.66 us against 2.90 with one lane and four partial
+    // sums, the beam 3.36 against 3.43, the 9^3 cube 3.52 against 3.48;
+    // 4 lanes: 3.68, 3.67, 4.47).  fp64 stays at one lane: a group's ordered
+    // shuffle-and-add rounds cost more than they save (beam 5.07 us with one
+    // lane, 13.5 with two, 10.8 with four; tools/resident_g_probe.py)
+    h->res_g = F32 ? (used * 8 <= 1024 ? 8 : 2) : 1;
+    if (const char *e = getenv("SS_RESIDENT_G")) {                 // A/B: 1, 2, 4 or 8
         const int g = atoi(e);
-        if ((g == 1 || g == 4 || g == 8) && used * g <= 1024) h->res_g = g;
+        if ((g == 1 || g == 2 || g == 4 || g == 8) && used * g <= 1024) h->res_g = g;
     }
     h->res_threads = (int)std::max<int64_t>(32, (used * h->res_g + 31) / 32 * 32);
     for (const void *fn : {(const void *)resident_kernel<F32, 0, 4>, (const void *)resident_kernel<F32, 1, 4>,
                            (const void *)resident_kernel<F32, 0, 8>, (const void *)resident_kernel<F32, 1, 8>,
+                           (const void *)resident_kernel<F32, 0, 2>, (const void *)resident_kernel<F32, 1, 2>,
                            (const void *)resident_kernel<F32, 0, 1>, (const void *)resident_kernel<F32, 1, 1>}) {
         // per-function attributes are shared by every engine in the process:
         // grant the device maximum, never this engine's size
@@ -1274,6 +1279,7 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
         int clusters = 0;
         const bool e0 = h->integrator == SS_EULER;
         const void *fn = h->res_g == 1 ? (e0 ? (const void *)resident_kernel<F32, 0, 1> : (const void *)resident_kernel<F32, 1, 1>)
+                       : h->res_g == 2 ? (e0 ? (const void *)resident_kernel<F32, 0, 2> : (const void *)resident_kernel<F32, 1, 2>)
                                        : (e0 ? (const void *)resident_kernel<F32, 0, 4> : (const void *)resident_kernel<F32, 1, 4>);
         if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess || clusters < 1) {
             cudaGetLastError();

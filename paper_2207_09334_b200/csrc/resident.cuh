@@ -255,15 +255,29 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
                 }
                 const double4 xo = xs[e & 0xfffu];
                 const double dx = xo.x - x4.x, dy = xo.y - x4.y, dz = xo.z - x4.z;
-                const double len = sqrt((dx * dx + dy * dy) + dz * dz);
-                if (len < 1e-12) {                          // skipped and counted (_kernels.py:58-60)
-                    if (e & 0x1000u) ++deg;
-                } else {
-                    const double c = spring_c64(kl.x, len, l0);
+                const double d2 = (dx * dx + dy * dy) + dz * dz;
+                // the branch-free IEEE fast paths (tile_f64.cuh); a term outside
+                // them is redone with the library operators -- terms are
+                // independent, so the redo is per incidence
+                bool ok_s, ok_d;
+                const double lf = sqrt_rn_fast(d2, ok_s);
+                const double num = kl.x * (lf - l0);
+                double c = div_rn_fast(num, lf, ok_d);
+                const bool zero = (__double2hiint(num) & 0x7fffffff) == 0 && __double2loint(num) == 0;
+                add = ok_s && (ok_d || zero) && __double2hiint(lf) > kDegenerateHi;
+                if (!add) {
+                    const double len = sqrt(d2);
+                    if (len < 1e-12) {                      // skipped and counted (_kernels.py:58-60)
+                        if (e & 0x1000u) ++deg;
+                    } else {
+                        c = spring_c64(kl.x, len, l0);
+                        add = true;
+                    }
+                }
+                if (add) {
                     fx = c * dx;
                     fy = c * dy;
                     fz = c * dz;
-                    add = true;
                 }
             }
             const unsigned ballot = __ballot_sync(gmask, add) >> leader;
@@ -288,7 +302,7 @@ resident_spring_sum(const ResidentArgs &a, const unsigned char *smem, const uint
 
 // INTEG: 0 Euler, 1 Verlet.  G lanes per mass slot: slot m = tid / G.
 template <bool F32, int INTEG, int G>
-__global__ void __launch_bounds__(G == 1 ? 256 : 1024, 1) resident_kernel(Params<typename Prec<F32>::T> p,
+__global__ void __launch_bounds__(G == 1 ? 256 : G == 2 ? 512 : 1024, 1) resident_kernel(Params<typename Prec<F32>::T> p,
                                                                         ResidentArgs a) {
     using T = typename Prec<F32>::T;
     using T4 = typename Prec<F32>::T4;
