@@ -446,6 +446,27 @@ def test_sharded_general_graph_bitwise(transport):
         assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["p2p", "copy"])
+@pytest.mark.parametrize("integrator", ["verlet", "rk4"])
+def test_sharded_general_graph_fp32(transport, integrator):
+    """The fp32 general-graph format (rest vectors formed from the staged
+    X0, tile_lean_kernel INLINE; sharded Verlet on its boundary-tiles-first
+    variant) in 3 slabs, within fp32 rounding of one engine."""
+    from paper_2207_09334_b200.sharded import ShardGroup
+    c = L.excite(L.block_scene(12), seed=7)
+    c.k = c.k * (1.0 + 1e-7 * np.arange(c.k.size))
+    one = Engine(c, precision="f32", integrator=integrator)
+    assert one.info()["tile_kernel"] == 6
+    grp = ShardGroup.from_scene(c, 3, precision="f32", transport=transport, integrator=integrator)
+    assert all(e.info()["tile_kernel"] == 6 for e in grp.engines)
+    one.step(40)
+    grp.step(40)
+    x, _ = _assemble(grp)
+    disp = np.abs(one.x - c.x).max()
+    assert np.abs(x - one.x).max() <= 1e-4 * disp
+
+
 def _ipc_beam_worker(rank, world, port, steps, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
