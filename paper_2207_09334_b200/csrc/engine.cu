@@ -3193,18 +3193,19 @@ extern "C" int ss_step_group(ss_engine **hs, int n, int64_t count, ss_step_resul
                 break;
             }
             void *xa = buf(a), *xb = buf(b);
+            // (an empty plane -- no spring crosses this cut -- launches nothing)
             if (f32) {
-                halo_copy_kernel<float4><<<(na + 255) / 256, 256, 0, a->stream>>>(
+                if (na) halo_copy_kernel<float4><<<(na + 255) / 256, 256, 0, a->stream>>>(
                     (const float4 *)xa, a->halo_send_idx[1], (float4 *)xb, b->halo_recv_idx[0], na);
-                halo_copy_kernel<float4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
+                if (nb) halo_copy_kernel<float4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
                     (const float4 *)xb, b->halo_send_idx[0], (float4 *)xa, a->halo_recv_idx[1], nb);
             } else {
-                halo_copy_kernel<double4><<<(na + 255) / 256, 256, 0, a->stream>>>(
+                if (na) halo_copy_kernel<double4><<<(na + 255) / 256, 256, 0, a->stream>>>(
                     (const double4 *)xa, a->halo_send_idx[1], (double4 *)xb, b->halo_recv_idx[0], na);
-                halo_copy_kernel<double4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
+                if (nb) halo_copy_kernel<double4><<<(nb + 255) / 256, 256, 0, a->stream>>>(
                     (const double4 *)xb, b->halo_send_idx[0], (double4 *)xa, a->halo_recv_idx[1], nb);
             }
-            a->launches += 2;
+            a->launches += (na ? 1 : 0) + (nb ? 1 : 0);
         }
     };
     // one divergence step for the whole group (shard 0's word): every shard

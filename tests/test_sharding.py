@@ -467,6 +467,35 @@ def test_sharded_general_graph_fp32(transport, integrator):
     assert np.abs(x - one.x).max() <= 1e-4 * disp
 
 
+def _crawler_line(copies: int):
+    """``copies`` crawlers (demos/crawler.py: floor contact with friction,
+    two sinusoid actuation groups, damping) side by side along x, so the
+    batch is x-major and splits into x-slabs between walkers."""
+    from paper_2207_09334_b200 import crawler_scene, replicate
+    b = replicate(crawler_scene(), copies)
+    n = b.instance_masses
+    span = np.ptp(b.x[:n, 0]) + 0.25
+    b.x[:, 0] += np.repeat(np.arange(copies) * span, n)
+    return b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport,integrator", [("copy", "verlet"), ("p2p", "verlet"), ("p2p", "euler"),
+                                                  ("copy", "rk4"), ("p2p", "rk4")])
+def test_sharded_walkers_with_groups_and_contact(transport, integrator):
+    """A line of 6 walkers (actuation groups, floor contact and friction,
+    damping) in 3 x-slabs: fp64 bitwise equal to one engine."""
+    from paper_2207_09334_b200.sharded import ShardGroup
+    line = _crawler_line(6)
+    one = Engine(line, integrator=integrator, precision="f64")
+    grp = ShardGroup.from_scene(line, 3, precision="f64", transport=transport, integrator=integrator)
+    for n in (17, 300):
+        one.step(n)
+        grp.step(n)
+        x, v = _assemble(grp)
+        assert x.tobytes() == one.x.tobytes() and v.tobytes() == one.v.tobytes()
+
+
 def _ipc_beam_worker(rank, world, port, steps, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
