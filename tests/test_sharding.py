@@ -467,6 +467,24 @@ def test_sharded_general_graph_fp32(transport, integrator):
     assert np.abs(x - one.x).max() <= 1e-4 * disp
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport,integrator", [("copy", "verlet"), ("p2p", "verlet"), ("p2p", "rk4"),
+                                                  ("copy", "euler")])
+def test_thin_slabs(transport, integrator):
+    """6 x-planes in 5 slabs: one-plane slabs whose every mass is both a
+    boundary mass and a neighbour's ghost; fp64 bitwise equal to one engine."""
+    cells = 5
+    full = L.excite(L.block_scene(cells), seed=11)
+    v = excited_velocities(full.mass_count)
+    one = Engine(full, integrator=integrator, precision="f64")
+    grp = ShardGroup(cells, 5, precision="f64", v_global=v, integrator=integrator, transport=transport)
+    for n in (3, 40):
+        one.step(n)
+        grp.step(n)
+        assert grp.positions().tobytes() == one.x.tobytes()
+        assert grp.velocities().tobytes() == one.v.tobytes()
+
+
 def _crawler_line(copies: int):
     """``copies`` crawlers (demos/crawler.py: floor contact with friction,
     two sinusoid actuation groups, damping) side by side along x, so the
