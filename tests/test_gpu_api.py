@@ -634,8 +634,13 @@ def test_graph_replays_are_bitwise_the_launches(precision, integrator, monkeypat
     replays give the bits of one launch per substep, in both precisions."""
     from paper_2207_09334_b200 import crawler_scene, lattice as L, replicate
     monkeypatch.setenv("SS_RESIDENT", "0")
+    def general():                                          # every tile on the inline general-graph format
+        c = L.excite(L.block_scene(14), seed=5)
+        c.k = c.k * (1.0 + 1e-7 * np.arange(c.k.size))
+        return c
     for make in (lambda: L.excite(L.block_scene(20), seed=3),
-                 lambda: replicate(crawler_scene(), 48, jitter=1e-6, seed=2)):     # 2 groups, contact
+                 lambda: replicate(crawler_scene(), 48, jitter=1e-6, seed=2),     # 2 groups, contact
+                 general):
         g, n = _graph_pair(make, monkeypatch, integrator=integrator, precision=precision)
         for eng in (g, n):
             for b in range(6):
