@@ -5,12 +5,14 @@ so a contiguous id range is a slab of whole x-planes.  Rank g owns planes
 [i_lo, i_hi) and holds, in its local scene, one halo plane per neighbour
 (marked fixed) plus every spring touching an owned mass — with its GLOBAL id
 order preserved, so each owned mass sums its springs in the same order as on
-one device and the results are bitwise identical.  After every substep the
-first and last owned planes go to the neighbours' halo planes: stored by the
-step kernel itself into the neighbours' position buffers over peer memory,
-synchronised by device-side step flags (``attach_peers``, the default), or
-NCCL send/recv on the engine stream (``SS_HALO=nccl``), or device copies for
-same-device shards (``ShardGroup``).
+one device and the results are bitwise identical.  After every substep (RK4:
+every stage, into the neighbours' stage buffers) the first and last owned
+planes go to the neighbours' halo planes: stored by the step kernel itself
+into the neighbours' position buffers over peer memory, synchronised by
+device-side sequence flags (``attach_peers``, the default), or NCCL
+send/recv on the engine stream (``SS_HALO=nccl``), or device copies for
+same-device shards (``ShardGroup``, whose shards also share one divergence
+step).
 """
 
 from __future__ import annotations
