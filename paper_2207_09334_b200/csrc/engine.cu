@@ -1487,6 +1487,12 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                 int sms = 0;
                 CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
                 if (!getenv("SS_PDL") && L.n_tiles >= 48 && L.n_tiles <= 3 * (int64_t)sms) h->pdl = false;
+                // (UNROLL, MINB) = (3, 3) up to ~13 tiles per SM: three incidences
+                // in flight per lane beat the fourth CTA per SM while the grid is a
+                // few waves (42-cell cube 12.3 -> 12.0 us, 60: 22.7 -> 21.9, 75:
+                // 37.4 -> 37.0); (2, 4) beyond (80 cells 44.6 vs 45.2, the 10M
+                // cube 63.3 vs 64.4; tools/f64_variant_probe.py)
+                if (L.n_tiles <= 13 * (int64_t)sms) h->f64_variant = 3;
                 if (const char *e = getenv("SS_F64_VARIANT")) h->f64_variant = atoi(e);
                 for (auto *kk : {tile_f64_kernel<0, false, 2, 4>, tile_f64_kernel<1, false, 2, 4>,
                                  tile_f64_kernel<0, true, 2, 4>, tile_f64_kernel<1, true, 2, 4>,
