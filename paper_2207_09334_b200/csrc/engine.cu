@@ -143,6 +143,7 @@ struct ss_engine {
     size_t lean_smem = 0;          // fp32 Euler/Verlet compact-format tile kernel (tile_f32.cuh), 0 = off
     size_t f64_smem = 0;           // fp64 Euler/Verlet compact-format tile kernel (tile_f64.cuh), 0 = off
     int f64_variant = 0;           // its (UNROLL, MINB) instantiation: 0 (2,4), 1 (1,4), 2 (2,3), 3 (3,3), 4 (1,5), 5 (2,5)
+    int f64_rk4_variant = 0;       // the RK4 stages' instantiation: 0 (2,4) or 3 (3,3)
     int lean_lanes = 1;            // threads per mass of that kernel (2: scenes with few tiles)
     int persist_max_grid = 0;      // co-resident CTAs of the persistent kernel (0: never persistent)
     bool pdl = true;               // programmatic dependent launch between substeps (SS_PDL=0: off)
@@ -673,11 +674,16 @@ template <bool GROUPS>
 void launch_rk4_f64(ss_engine *h, const Params<double> &p, int grid, int stage) {
     void (*k)(Params<double>) = nullptr;
     const bool inl = h->tl.inline_kl;
+    const bool v3 = !inl && h->f64_rk4_variant == 3;      // (3, 3): grids of a few waves
     switch (stage) {
-        case 1: k = inl ? tile_f64_kernel<2, GROUPS, 2, 4, true> : tile_f64_kernel<2, GROUPS, 2, 4>; break;
-        case 2: k = inl ? tile_f64_kernel<3, GROUPS, 2, 4, true> : tile_f64_kernel<3, GROUPS, 2, 4>; break;
-        case 3: k = inl ? tile_f64_kernel<4, GROUPS, 2, 4, true> : tile_f64_kernel<4, GROUPS, 2, 4>; break;
-        default: k = inl ? tile_f64_kernel<5, GROUPS, 2, 4, true> : tile_f64_kernel<5, GROUPS, 2, 4>; break;
+        case 1: k = inl ? tile_f64_kernel<2, GROUPS, 2, 4, true> : v3 ? tile_f64_kernel<2, GROUPS, 3, 3>
+                                                                      : tile_f64_kernel<2, GROUPS, 2, 4>; break;
+        case 2: k = inl ? tile_f64_kernel<3, GROUPS, 2, 4, true> : v3 ? tile_f64_kernel<3, GROUPS, 3, 3>
+                                                                      : tile_f64_kernel<3, GROUPS, 2, 4>; break;
+        case 3: k = inl ? tile_f64_kernel<4, GROUPS, 2, 4, true> : v3 ? tile_f64_kernel<4, GROUPS, 3, 3>
+                                                                      : tile_f64_kernel<4, GROUPS, 2, 4>; break;
+        default: k = inl ? tile_f64_kernel<5, GROUPS, 2, 4, true> : v3 ? tile_f64_kernel<5, GROUPS, 3, 3>
+                                                                       : tile_f64_kernel<5, GROUPS, 2, 4>; break;
     }
     if (h->pdl) launch_pdl(k, grid, kTile, h->f64_smem, h->stream, p);
     else k<<<grid, kTile, h->f64_smem, h->stream>>>(p);
@@ -1493,7 +1499,13 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                 // 37.4 -> 37.0); (2, 4) beyond (80 cells 44.6 vs 45.2, the 10M
                 // cube 63.3 vs 64.4; tools/f64_variant_probe.py)
                 if (L.n_tiles <= 13 * (int64_t)sms) h->f64_variant = 3;
-                if (const char *e = getenv("SS_F64_VARIANT")) h->f64_variant = atoi(e);
+                // RK4 stages: up to 7 tiles per SM (42 cells 52.1 -> 50.5 us per
+                // step, 60 cells 94.4 -> 91.9; 75 cells 163.8 against 169.0)
+                if (L.n_tiles <= 7 * (int64_t)sms) h->f64_rk4_variant = 3;
+                if (const char *e = getenv("SS_F64_VARIANT")) {
+                    h->f64_variant = atoi(e);
+                    h->f64_rk4_variant = h->f64_variant == 3 ? 3 : 0;
+                }
                 for (auto *kk : {tile_f64_kernel<0, false, 2, 4>, tile_f64_kernel<1, false, 2, 4>,
                                  tile_f64_kernel<0, true, 2, 4>, tile_f64_kernel<1, true, 2, 4>,
                                  tile_f64_kernel<0, false, 1, 4>, tile_f64_kernel<1, false, 1, 4>,
@@ -1515,7 +1527,11 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_f64_kernel<2, false, 2, 4, true>, tile_f64_kernel<3, false, 2, 4, true>,
                                  tile_f64_kernel<4, false, 2, 4, true>, tile_f64_kernel<5, false, 2, 4, true>,
                                  tile_f64_kernel<2, true, 2, 4, true>, tile_f64_kernel<3, true, 2, 4, true>,
-                                 tile_f64_kernel<4, true, 2, 4, true>, tile_f64_kernel<5, true, 2, 4, true>})
+                                 tile_f64_kernel<4, true, 2, 4, true>, tile_f64_kernel<5, true, 2, 4, true>,
+                                 tile_f64_kernel<2, false, 3, 3>, tile_f64_kernel<3, false, 3, 3>,
+                                 tile_f64_kernel<4, false, 3, 3>, tile_f64_kernel<5, false, 3, 3>,
+                                 tile_f64_kernel<2, true, 3, 3>, tile_f64_kernel<3, true, 3, 3>,
+                                 tile_f64_kernel<4, true, 3, 3>, tile_f64_kernel<5, true, 3, 3>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_max));
             }
         }
