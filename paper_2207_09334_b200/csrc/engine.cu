@@ -207,6 +207,7 @@ struct ss_engine {
     long long *d_step_base = nullptr;
     int64_t graph_base_n = -1;                            // the device step base after the queued work (-1: unknown)
     bool use_graphs = true;                               // SS_GRAPH=0: off
+    int pdl_graph = -1;                                   // PDL inside captured graphs (-1: as pdl; autotune_pdl)
     bool graph_capturing = false;
 
     ~ss_engine() {
@@ -699,8 +700,8 @@ template <typename T>
 std::vector<unsigned char> graph_key(const ss_engine *h, const Params<T> &p, int64_t count) {
     std::vector<unsigned char> k(sizeof(Params<T>) + 64, 0);
     std::memcpy(k.data(), &p, sizeof(Params<T>));
-    int64_t extra[8] = {count, h->cur, h->integrator, h->pdl ? 1 : 0, h->lean_lanes, h->f64_variant,
-                        (int64_t)(intptr_t)h->scale, h->has_prev ? 1 : 0};
+    int64_t extra[8] = {count, h->cur, h->integrator, (h->pdl ? 1 : 0) | (h->pdl_graph + 1) << 1, h->lean_lanes,
+                        h->f64_variant, (int64_t)(intptr_t)h->scale, h->has_prev ? 1 : 0};
     std::memcpy(k.data() + sizeof(Params<T>), extra, sizeof extra);
     return k;
 }
@@ -744,7 +745,10 @@ int try_graph(ss_engine *h, int64_t count, Params<typename Prec<F32>::T> p, int 
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         h->n = 0;                                            // (the loop numbers steps h->n + s + 1)
         h->graph_capturing = true;
+        const bool pdl0 = h->pdl;
+        if (h->pdl_graph >= 0) h->pdl = h->pdl_graph != 0;    // (replays may prefer the other choice)
         int rc = launch_steps<F32, LAYOUT>(h, count);
+        h->pdl = pdl0;
         h->graph_capturing = false;
         h->n = n0;
         if (rc == SS_OK) step_base_add<<<1, 1, 0, h->stream>>>(h->d_step_base, (long long)count);
@@ -1034,6 +1038,94 @@ int reset_divergence(ss_engine *h) {
     CK(cudaMemcpyAsync(h->d_div_mass, &nonei, sizeof nonei, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return SS_OK;
+}
+
+// Programmatic dependent launch on or off, timed on this scene.  For grids
+// of one to eight CTAs per SM the next substep's early CTAs can pile onto a
+// few SMs and cost more than the overlap gains, and where that happens
+// depends on the scene (178-686 tiles, 6-17%).  PDL changes no
+// bit, so the engine times a few substeps of each choice on its own buffers
+// and keeps the faster (by at least 3%); the state, counters and step
+// number are restored afterwards.  SS_PDL fixes the choice, SS_AUTOTUNE=0
+// keeps the static one.
+int autotune_pdl(ss_engine *h) {
+    if (getenv("SS_PDL")) return SS_OK;
+    if (const char *e = getenv("SS_AUTOTUNE"))
+        if (atoi(e) == 0) return SS_OK;
+    if (h->layout != SS_LAYOUT_TILE || h->res_image || !(h->lean_smem || h->f64_smem)) return SS_OK;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    const int64_t tiles = h->tl.n_tiles;
+    if (tiles < sms || tiles > 8 * (int64_t)sms) return SS_OK;
+    const size_t vb = (size_t)h->ND * (h->precision == SS_F32 ? sizeof(float4) : sizeof(double4));
+    void *live[4] = {h->X[0], h->X[1], h->V, h->U};
+    void *keep[4] = {nullptr, nullptr, nullptr, nullptr};
+    int rc = SS_OK;
+    for (int i = 0; i < 4 && rc == SS_OK; ++i) {
+        if (!live[i]) continue;
+        if (cudaMalloc(&keep[i], vb) != cudaSuccess) {
+            cudaGetLastError();
+            keep[i] = nullptr;
+            rc = -1;                                        // no room to snapshot: keep the static choice
+            break;
+        }
+        if (cudaMemcpyAsync(keep[i], live[i], vb, cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess) rc = -1;
+    }
+    unsigned long long deg0 = 0;
+    if (rc == SS_OK && cudaMemcpy(&deg0, h->d_degenerate, sizeof deg0, cudaMemcpyDeviceToHost) != cudaSuccess) rc = -1;
+    const int64_t n0 = h->n, launches0 = h->launches;
+    const double t0 = h->t;
+    const int cur0 = h->cur;
+    const bool prev0 = h->has_prev, graphs0 = h->use_graphs, pdl0 = h->pdl;
+    if (rc == SS_OK) {
+        cudaEvent_t ev[2];
+        CK(cudaEventCreate(&ev[0]));
+        CK(cudaEventCreate(&ev[1]));
+        // ms[mode][choice]: mode 0 launches one by one, mode 1 graph replays
+        // (a batch shape's second occurrence is captured, later ones replay)
+        float ms[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+        for (int mode = 0; mode < 2 && rc == SS_OK; ++mode) {
+            h->use_graphs = mode == 1;
+            for (int c = 0; c < 2 && rc == SS_OK; ++c) {
+                const bool pdl = c == 0 ? pdl0 : !pdl0;
+                h->pdl = pdl;
+                h->pdl_graph = pdl ? 1 : 0;
+                for (int w = 0; w < 3 && rc == SS_OK; ++w) rc = dispatch_steps(h, 32);   // even counts: the parity returns
+                if (rc == SS_OK) CK(cudaEventRecord(ev[0], h->stream));
+                for (int w = 0; w < 2 && rc == SS_OK; ++w) rc = dispatch_steps(h, 32);
+                if (rc == SS_OK) CK(cudaEventRecord(ev[1], h->stream));
+                if (rc == SS_OK) {
+                    CK(cudaEventSynchronize(ev[1]));
+                    CK(cudaEventElapsedTime(&ms[mode][c], ev[0], ev[1]));
+                }
+            }
+        }
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        h->pdl = (rc == SS_OK && ms[0][1] < 0.97f * ms[0][0]) ? !pdl0 : pdl0;
+        h->pdl_graph = ((rc == SS_OK && ms[1][1] < 0.97f * ms[1][0]) ? !pdl0 : pdl0) ? 1 : 0;
+        // the tuning batches' graphs go: they captured this state's buffers
+        for (auto &g : h->graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        h->graphs.clear();
+        h->graph_seen.clear();
+        h->graph_base_n = -1;
+    }
+    // restore the state the engine was created with
+    for (int i = 0; i < 4; ++i)
+        if (keep[i]) cudaMemcpyAsync(live[i], keep[i], vb, cudaMemcpyDeviceToDevice, h->stream);
+    cudaMemcpyAsync(h->d_degenerate, &deg0, sizeof deg0, cudaMemcpyHostToDevice, h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+    for (void *k : keep)
+        if (k) cudaFree(k);
+    h->n = n0;
+    h->t = t0;
+    h->cur = cur0;
+    h->has_prev = prev0;
+    h->launches = launches0;
+    h->use_graphs = graphs0;
+    if (rc != SS_OK && rc != -1) return rc;
+    return reset_divergence(h);
 }
 
 // After an enqueued batch: read the divergence record, fix up n/t/cur.
@@ -2191,6 +2283,7 @@ int ss_create(const ss_scene_desc *d, ss_engine **out) {
                                 : create_impl<false>(h.get(), d, d->layout);
     if (rc) return rc;
     if ((rc = setup_persistent(h.get()))) return rc;
+    if ((rc = autotune_pdl(h.get()))) return rc;
     CK(cudaStreamSynchronize(h->stream));
     *out = h.release();
     return SS_OK;

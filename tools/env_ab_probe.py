@@ -1,6 +1,7 @@
 """µs per substep of excited cubes (graph replays) under alternative
 environment switches, e.g.  PREC=f32 CELLS=42,60 AB="SS_LEAN_LANES=1;SS_LEAN_LANES=2;"
-(an empty entry = the defaults) -- dev tool."""
+(an empty entry = the defaults); MODE=single times one 400-substep batch
+(launches) instead of repeated 100-substep batches (graph replays) -- dev tool."""
 import json
 import os
 import sys
@@ -22,14 +23,18 @@ for cells in [int(c) for c in os.environ.get("CELLS", "42,60").split(",")]:
             os.environ[k] = v
         e = Engine(sc, integrator=integ, precision=prec)
         st = torch.cuda.ExternalStream(e.stream_ptr)
-        for _ in range(6):
+        single = os.environ.get("MODE") == "single"         # one big batch: launches, no graph replays
+        for _ in range(1 if single else 6):
             e.step_async(100)
         e.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(st)
-        for _ in range(4):
-            e.step_async(100)
+        if single:
+            e.step_async(400)
+        else:
+            for _ in range(4):
+                e.step_async(100)
         b.record(st)
         b.synchronize()
         e.synchronize()
