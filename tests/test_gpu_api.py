@@ -673,3 +673,30 @@ def test_graph_replays_report_divergence_like_the_launches(monkeypatch):
         eng.close()
     assert got[0] == got[1]
     assert got[0][1] > 30                                   # (diverged inside a replayed batch)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("integrator", ["verlet", "rk4"])
+def test_pdl_autotune_leaves_no_trace(precision, integrator, monkeypatch):
+    """Engine creation times both PDL choices on mid-size scenes (one to eight
+    tiles per SM) on the engine's own buffers: afterwards the state, step
+    counter, launch and degenerate counters are the untuned engine's, and so
+    are the results."""
+    from paper_2207_09334_b200 import lattice as L
+    scene = L.excite(L.block_scene(40), seed=4)
+    engines = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SS_AUTOTUNE", flag)
+        engines.append(Engine(scene, integrator=integrator, precision=precision))
+    monkeypatch.delenv("SS_AUTOTUNE")
+    tuned, plain = engines
+    assert 148 <= tuned.info()["tile_count"] <= 8 * 148
+    for e in engines:
+        assert e.n == 0 and e.launch_count == 0 and e.degenerate_springs == 0
+        assert e.x.tobytes() == scene.x.tobytes()
+        e.step(30)
+        e.step(30)
+    assert tuned.x.tobytes() == plain.x.tobytes() and tuned.v.tobytes() == plain.v.tobytes()
+    assert tuned.n == plain.n == 60 and tuned.launch_count == plain.launch_count
+    for e in engines:
+        e.close()
