@@ -272,6 +272,7 @@ def kernel_of(info: dict) -> tuple[str, str]:
     tk = info["tile_kernel"]
     if fp32:
         return {2: ("tile_compact", "tile_lean_kernel"), 6: ("tile_inline", "tile_lean_kernel"),
+                7: ("tile_compact_x0", "tile_lean_kernel"),
                 1: ("tile_explicit", "tile_lean_kernel")}.get(tk, ("tile_explicit", "step_kernel"))
     return {5: ("tile_inline", "tile_f64_kernel"), 4: ("tile_compact", "tile_f64_kernel"),
             3: ("tile_compact", "step_kernel")}.get(tk, ("tile_explicit", "step_kernel"))

@@ -192,7 +192,10 @@ typedef struct ss_info {
     int32_t tile_kernel;       /* dominant kernel / record format: fp32 1 explicit, 2 compact (tile_lean_kernel; 0: step_kernel);
                                   fp64 0 explicit, 3 compact (step_kernel), 4 compact (tile_f64_kernel),
                                   5 inline (tile_f64_kernel, (k, l0) per incidence: general graphs);
-                                  fp32 6 inline (tile_lean_kernel, records per incidence: general graphs) */
+                                  fp32 6 inline (tile_lean_kernel, records per incidence: general graphs),
+                                  7 compact with a (k, k*l0, group) dictionary and rest vectors formed
+                                  from X0 (tile_lean_kernel: positions off a lattice, e.g. jittered
+                                  robot populations) */
     int32_t kernel_smem;       /* its dynamic shared memory per CTA */
 } ss_info;
 int ss_get_info(ss_engine *h, ss_info *info);

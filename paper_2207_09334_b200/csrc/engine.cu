@@ -600,12 +600,17 @@ template <bool GROUPS>
 void launch_rk4_lean(ss_engine *h, const Params<float> &p, int grid, int stage) {
     const bool two = h->lean_lanes == 2;
     void (*k)(Params<float>) = nullptr;
-    if (h->tl.inline_kl) {
+    if (h->tl.inline_kl || h->tl.dict_x0) {               // records with the staged X0 (REC 1 / 2)
+        const bool i1 = h->tl.inline_kl;
         switch (stage) {
-            case 1: k = tile_lean_kernel<2, GROUPS, kInlineMinB, 1, false, true>; break;
-            case 2: k = tile_lean_kernel<3, GROUPS, kInlineMinB, 1, false, true>; break;
-            case 3: k = tile_lean_kernel<4, GROUPS, kInlineMinB, 1, false, true>; break;
-            default: k = tile_lean_kernel<5, GROUPS, kInlineMinB, 1, false, true>; break;
+            case 1: k = i1 ? tile_lean_kernel<2, GROUPS, kInlineMinB, 1, false, 1>
+                           : tile_lean_kernel<2, GROUPS, kInlineMinB, 1, false, 2>; break;
+            case 2: k = i1 ? tile_lean_kernel<3, GROUPS, kInlineMinB, 1, false, 1>
+                           : tile_lean_kernel<3, GROUPS, kInlineMinB, 1, false, 2>; break;
+            case 3: k = i1 ? tile_lean_kernel<4, GROUPS, kInlineMinB, 1, false, 1>
+                           : tile_lean_kernel<4, GROUPS, kInlineMinB, 1, false, 2>; break;
+            default: k = i1 ? tile_lean_kernel<5, GROUPS, kInlineMinB, 1, false, 1>
+                            : tile_lean_kernel<5, GROUPS, kInlineMinB, 1, false, 2>; break;
         }
         if (h->pdl) launch_pdl(k, grid, kTile, h->lean_smem, h->stream, p);
         else k<<<grid, kTile, h->lean_smem, h->stream>>>(p);
@@ -626,10 +631,19 @@ template <bool GROUPS>
 void launch_tile_f32(ss_engine *h, const Params<float> &p, int grid) {
     const bool euler = h->integrator == SS_EULER;
     if (h->tl.inline_kl) {                                 // general graphs: records streamed per incidence
-        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, true, true>
-                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, true, true>)
-                             : (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, false, true>
-                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, false, true>);
+        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, true, 1>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, true, 1>)
+                             : (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, false, 1>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, false, 1>);
+        if (h->pdl) launch_pdl(ki, grid, kTile, h->lean_smem, h->stream, p);
+        else ki<<<grid, kTile, h->lean_smem, h->stream>>>(p);
+        return;
+    }
+    if (h->tl.dict_x0) {                                   // (k, k*l0, group) dictionary, D from the staged X0
+        auto *ki = h->p2p_on ? (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, true, 2>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, true, 2>)
+                             : (euler ? tile_lean_kernel<0, GROUPS, kInlineMinB, 1, false, 2>
+                                      : tile_lean_kernel<1, GROUPS, kInlineMinB, 1, false, 2>);
         if (h->pdl) launch_pdl(ki, grid, kTile, h->lean_smem, h->stream, p);
         else ki<<<grid, kTile, h->lean_smem, h->stream>>>(p);
         return;
@@ -1387,6 +1401,39 @@ int setup_resident(ss_engine *h, const ss_scene_desc *d) {
     return SS_OK;
 }
 
+// The tiled layout of a scene: masses in spatial bricks first; where that
+// gives tiles whose halo does not fit shared memory (dev_smem bytes), or
+// whose halo is several times the tile (instances of a batch stacked at the
+// same place: a brick holds the same mass of many robots, whose partners are
+// all elsewhere), the caller's order, which keeps each instance's masses
+// together -- the order with the smaller halo wins.
+int choose_tiles(const ss_scene_desc *d, bool f32, int64_t dev_smem, TileLayout &out) {
+    const size_t vec = f32 ? sizeof(float4) : sizeof(double4);
+    TileLayout best;
+    bool have = false;
+    int rc = SS_OK;
+    for (int order = 1; order >= 0; --order) {
+        TileInput ti{d->n_masses, d->n_springs, d->si, d->sj, d->x, d->k, d->l0,
+                     (d->group && d->n_groups) ? d->group : nullptr, f32, order};
+        TileLayout cand;
+        rc = build_tiles(ti, cand);
+        if (rc != SS_OK) continue;
+        const size_t need = 128 + ((cand.max_tile_smem + 127u) & ~127u) + (size_t)(kTile + cand.max_halo) * vec;
+        if ((int64_t)need > dev_smem) {
+            rc = ss::fail(SS_EINVAL, "tile needs %zu B of shared memory (> %lld)", need, (long long)dev_smem);
+            continue;
+        }
+        if (!have || cand.halo_ratio < best.halo_ratio) {
+            best = std::move(cand);
+            have = true;
+        }
+        if (best.halo_ratio <= 3.0) break;                     // bricks did their job (lattices: 1.2-2.6)
+    }
+    if (!have) return rc;
+    out = std::move(best);
+    return SS_OK;
+}
+
 template <bool F32>
 int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     using T = typename Prec<F32>::T;
@@ -1396,9 +1443,9 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
     // ---- topology first: it may renumber the masses
     int layout = want_layout;
     if (layout == SS_LAYOUT_AUTO || layout == SS_LAYOUT_TILE) {
-        TileInput ti{N, S, d->si, d->sj, d->x, d->k, d->l0,
-                     (d->group && d->n_groups) ? d->group : nullptr, F32, 1};
-        rc = build_tiles(ti, h->tl);
+        int dev_smem = 0;
+        CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        rc = choose_tiles(d, F32, dev_smem, h->tl);
         if (rc == SS_OK) {
             layout = SS_LAYOUT_TILE;
         } else if (want_layout == SS_LAYOUT_TILE) {
@@ -1488,6 +1535,10 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
         h->d_toff = reinterpret_cast<unsigned long long *>(p);
         if ((rc = up_vec(h, &p, L.split))) return rc;
         h->d_tsplit = reinterpret_cast<unsigned int *>(p);
+        if (F32 && L.dict_x0) {                   // rest vectors formed from X0 on the device
+            if ((rc = h->alloc(&h->d_x0dev, h->x0.size() * sizeof(double)))) return rc;
+            if ((rc = upload(h, h->d_x0dev, h->x0.data(), h->x0.size() * sizeof(double)))) return rc;
+        }
         if (L.inline_kl) {                        // general-graph format: records streamed, not staged
             if (F32) {
                 if ((rc = up_vec(h, &p, L.kd_inline))) return rc;
@@ -1527,12 +1578,12 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
             if (kname != "step1" && !L.has_self && L.compact &&
                 (int64_t)h->smem_bytes <= dev_max) {
                 h->lean_smem = h->smem_bytes;
-                if (L.inline_kl) h->lean_smem += (size_t)(kTile + L.max_halo) * 3 * sizeof(double);   // staged X0
+                if (L.inline_kl || L.dict_x0) h->lean_smem += (size_t)(kTile + L.max_halo) * 3 * sizeof(double);   // staged X0
                 // scenes with few tiles (at most 3 per SM) use two lanes per mass:
                 // 512-thread CTAs, twice the warps for the same tiles
                 int sms = 0;
                 CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-                h->lean_lanes = L.n_tiles <= 3 * (int64_t)sms && !L.inline_kl ? 2 : 1;
+                h->lean_lanes = L.n_tiles <= 3 * (int64_t)sms && !L.inline_kl && !L.dict_x0 ? 2 : 1;
                 if (const char *e = getenv("SS_LEAN_LANES")) h->lean_lanes = atoi(e) == 2 ? 2 : 1;
                 if (h->lean_lanes == 2) {
                     h->lean_smem += (size_t)kTile * sizeof(float4);        // lane 1's partial sums
@@ -1562,7 +1613,15 @@ int create_impl(ss_engine *h, const ss_scene_desc *d, int want_layout) {
                                  tile_lean_kernel<3, false, kInlineMinB, 1, false, true>, tile_lean_kernel<4, false, kInlineMinB, 1, false, true>,
                                  tile_lean_kernel<5, false, kInlineMinB, 1, false, true>, tile_lean_kernel<2, true, kInlineMinB, 1, false, true>,
                                  tile_lean_kernel<3, true, kInlineMinB, 1, false, true>, tile_lean_kernel<4, true, kInlineMinB, 1, false, true>,
-                                 tile_lean_kernel<5, true, kInlineMinB, 1, false, true>})
+                                 tile_lean_kernel<5, true, kInlineMinB, 1, false, true>,
+                                 tile_lean_kernel<0, false, kInlineMinB, 1, false, 2>, tile_lean_kernel<1, false, kInlineMinB, 1, false, 2>,
+                                 tile_lean_kernel<0, true, kInlineMinB, 1, false, 2>, tile_lean_kernel<1, true, kInlineMinB, 1, false, 2>,
+                                 tile_lean_kernel<0, false, kInlineMinB, 1, true, 2>, tile_lean_kernel<1, false, kInlineMinB, 1, true, 2>,
+                                 tile_lean_kernel<0, true, kInlineMinB, 1, true, 2>, tile_lean_kernel<1, true, kInlineMinB, 1, true, 2>,
+                                 tile_lean_kernel<2, false, kInlineMinB, 1, false, 2>, tile_lean_kernel<3, false, kInlineMinB, 1, false, 2>,
+                                 tile_lean_kernel<4, false, kInlineMinB, 1, false, 2>, tile_lean_kernel<5, false, kInlineMinB, 1, false, 2>,
+                                 tile_lean_kernel<2, true, kInlineMinB, 1, false, 2>, tile_lean_kernel<3, true, kInlineMinB, 1, false, 2>,
+                                 tile_lean_kernel<4, true, kInlineMinB, 1, false, 2>, tile_lean_kernel<5, true, kInlineMinB, 1, false, 2>})
                     CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
             }
         }
@@ -2886,7 +2945,7 @@ int ss_get_info(ss_engine *h, ss_info *info) {
         info->tile_halo_ratio = h->tl.halo_ratio;
         info->tile_foreign_frac = h->tl.foreign_frac;
         info->smem_per_block = (int32_t)h->smem_bytes;
-        info->tile_kernel = h->lean_smem ? (h->tl.inline_kl ? 6 : h->tl.compact ? 2 : 1)
+        info->tile_kernel = h->lean_smem ? (h->tl.inline_kl ? 6 : h->tl.dict_x0 ? 7 : h->tl.compact ? 2 : 1)
                           : h->f64_smem ? (h->tl.inline_kl ? 5 : 4)
                                         : (h->precision == SS_F64 && h->tl.compact ? 3 : 0);
         info->kernel_smem = (int32_t)(h->lean_smem ? h->lean_smem : h->f64_smem ? h->f64_smem : h->smem_bytes);
@@ -2910,10 +2969,8 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     if (d->n_masses <= 0 || !d->x || (d->n_springs && (!d->si || !d->sj || !d->k || !d->l0)))
         return ss::fail(SS_EINVAL, "ss_plan: incomplete scene");
     const bool f32 = d->precision == SS_F32;
-    TileInput ti{d->n_masses, d->n_springs, d->si, d->sj, d->x, d->k, d->l0,
-                 (d->group && d->n_groups) ? d->group : nullptr, f32, 1};
     TileLayout tl;
-    int rc = build_tiles(ti, tl);
+    int rc = choose_tiles(d, f32, 232448, tl);             // (host-only: B200's opt-in shared memory per CTA)
     if (rc) return rc;
     std::memset(info, 0, sizeof *info);
     info->n_masses = d->n_masses;
@@ -2935,7 +2992,7 @@ extern "C" int ss_plan(const ss_scene_desc *d, ss_info *info) {
     const int64_t per_spring = f32 ? 16 : 24, per_mass = f32 ? 64 : 128;
     info->algorithmic_bytes_per_step = (double)(per_spring * d->n_springs + per_mass * d->n_masses);
     info->kernel_smem = info->smem_per_block;
-    info->tile_kernel = f32 ? (tl.inline_kl ? 6 : tl.compact ? 2 : 1) : (tl.inline_kl ? 5 : tl.compact ? 3 : 0);
+    info->tile_kernel = f32 ? (tl.inline_kl ? 6 : tl.dict_x0 ? 7 : tl.compact ? 2 : 1) : (tl.inline_kl ? 5 : tl.compact ? 3 : 0);
     return SS_OK;
 }
 

@@ -182,11 +182,15 @@ __device__ __forceinline__ void acc3(V3<float> &s, float c, float dx, float dy, 
 // caller combines the lanes' sums; dmin_out gets the smallest d^2 seen (the
 // degenerate recount, by lane 0, covers all own springs).
 // (k, k*l0, Dx, Dy), Dz and group of incidence q (entry e): the tile's
-// dictionary, or (INLINE, general graphs) this mass's column of the inline
+// dictionary, or (REC 1, general graphs) this mass's column of the inline
 // (k, k*l0) records in global memory (tiles.h), streamed, with
 // D = fp32(X0_partner - X0_me) from the fp64 rest positions staged in shared
 // memory (sX0: x, y, z planes of ns slots) -- the dictionary's value.
-template <bool INLINE>
+// REC 0: the dictionary (rest vector stored); 1: inline records (general
+// graphs); 2: the dictionary of (k, k*l0, group) with the rest vector from
+// the staged X0 (scenes whose positions are off a lattice -- jittered robot
+// populations -- where a D-keyed dictionary overflows but the materials do not)
+template <int REC>
 struct F32Rec {
     const float4 *dict;          // dictionary (2 float4 per entry)
     const float2 *kk;            // inline (k, k*l0) + column
@@ -196,16 +200,24 @@ struct F32Rec {
     double mx, my, mz;           //   X0 of this mass
     __device__ __forceinline__ float2 load(int q) const { return __ldcs(kk + (q << 8)); }
     __device__ __forceinline__ void get(uint32_t e, int q, float4 &kd, float &dz_, int &grp) const {
-        get(e, q, INLINE ? load(q) : make_float2(0.f, 0.f), kd, dz_, grp);
+        get(e, q, REC == 1 ? load(q) : make_float2(0.f, 0.f), kd, dz_, grp);
     }
     // k2: the inline (k, k*l0) of incidence q, already loaded
     __device__ __forceinline__ void get(uint32_t e, int q, float2 k2, float4 &kd, float &dz_, int &grp) const {
-        if constexpr (INLINE) {
+        if constexpr (REC == 1) {
             const uint32_t sl = e & 0x3ffu;
             kd = make_float4(k2.x, k2.y, __double2float_rn(__dsub_rn(sX0[sl], mx)),
                              __double2float_rn(__dsub_rn(sX0[ns + sl], my)));
             dz_ = __double2float_rn(__dsub_rn(sX0[2 * ns + sl], mz));
             grp = g ? g[q << 8] : -1;
+        } else if constexpr (REC == 2) {
+            const float4 *ent = dict + 2 * (e >> 10);
+            const float4 k4 = ent[0];
+            const uint32_t sl = e & 0x3ffu;
+            kd = make_float4(k4.x, k4.y, __double2float_rn(__dsub_rn(sX0[sl], mx)),
+                             __double2float_rn(__dsub_rn(sX0[ns + sl], my)));
+            dz_ = __double2float_rn(__dsub_rn(sX0[2 * ns + sl], mz));
+            grp = __float_as_int(ent[1].y);
         } else {
             const float4 *ent = dict + 2 * (e >> 10);
             kd = ent[0];
@@ -216,23 +228,25 @@ struct F32Rec {
     }
 };
 
-template <bool GROUPS, int LANES = 1, bool INLINE = false>
+template <bool GROUPS, int LANES = 1, int REC = 0>
 __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const TileView &v, int l, const float4 &rm,
                                                   int n_own, int n_inc, V3<float> &s, int lane = 0,
                                                   float *dmin_out = nullptr, int tile = 0) {
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(v.bl + v.h->off_oo) + l;
-    F32Rec<INLINE> rec;
-    if constexpr (INLINE) {
+    F32Rec<REC> rec;
+    if constexpr (REC == 1) {
         const unsigned long long b0 = p.topo.kl_off[tile] + (unsigned long long)l;
         rec.kk = p.topo.kd_inline + b0;
         rec.g = p.topo.g_inline ? p.topo.g_inline + b0 : nullptr;
+    } else {
+        rec.dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);
+    }
+    if constexpr (REC != 0) {                               // the staged X0 planes
         rec.ns = kTile + (int)p.topo.max_halo;
         rec.sX0 = reinterpret_cast<const double *>(v.sY + rec.ns);
         rec.mx = rec.sX0[l];
         rec.my = rec.sX0[rec.ns + l];
         rec.mz = rec.sX0[2 * rec.ns + l];
-    } else {
-        rec.dict = reinterpret_cast<const float4 *>(v.bl + v.h->off_okl);
     }
     float dmin = INFINITY;
     auto body = [&](int q, float2 k2) {
@@ -252,7 +266,7 @@ __device__ __forceinline__ unsigned incidence_sum(const Params<float> &p, const 
         dmin = fminf(dmin, d2);                             // a degenerate reference is also degenerate at its owner
         acc3(s, c, dx, dy, dz_);
     };
-    if constexpr (INLINE) {
+    if constexpr (REC == 1) {
         // records streamed from HBM, software pipelined: the next group's
         // loads are in flight while this group computes
         constexpr int P = 4;
@@ -341,9 +355,9 @@ __device__ __forceinline__ void mbar_wait_warp0(uint64_t *bar, uint32_t phase) {
 // mass l = t mod 256 with lane t / 256 taking every other incidence, and the
 // lanes' sums meet in shared memory in a fixed order -- twice the warps for
 // the same tiles, for scenes too small to fill the GPU.
-template <int INTEG, bool GROUPS, int LANES = 1, bool ORDERED = false, bool INLINE = false>
+template <int INTEG, bool GROUPS, int LANES = 1, bool ORDERED = false, int REC = 0>
 __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char *smem) {
-    static_assert(!(INLINE && LANES > 1), "inline records step with one lane per mass");
+    static_assert(!(REC != 0 && LANES > 1), "records with the staged X0 step with one lane per mass");
     const Topology<float> &t = p.topo;
     const int tid = threadIdx.x;
     const int l = tid % kTile, lane = tid / kTile;
@@ -373,12 +387,12 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         bulk_copy(bl, t.blob + g0, split, bar);
         bulk_copy(bl + split, t.blob + g0 + split, bytes - split, bar + 1);
     }
-    // INLINE: the fp64 rest positions X0 of own and halo slots, as x, y, z
+    // REC != 0: the fp64 rest positions X0 of own and halo slots, as x, y, z
     // planes behind the staged displacements (rest vectors formed per
     // incidence); step-independent, so staged before the grid dependency
     const int ns = kTile + (int)t.max_halo;
     double *sX0 = reinterpret_cast<double *>(sR + ns);
-    if constexpr (INLINE) {
+    if constexpr (REC != 0) {
         if (active) {
             sX0[l] = __ldg(t.x0 + 3 * (long long)m);
             sX0[ns + l] = __ldg(t.x0 + 3 * (long long)m + 1);
@@ -446,7 +460,7 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
         if (p.debug != 1) {
             const uint16_t cnt = reinterpret_cast<const uint16_t *>(bl + v.h->off_cnt)[l];
             flush_degenerate(p.degenerate,
-                             incidence_sum<GROUPS, 1, INLINE>(p, v, l, x4, cnt & 0xff, cnt >> 8, s, 0, nullptr, tile));
+                             incidence_sum<GROUPS, 1, REC>(p, v, l, x4, cnt & 0xff, cnt >> 8, s, 0, nullptr, tile));
         }
     } else {
         // lane 1's partial sums (and its smallest d^2) meet lane 0's in shared
@@ -474,11 +488,11 @@ __device__ __forceinline__ void lean_body(const Params<float> &p, unsigned char 
     tile_epilogue<INTEG>(p, m, s, x4, hist, need_prev, tile);
 }
 
-template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1, bool ORDERED = false, bool INLINE = false>
+template <int INTEG, bool GROUPS, int MINB = 6, int LANES = 1, bool ORDERED = false, int REC = 0>
 __global__ void __launch_bounds__(kTile * LANES, LANES == 1 ? MINB : 3) tile_lean_kernel(Params<float> p) {
     extern __shared__ __align__(128) unsigned char smem[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    lean_body<INTEG, GROUPS, LANES, ORDERED, INLINE>(p, smem);
+    lean_body<INTEG, GROUPS, LANES, ORDERED, REC>(p, smem);
     xchg_finish(p, lean_tile<ORDERED>(p));
 }
 

@@ -125,6 +125,7 @@ struct TileLayout {
     std::vector<int8_t> g_inline;   // inline format: group per incidence (empty: no groups)
     std::vector<uint64_t> kl_off;   // inline format: n_tiles + 1 slot offsets (W * 256 per tile)
     std::vector<float> kd_inline;   // fp32 inline format: (k, k*l0) per incidence slot
+    bool dict_x0 = false;           // fp32 compact: dictionary of (k, k*l0, group), D formed from X0 (canonical bit 3)
     double halo_ratio = 0.0;        // mean (n + n_halo) / n
     double foreign_frac = 0.0;      // refs whose owner lies in another tile
 };

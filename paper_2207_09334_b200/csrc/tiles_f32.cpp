@@ -60,7 +60,10 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
     const bool explicit_only = env && std::strcmp(env, "explicit") == 0;
     const bool inline_only = env && !explicit_only && atoi(env) == 0;
     if (!explicit_only) {
+        // the D-keyed dictionary, then a (k, k*l0, group) dictionary with the
+        // rest vectors formed from X0 on the device, then inline records
         int rc = inline_only ? SS_EAGAIN_DICT : build_tiles_f32_fmt(in, L, 1);
+        if (rc == SS_EAGAIN_DICT && !inline_only) rc = build_tiles_f32_fmt(in, L, 3);
         if (rc == SS_EAGAIN_DICT) rc = build_tiles_f32_fmt(in, L, 2);
         if (rc != SS_EAGAIN_DICT && rc != SS_EAGAIN_SHAPE) return rc;
     }
@@ -68,7 +71,7 @@ int build_tiles_f32(const TileInput &in, TileLayout &L) {
 }
 
 int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
-    const bool use_dict = mode != 0, inline_rec = mode == 2;
+    const bool use_dict = mode != 0, inline_rec = mode == 2, dict_x0 = mode == 3;
     const int64_t N = in.N, S = in.S;
     if (N >= (1ll << 30) || S >= (1ll << 31)) return fail(SS_EINVAL, "scene too large for the tiled layout");
     L = TileLayout{};
@@ -245,6 +248,9 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
             std::map<Key, uint32_t> dict;
             auto key_of = [&](int32_t s, int64_t m) {
                 const int64_t o = (int64_t)in.si[s] + in.sj[s] - m;
+                if (dict_x0)                                  // D formed on the device from X0
+                    return std::make_tuple((float)in.k[s], (float)(in.k[s] * in.l0[s]),
+                                           has_g ? (int)in.group[s] : -1, 0.f, 0.f, 0.f);
                 return std::make_tuple((float)in.k[s], (float)(in.k[s] * in.l0[s]), has_g ? (int)in.group[s] : -1,
                                        (float)(in.x[3 * o] - in.x[3 * m]), (float)(in.x[3 * o + 1] - in.x[3 * m + 1]),
                                        (float)(in.x[3 * o + 2] - in.x[3 * m + 2]));
@@ -276,7 +282,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
             const uint32_t D = (uint32_t)dict.size(), inc_n = (uint32_t)Wi << 8;
             TileHdr h{};
             h.n = n; h.W = Wi; h.Wr = 0; h.n_halo = (uint32_t)halo_ids.size(); h.n_foreign = 0;
-            h.canonical = 1 | 2 | (inline_rec ? 4 : 0);       // bit 1: compact format; bit 2: inline records
+            h.canonical = 1 | 2 | (inline_rec ? 4 : 0) | (dict_x0 ? 8 : 0);   // bit 1: compact; 2: inline; 3: D from X0
             h.slice_log2 = 8;
             h.n_dict = D;
             uint32_t off = al16(sizeof(TileHdr));
@@ -408,6 +414,7 @@ int build_tiles_f32_fmt(const TileInput &in, TileLayout &L, int mode) {
     if (err == 3) return SS_EAGAIN_DICT;
     L.compact = use_dict;
     L.inline_kl = inline_rec;
+    L.dict_x0 = dict_x0;
     if (inline_rec) {
         L.kl_off.assign(n_tiles + 1, 0);
         for (int64_t t = 0; t < n_tiles; ++t) L.kl_off[t + 1] = L.kl_off[t] + tKD[t].size() / 2;

@@ -272,6 +272,34 @@ def test_fp32_inline_rest_vectors_equal_the_dictionary(integrator, monkeypatch):
     assert inl.forces(xp, scene.v, 0.0).tobytes() == comp.forces(xp, scene.v, 0.0).tobytes()
 
 
+@pytest.mark.parametrize("integrator", ["verlet", "rk4"])
+def test_fp32_dictionary_with_rest_vectors_from_x0(integrator, monkeypatch):
+    """Walkers jittered in place (positions off the lattice, shared materials):
+    a rest-vector-keyed dictionary overflows, a (k, k*l0, group) one does not
+    (tile_kernel 7: D formed from the staged X0).  Same D and the same order as
+    the inline records, so the two formats agree bit for bit; within the fp32
+    tolerance of the fp64 engine over 2000 steps (groups and contact)."""
+    from paper_2207_09334_b200 import crawler_scene, replicate
+    batch = replicate(crawler_scene(), 96, jitter=1e-6, seed=3)
+    monkeypatch.setenv("SS_RESIDENT", "0")
+    x0 = Engine(batch, integrator=integrator, precision="f32")
+    monkeypatch.setenv("SS_TILE_DICT", "0")
+    inl = Engine(batch, integrator=integrator, precision="f32")
+    monkeypatch.delenv("SS_TILE_DICT")
+    assert x0.info()["tile_kernel"] == 7 and inl.info()["tile_kernel"] == 6
+    x0.step(100)
+    inl.step(100)
+    assert x0.x.tobytes() == inl.x.tobytes() and x0.v.tobytes() == inl.v.tobytes()
+    rng = np.random.default_rng(9)
+    xp = batch.x + 1e-3 * rng.standard_normal(batch.x.shape)
+    assert x0.forces(xp, batch.v, 0.0).tobytes() == inl.forces(xp, batch.v, 0.0).tobytes()
+    e64 = Engine(batch, integrator=integrator, precision="f64")
+    e64.step(2000 if integrator == "verlet" else 500)
+    x0.step(1900 if integrator == "verlet" else 400)
+    span = np.abs(e64.x - batch.x).max()
+    assert np.abs(x0.x - e64.x).max() <= 1e-3 * span
+
+
 @pytest.mark.parametrize("lanes", ["1", "2"])
 def test_degenerate_springs_in_tiled_fp32(lanes, monkeypatch):
     """Coincident endpoints in a multi-tile fp32 scene: the spring is skipped

@@ -172,6 +172,12 @@ def test_fp64_compact_tile_plan_on_host(monkeypatch):
     assert plan(cube, precision="f32")["tile_kernel"] == 2
     f32i = plan(rnd, precision="f32")
     assert f32i["tile_kernel"] == 6 and f32i["tile_blob_bytes"] >= 8 * 2 * rnd.spring_count   # (k, k*l0)
+    # positions off the lattice, materials shared: the (k, k*l0, group)
+    # dictionary with rest vectors formed from X0 (7); fp64 keys never held D
+    from paper_2207_09334_b200 import crawler_scene, replicate
+    pop = replicate(crawler_scene(), 96, jitter=1e-6, seed=3)
+    assert plan(pop, precision="f32")["tile_kernel"] == 7
+    assert plan(pop, precision="f64")["tile_kernel"] == 3
 
 
 def test_engine_without_gpu_fails_loudly():
